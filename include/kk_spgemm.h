@@ -1,0 +1,156 @@
+/*
+ * kk_spgemm.h -- C ABI of the B200 two-phase hash SpGEMM, C = A * B on CSR matrices.
+ *
+ * The calls follow the paper's statement of the two-phase protocol
+ * (Sec. 2.2.1):
+ *   "we first allocate the row pointers of C"            -> caller allocates c_row_map
+ *   "We may compress B into B_C"                          -> inside kk_spgemm_symbolic
+ *   "perform the symbolic phase on A and B_C to fill the row pointers array"
+ *                                                         -> kk_spgemm_symbolic
+ *   "The last entry of the row pointers array amounts to ... nnz(C)"
+ *                                                         -> *c_nnz (host) on return
+ *   "Then we allocate two more arrays ... of size nnz(C)" -> caller allocates entries/values
+ *   "Finally, we perform the numeric phase"               -> kk_spgemm_numeric
+ * and the kernel handle of PAPER.md:708-712 (Sec. 6: variant choice and symbolic
+ * state carried between the phases).
+ *
+ * Conventions (all functions):
+ *   - Matrix arrays (row_map, entries, values) are DEVICE pointers on the handle's
+ *     device.  The library never takes ownership of them.
+ *   - row_map has nrows+1 entries of `offset_type` (int32 or int64); A, B and C use
+ *     the same offset type.  entries are int32 column indices.  values are float
+ *     or double, the same type for A, B and C.  Rows may be unsorted and may hold
+ *     duplicate columns (duplicates are summed).
+ *   - C's pattern is the structural product: an entry exists wherever a stored
+ *     A(i,j) meets a stored B(j,c), whatever the value (cancelled zeros are kept).
+ *   - All device work is enqueued on `stream` (a cudaStream_t, 0 = legacy default).
+ *     kk_spgemm_symbolic synchronises `stream` once, to return nnz(C) to the host.
+ *     kk_spgemm_numeric is fully asynchronous.
+ *   - Errors are returned as kk_status_t; nothing is thrown across the ABI.  On an
+ *     error, kk_last_error_detail() gives a one-line description.
+ *   - A handle is not thread-safe; distinct handles are independent.
+ */
+#ifndef KK_SPGEMM_H
+#define KK_SPGEMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    KK_OK = 0,
+    KK_ERR_INVALID_ARG = 1,      /* null pointer, negative size, bad option value */
+    KK_ERR_DIM_MISMATCH = 2,     /* A.ncols != B.nrows */
+    KK_ERR_UNSUPPORTED_TYPE = 3, /* mixed offset or value types */
+    KK_ERR_INDEX_OVERFLOW = 4,   /* nnz(C) > INT32_MAX with int32 offsets; or column index
+                                    out of range when opts.validate = 1 */
+    KK_ERR_STALE_HANDLE = 5,     /* numeric called without a matching symbolic */
+    KK_ERR_OUT_OF_MEMORY = 6,    /* workspace allocation failed */
+    KK_ERR_CUDA = 7              /* CUDA launch or runtime error */
+} kk_status_t;
+
+typedef enum { KK_I32 = 0, KK_I64 = 1 } kk_index_t;
+typedef enum { KK_F32 = 0, KK_F64 = 1 } kk_scalar_t;
+
+/* A CSR matrix ("CrsMatrix" / "StaticCrsGraph"); device pointers. */
+typedef struct {
+    int64_t nrows;
+    int64_t ncols;
+    int64_t nnz;              /* = row_map[nrows] */
+    kk_index_t offset_type;   /* type of row_map */
+    kk_scalar_t value_type;   /* type of values */
+    const void* row_map;      /* nrows+1 offsets */
+    const int32_t* entries;   /* nnz column indices */
+    const void* values;       /* nnz values (may be NULL for symbolic-only use) */
+} kk_csr_t;
+
+typedef struct kk_spgemm_handle_s* kk_spgemm_handle_t;
+
+/* Workspace allocator: alloc(bytes, stream, ctx) returns device memory usable on
+ * `stream`; free(ptr, bytes, stream, ctx) releases it.  NULL = cudaMallocAsync /
+ * cudaFreeAsync.  The handle grows its workspace monotonically and frees it in
+ * kk_spgemm_destroy. */
+typedef void* (*kk_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*kk_free_fn)(void* ptr, size_t bytes, void* stream, void* ctx);
+
+typedef struct {
+    int sort_rows;     /* 1 (default): C rows sorted by column; 0: any order within a row */
+    int compression;   /* -1 (default) auto, 0 off, 1 on: compress B into B_C */
+    int validate;      /* 1: check column indices of A and B are in range (error otherwise) */
+    int num_streams;   /* internal streams used to overlap work bins (default 2, 1 = none) */
+    kk_alloc_fn alloc;
+    kk_free_fn free;
+    void* alloc_ctx;
+} kk_spgemm_opts_t;
+
+typedef struct {
+    int64_t muladds;          /* sum_i sum_{j in A(i,:)} nnz(B(j,:)) */
+    int64_t nnz_c;            /* row_map[m] of the last symbolic */
+    int64_t compressed_words; /* |B_C| (0 when compression was not used) */
+    int compression_used;     /* 1 if the last symbolic ran on B_C */
+    int b_sorted;             /* 1 if every row of B was non-decreasing */
+    int b_strict;             /* 1 if every row of B was strictly increasing */
+    int num_symbolic_bins;
+    int num_numeric_bins;
+    int64_t symbolic_bin_rows[16]; /* rows per symbolic work bin */
+    int64_t numeric_bin_rows[16];  /* rows per numeric work bin */
+    int64_t kernel_launches;  /* total kernels this handle launched since creation */
+    int64_t workspace_bytes;  /* bytes currently held */
+} kk_spgemm_stats_t;
+
+/* Fill *opts with the defaults listed above. */
+void kk_spgemm_opts_default(kk_spgemm_opts_t* opts);
+
+/* Create a handle on CUDA device `device` (>= 0).  opts may be NULL (defaults). */
+kk_status_t kk_spgemm_create(kk_spgemm_handle_t* handle, int device, const kk_spgemm_opts_t* opts);
+
+/* Release the handle and its workspace (after synchronising its device work). */
+kk_status_t kk_spgemm_destroy(kk_spgemm_handle_t handle);
+
+/* Step a1+a2 (per-row FLOPs, parallel prefix sum):
+ * flops[i] = sum_{j in A(i,:)} nnz(B(j,:)) (device, m int64, may be NULL);
+ * flops_scan = exclusive prefix of flops (device, m+1 int64, may be NULL);
+ * *total (host, may be NULL) = flops_scan[m] -- synchronises `stream` when non-NULL.
+ * Used for flop-balanced row partitioning across GPUs. */
+kk_status_t kk_spgemm_row_flops(kk_spgemm_handle_t handle, const kk_csr_t* A, const kk_csr_t* B,
+                                int64_t* flops, int64_t* flops_scan, int64_t* total, void* stream);
+
+/* Step a4 ("compress B into B_C by representing the column indices by
+ * bits"): for each row j of B, writes len[j] (device, n int32) pairs
+ * (word = col >> 5, mask = OR of 1 << (col & 31)) at pairs[B.row_map[j] ...]
+ * (device, capacity nnz(B) uint64, word in the low 32 bits, mask in the high 32).
+ * Adjacent equal words are merged; on sorted rows this is the canonical form
+ * (distinct increasing words).  Exposed for tests; symbolic calls it internally. */
+kk_status_t kk_spgemm_compress(kk_spgemm_handle_t handle, const kk_csr_t* B, int32_t* len, uint64_t* pairs,
+                               void* stream);
+
+/* Symbolic phase: fills c_row_map (device, A.nrows+1 entries of
+ * A.offset_type, caller-allocated) with the row pointers of C and returns nnz(C) in
+ * *c_nnz (host).  Runs flop count, scan, binning, compression and the per-bin
+ * symbolic kernels; the handle keeps the row bins for the numeric phase. */
+kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t handle, const kk_csr_t* A, const kk_csr_t* B,
+                               void* c_row_map, int64_t* c_nnz, void* stream);
+
+/* Numeric phase (Eq. (1) at PAPER.md:160-163): writes the column
+ * indices (c_entries, device, nnz(C) int32) and values (c_values, device, nnz(C) of
+ * A.value_type) of C.  c_row_map must be the array filled by the last symbolic call
+ * on the same A/B patterns (same sizes, pointers and types), else
+ * KK_ERR_STALE_HANDLE.  The values of A and B may change between calls
+ * (symbolic reuse). */
+kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t handle, const kk_csr_t* A, const kk_csr_t* B,
+                              const void* c_row_map, int32_t* c_entries, void* c_values, void* stream);
+
+/* Statistics of the last symbolic/numeric pair. */
+kk_status_t kk_spgemm_stats(kk_spgemm_handle_t handle, kk_spgemm_stats_t* stats);
+
+const char* kk_status_string(kk_status_t status);
+const char* kk_last_error_detail(kk_spgemm_handle_t handle);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KK_SPGEMM_H */

@@ -1,0 +1,476 @@
+// kk_api.cu -- C ABI (include/kk_spgemm.h): handle, workspace, phase orchestration.
+//
+// Symbolic: init status -> a4 check/compress B -> a1 row flops + bins
+// -> a2 scan of flops -> a3 stable binning -> a5 per-bin symbolic kernels -> a6 scan of
+// counts into the caller's row map -> numeric bins from exact counts -> ONE device->host
+// copy of the status block + stream sync (nnz(C) must reach the host before C's arrays
+// can be allocated).
+// Numeric: per-bin numeric kernels with the fused sort; asynchronous.
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/kk_spgemm.h"
+#include "kk_internal.cuh"
+
+using kk::DevStatus;
+using kk::MatView;
+
+namespace {
+
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct kk_spgemm_handle_s {
+    int device = 0;
+    int num_sms = 148;
+    kk_spgemm_opts_t opts;
+    std::string err;
+    long long launches = 0;
+    // workspace
+    Buf flops, fscan, binid, perm_sym, perm_num, counts, binscratch, binstart, bc_len, pairs, cursors, partial,
+        status;
+    DevStatus* h_status = nullptr;  // pinned
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // record of the last symbolic (stale-handle check)
+    struct Rec {
+        bool valid = false;
+        int64_t m = 0, n = 0, k = 0, nnzA = 0, nnzB = 0, nnzC = 0;
+        const void *arm = nullptr, *aent = nullptr, *brm = nullptr, *bent = nullptr, *crm = nullptr;
+        int offt = 0;
+    } rec;
+    int host_num_bin_start[kk::NB + 1] = {0};
+    kk_spgemm_stats_t stats;
+};
+
+static kk_status_t fail(kk_spgemm_handle_t h, kk_status_t s, const char* fmt, ...) {
+    if (h) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof(buf), fmt, ap);
+        va_end(ap);
+        h->err = buf;
+    }
+    return s;
+}
+
+static kk_status_t cuda_check(kk_spgemm_handle_t h, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return KK_OK;
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) return fail(h, KK_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+    return fail(h, KK_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static kk_status_t ensure(kk_spgemm_handle_t h, Buf& b, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return KK_OK;
+    bytes = bytes + bytes / 8 + 256;
+    if (b.p) {
+        if (h->opts.free)
+            h->opts.free(b.p, b.bytes, s, h->opts.alloc_ctx);
+        else
+            cudaFreeAsync(b.p, s);
+        b.p = nullptr;
+        b.bytes = 0;
+    }
+    void* p = nullptr;
+    if (h->opts.alloc) {
+        p = h->opts.alloc(bytes, s, h->opts.alloc_ctx);
+        if (!p) return fail(h, KK_ERR_OUT_OF_MEMORY, "workspace allocation of %zu bytes failed", bytes);
+    } else {
+        cudaError_t e = cudaMallocAsync(&p, bytes, s);
+        if (e != cudaSuccess) return cuda_check(h, e, "cudaMallocAsync(workspace)");
+    }
+    b.p = p;
+    b.bytes = bytes;
+    return KK_OK;
+}
+
+static void release(kk_spgemm_handle_t h, Buf& b) {
+    if (!b.p) return;
+    if (h->opts.free)
+        h->opts.free(b.p, b.bytes, nullptr, h->opts.alloc_ctx);
+    else
+        cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
+static kk_status_t check_csr(kk_spgemm_handle_t h, const kk_csr_t* M, const char* name, bool need_values) {
+    if (!M) return fail(h, KK_ERR_INVALID_ARG, "%s is NULL", name);
+    if (M->nrows < 0 || M->ncols < 0 || M->nnz < 0)
+        return fail(h, KK_ERR_INVALID_ARG, "%s has a negative size", name);
+    if (M->nrows >= INT32_MAX || M->ncols >= INT32_MAX)
+        return fail(h, KK_ERR_INVALID_ARG, "%s: dimensions must be < 2^31", name);
+    if (M->offset_type != KK_I32 && M->offset_type != KK_I64)
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE, "%s: bad offset_type", name);
+    if (M->value_type != KK_F32 && M->value_type != KK_F64)
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE, "%s: bad value_type", name);
+    if (!M->row_map) return fail(h, KK_ERR_INVALID_ARG, "%s.row_map is NULL", name);
+    if (M->nnz > 0 && !M->entries) return fail(h, KK_ERR_INVALID_ARG, "%s.entries is NULL", name);
+    if (need_values && M->nnz > 0 && !M->values) return fail(h, KK_ERR_INVALID_ARG, "%s.values is NULL", name);
+    if (M->offset_type == KK_I32 && M->nnz > INT32_MAX)
+        return fail(h, KK_ERR_INDEX_OVERFLOW, "%s: nnz exceeds int32 offsets", name);
+    return KK_OK;
+}
+
+static kk_status_t check_pair(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, bool need_values) {
+    kk_status_t s;
+    if ((s = check_csr(h, A, "A", need_values)) != KK_OK) return s;
+    if ((s = check_csr(h, B, "B", need_values)) != KK_OK) return s;
+    if (A->ncols != B->nrows)
+        return fail(h, KK_ERR_DIM_MISMATCH, "A.ncols (%lld) != B.nrows (%lld)", (long long)A->ncols,
+                    (long long)B->nrows);
+    if (A->offset_type != B->offset_type)
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE, "A and B must use the same offset type");
+    if (need_values && A->value_type != B->value_type)
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE, "A and B must use the same value type");
+    return KK_OK;
+}
+
+static MatView view(const kk_csr_t* M) {
+    MatView v;
+    v.nrows = M->nrows;
+    v.ncols = M->ncols;
+    v.nnz = M->nnz;
+    v.row_map = M->row_map;
+    v.entries = M->entries;
+    v.values = M->values;
+    return v;
+}
+
+static int pick_logG(double avg) {
+    // lanes per B row: smallest power of two >= 0.75 * average row length, in [4, 32]
+    double want = avg * 0.75;
+    int lg = 2;
+    while (lg < 5 && (double)(1 << lg) < want) ++lg;
+    return lg;
+}
+
+extern "C" {
+
+void kk_spgemm_opts_default(kk_spgemm_opts_t* o) {
+    if (!o) return;
+    memset(o, 0, sizeof(*o));
+    o->sort_rows = 1;
+    o->compression = -1;
+    o->validate = 0;
+    o->num_streams = 2;
+}
+
+const char* kk_status_string(kk_status_t s) {
+    switch (s) {
+        case KK_OK: return "KK_OK";
+        case KK_ERR_INVALID_ARG: return "KK_ERR_INVALID_ARG";
+        case KK_ERR_DIM_MISMATCH: return "KK_ERR_DIM_MISMATCH";
+        case KK_ERR_UNSUPPORTED_TYPE: return "KK_ERR_UNSUPPORTED_TYPE";
+        case KK_ERR_INDEX_OVERFLOW: return "KK_ERR_INDEX_OVERFLOW";
+        case KK_ERR_STALE_HANDLE: return "KK_ERR_STALE_HANDLE";
+        case KK_ERR_OUT_OF_MEMORY: return "KK_ERR_OUT_OF_MEMORY";
+        case KK_ERR_CUDA: return "KK_ERR_CUDA";
+    }
+    return "KK_ERR_UNKNOWN";
+}
+
+const char* kk_last_error_detail(kk_spgemm_handle_t h) { return h ? h->err.c_str() : "null handle"; }
+
+kk_status_t kk_spgemm_create(kk_spgemm_handle_t* out, int device, const kk_spgemm_opts_t* opts) {
+    if (!out) return KK_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (device < 0) return KK_ERR_INVALID_ARG;
+    kk_spgemm_opts_t o;
+    kk_spgemm_opts_default(&o);
+    if (opts) o = *opts;
+    if (o.compression < -1 || o.compression > 1) return KK_ERR_INVALID_ARG;
+    if ((o.alloc == nullptr) != (o.free == nullptr)) return KK_ERR_INVALID_ARG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) {
+        cudaGetLastError();
+        return KK_ERR_CUDA;
+    }
+    cudaSetDevice(device);
+    kk_spgemm_handle_t h = new kk_spgemm_handle_s();
+    h->device = device;
+    h->opts = o;
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMallocHost((void**)&h->h_status, sizeof(DevStatus)) != cudaSuccess) {
+        cudaGetLastError();
+        delete h;
+        return KK_ERR_OUT_OF_MEMORY;
+    }
+    memset(h->h_status, 0, sizeof(DevStatus));
+    if (o.num_streams > 1) {
+        cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+    }
+    memset(&h->stats, 0, sizeof(h->stats));
+    *out = h;
+    return KK_OK;
+}
+
+kk_status_t kk_spgemm_destroy(kk_spgemm_handle_t h) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    Buf* bufs[] = {&h->flops, &h->fscan, &h->binid, &h->perm_sym, &h->perm_num, &h->counts, &h->binscratch,
+                   &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status};
+    for (Buf* b : bufs) release(h, *b);
+    if (h->h_status) cudaFreeHost(h->h_status);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
+    cudaGetLastError();
+    delete h;
+    return KK_OK;
+}
+
+static kk::Launch make_launch(kk_spgemm_handle_t h, cudaStream_t s) {
+    kk::Launch L;
+    L.stream = s;
+    L.num_sms = h->num_sms;
+    L.launches = &h->launches;
+    return L;
+}
+
+kk_status_t kk_spgemm_compress(kk_spgemm_handle_t h, const kk_csr_t* B, int32_t* len, uint64_t* pairs,
+                               void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    kk_status_t st;
+    if ((st = check_csr(h, B, "B", false)) != KK_OK) return st;
+    if (B->nrows > 0 && !len) return fail(h, KK_ERR_INVALID_ARG, "len is NULL");
+    if (B->nnz > 0 && !pairs) return fail(h, KK_ERR_INVALID_ARG, "pairs is NULL");
+    cudaSetDevice(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    if ((st = ensure(h, h->status, sizeof(DevStatus), s)) != KK_OK) return st;
+    kk::Launch L = make_launch(h, s);
+    DevStatus* dst = (DevStatus*)h->status.p;
+    kk::init_status(L, dst);
+    kk::check_compress(L, B->offset_type == KK_I64, view(B), B->ncols, true, h->opts.validate != 0, len,
+                       (uint2*)pairs, dst);
+    return cuda_check(h, cudaGetLastError(), "kk_spgemm_compress launch");
+}
+
+kk_status_t kk_spgemm_row_flops(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, int64_t* flops,
+                                int64_t* flops_scan, int64_t* total, void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    kk_status_t st;
+    if ((st = check_pair(h, A, B, false)) != KK_OK) return st;
+    cudaSetDevice(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t m = A->nrows;
+    const bool off64 = A->offset_type == KK_I64;
+    if ((st = ensure(h, h->status, sizeof(DevStatus), s)) != KK_OK) return st;
+    if ((st = ensure(h, h->binid, (size_t)m, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->counts, (size_t)m * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->partial, (size_t)kk::scan_partial_len(m) * 8, s)) != KK_OK) return st;
+    int64_t* f = flops;
+    if (!f) {
+        if ((st = ensure(h, h->flops, (size_t)m * 8, s)) != KK_OK) return st;
+        f = (int64_t*)h->flops.p;
+    }
+    kk::Launch L = make_launch(h, s);
+    DevStatus* dst = (DevStatus*)h->status.p;
+    kk::init_status(L, dst);
+    kk::row_flops_bin(L, off64, view(A), view(B), B->ncols, 0, h->opts.validate != 0, nullptr, f,
+                      (uint8_t*)h->binid.p, (int32_t*)h->counts.p, dst);
+    if (flops_scan) kk::exclusive_scan(L, true, f, true, flops_scan, m, (int64_t*)h->partial.p, nullptr, nullptr);
+    if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_row_flops launch")) != KK_OK) return st;
+    if (total) {
+        cudaMemcpyAsync(h->h_status, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
+        if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_row_flops sync")) != KK_OK) return st;
+        if (h->opts.validate && h->h_status->bad_index)
+            return fail(h, KK_ERR_INDEX_OVERFLOW, "column index of A out of range");
+        *total = (int64_t)h->h_status->total_flops;
+    }
+    return KK_OK;
+}
+
+kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, void* c_row_map,
+                               int64_t* c_nnz, void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    h->rec.valid = false;
+    kk_status_t st;
+    if ((st = check_pair(h, A, B, false)) != KK_OK) return st;
+    if (!c_row_map) return fail(h, KK_ERR_INVALID_ARG, "c_row_map is NULL");
+    if (!c_nnz) return fail(h, KK_ERR_INVALID_ARG, "c_nnz is NULL");
+    cudaSetDevice(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t m = A->nrows, n = B->nrows, k = B->ncols;
+    const bool off64 = A->offset_type == KK_I64;
+    const int comp_mode = h->opts.compression;
+    // workspace
+    if ((st = ensure(h, h->status, sizeof(DevStatus), s)) != KK_OK) return st;
+    if ((st = ensure(h, h->flops, (size_t)m * 8, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->fscan, (size_t)(m + 1) * 8, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->binid, (size_t)m, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->perm_sym, (size_t)m * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->perm_num, (size_t)m * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->counts, (size_t)m * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->binscratch, (size_t)kk::bin_scratch_len(m) * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->binstart, sizeof(int) * 2 * (kk::NB + 1), s)) != KK_OK) return st;
+    if ((st = ensure(h, h->partial, (size_t)kk::scan_partial_len(m) * 8, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->cursors, (size_t)A->nnz * 4, s)) != KK_OK) return st;
+    if (comp_mode != 0) {
+        if ((st = ensure(h, h->bc_len, (size_t)n * 4, s)) != KK_OK) return st;
+        if ((st = ensure(h, h->pairs, (size_t)B->nnz * 8, s)) != KK_OK) return st;
+    }
+    DevStatus* dst = (DevStatus*)h->status.p;
+    int* sym_start = (int*)h->binstart.p;
+    int* num_start = sym_start + (kk::NB + 1);
+    kk::Launch L = make_launch(h, s);
+    const MatView Av = view(A), Bv = view(B);
+
+    kk::init_status(L, dst);
+    // a4: sortedness flags (+ B_C unless compression is off)
+    kk::check_compress(L, off64, Bv, k, comp_mode != 0, h->opts.validate != 0, (int32_t*)h->bc_len.p,
+                       (uint2*)h->pairs.p, dst);
+    // a1: flops per row, symbolic bins
+    kk::row_flops_bin(L, off64, Av, Bv, k, comp_mode, h->opts.validate != 0, (const int32_t*)h->bc_len.p,
+                      (int64_t*)h->flops.p, (uint8_t*)h->binid.p, (int32_t*)h->counts.p, dst);
+    // a2: F = exclusive scan of flops (kept in the handle for flop-balanced partitioning)
+    kk::exclusive_scan(L, true, h->flops.p, true, h->fscan.p, m, (int64_t*)h->partial.p, nullptr, nullptr);
+    // a3: bin rows by symbolic work
+    kk::bin_rows(L, m, (const uint8_t*)h->binid.p, (int32_t*)h->binscratch.p, (int32_t*)h->perm_sym.p, sym_start);
+    // a5: symbolic kernels per bin (dense bin on the side stream)
+    kk::SymArgs sa;
+    sa.off64 = off64;
+    sa.A = Av;
+    sa.B = Bv;
+    sa.k = k;
+    sa.bc_len = (const int32_t*)h->bc_len.p;
+    sa.pairs = (const uint2*)h->pairs.p;
+    sa.perm = (const int32_t*)h->perm_sym.p;
+    sa.bin_start = sym_start;
+    sa.counts = (int32_t*)h->counts.p;
+    sa.cursors = (int32_t*)h->cursors.p;
+    sa.st = dst;
+    sa.logG = pick_logG(n > 0 ? (double)B->nnz / (double)n / (comp_mode != 0 ? 2.0 : 1.0) : 1.0);
+    cudaStream_t side = nullptr;
+    if (h->side) {
+        cudaEventRecord(h->ev_fork, s);
+        cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+        side = h->side;
+    }
+    kk::symbolic_bins(L, sa, side);
+    if (side) {
+        cudaEventRecord(h->ev_join, side);
+        cudaStreamWaitEvent(s, h->ev_join, 0);
+    }
+    // a6: row map of C = exclusive scan of counts (overflow check for int32 offsets)
+    kk::exclusive_scan(L, false, h->counts.p, off64, c_row_map, m, (int64_t*)h->partial.p, &dst->nnz_c,
+                       &dst->overflow);
+    // numeric bins from exact counts
+    kk::numeric_binid(L, m, (const int32_t*)h->counts.p, (uint8_t*)h->binid.p);
+    kk::bin_rows(L, m, (const uint8_t*)h->binid.p, (int32_t*)h->binscratch.p, (int32_t*)h->perm_num.p, num_start);
+    // copy bin starts next to the status block, then the single device->host read
+    cudaMemcpyAsync(dst->sym_bin_start, sym_start, sizeof(int) * (kk::NB + 1), cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(dst->num_bin_start, num_start, sizeof(int) * (kk::NB + 1), cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(h->h_status, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
+    if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_symbolic launch")) != KK_OK) return st;
+    if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_symbolic sync")) != KK_OK) return st;
+    const DevStatus& hs = *h->h_status;
+    if (h->opts.validate && hs.bad_index) return fail(h, KK_ERR_INDEX_OVERFLOW, "column index out of range");
+    if (hs.overflow)
+        return fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) = %llu exceeds int32 row offsets; use KK_I64",
+                    (unsigned long long)hs.nnz_c);
+    *c_nnz = (int64_t)hs.nnz_c;
+    // record for numeric
+    h->rec.valid = true;
+    h->rec.m = m;
+    h->rec.n = n;
+    h->rec.k = k;
+    h->rec.nnzA = A->nnz;
+    h->rec.nnzB = B->nnz;
+    h->rec.nnzC = (int64_t)hs.nnz_c;
+    h->rec.arm = A->row_map;
+    h->rec.aent = A->entries;
+    h->rec.brm = B->row_map;
+    h->rec.bent = B->entries;
+    h->rec.crm = c_row_map;
+    h->rec.offt = (int)A->offset_type;
+    memcpy(h->host_num_bin_start, hs.num_bin_start, sizeof(h->host_num_bin_start));
+    // stats
+    kk_spgemm_stats_t& S = h->stats;
+    S.muladds = (int64_t)hs.total_flops;
+    S.nnz_c = (int64_t)hs.nnz_c;
+    S.compression_used = hs.use_comp;
+    S.compressed_words = hs.use_comp ? (int64_t)hs.total_words : 0;
+    S.b_sorted = hs.b_sorted;
+    S.b_strict = hs.b_strict;
+    S.num_symbolic_bins = kk::SYM_NBINS;
+    S.num_numeric_bins = kk::NUM_NBINS;
+    for (int b = 0; b < 16; ++b) {
+        S.symbolic_bin_rows[b] = b < kk::NB ? hs.sym_bin_start[b + 1] - hs.sym_bin_start[b] : 0;
+        S.numeric_bin_rows[b] = b < kk::NB ? hs.num_bin_start[b + 1] - hs.num_bin_start[b] : 0;
+    }
+    return KK_OK;
+}
+
+kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, const void* c_row_map,
+                              int32_t* c_entries, void* c_values, void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    kk_status_t st;
+    if ((st = check_pair(h, A, B, true)) != KK_OK) return st;
+    const auto& R = h->rec;
+    if (!R.valid || R.m != A->nrows || R.n != B->nrows || R.k != B->ncols || R.nnzA != A->nnz ||
+        R.nnzB != B->nnz || R.arm != A->row_map || R.aent != A->entries || R.brm != B->row_map ||
+        R.bent != B->entries || R.crm != c_row_map || R.offt != (int)A->offset_type)
+        return fail(h, KK_ERR_STALE_HANDLE, "numeric: no matching symbolic for these matrices / row map");
+    if (R.nnzC > 0 && (!c_entries || !c_values)) return fail(h, KK_ERR_INVALID_ARG, "c_entries/c_values is NULL");
+    cudaSetDevice(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    kk::Launch L = make_launch(h, s);
+    kk::NumArgs na;
+    na.off64 = A->offset_type == KK_I64;
+    na.f64 = A->value_type == KK_F64;
+    na.sort = h->opts.sort_rows != 0;
+    na.A = view(A);
+    na.B = view(B);
+    na.k = B->ncols;
+    na.c_row_map = c_row_map;
+    na.c_entries = c_entries;
+    na.c_values = c_values;
+    na.perm = (const int32_t*)h->perm_num.p;
+    na.bin_start = (const int*)h->binstart.p + (kk::NB + 1);
+    na.host_bin_start = h->host_num_bin_start;
+    na.cursors = (int32_t*)h->cursors.p;
+    na.st = (const DevStatus*)h->status.p;
+    na.logG = pick_logG(B->nrows > 0 ? (double)B->nnz / (double)B->nrows : 1.0);
+    cudaStream_t side = nullptr;
+    const bool dense = h->host_num_bin_start[kk::NUM_DENSE_BIN + 1] > h->host_num_bin_start[kk::NUM_DENSE_BIN];
+    if (h->side && dense) {
+        cudaEventRecord(h->ev_fork, s);
+        cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+        side = h->side;
+    }
+    kk::numeric_bins(L, na, side);
+    if (side) {
+        cudaEventRecord(h->ev_join, side);
+        cudaStreamWaitEvent(s, h->ev_join, 0);
+    }
+    return cuda_check(h, cudaGetLastError(), "kk_spgemm_numeric launch");
+}
+
+kk_status_t kk_spgemm_stats(kk_spgemm_handle_t h, kk_spgemm_stats_t* out) {
+    if (!h || !out) return KK_ERR_INVALID_ARG;
+    *out = h->stats;
+    out->kernel_launches = h->launches;
+    int64_t ws = 0;
+    const Buf* bufs[] = {&h->flops, &h->fscan, &h->binid, &h->perm_sym, &h->perm_num, &h->counts, &h->binscratch,
+                         &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status};
+    for (const Buf* b : bufs) ws += (int64_t)b->bytes;
+    out->workspace_bytes = ws;
+    return KK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// kk_internal.cuh -- internal declarations shared by kk_kernels.cu and kk_api.cu.
+//
+// Product code only: nothing here is shared with oracle/ (DESIGN.md "Boundary").
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kk {
+
+constexpr int NB = 16;                       // max work bins per phase
+constexpr uint32_t EMPTY = 0xffffffffu;      // empty hash slot (column indices are < 2^31)
+
+// Symbolic bins (by an upper bound ub_i of distinct keys of row i):
+//   0: ub = 0 (empty row, no kernel); b = 1..7: warp-owned shared hash with S = 32 << b
+//   slots (ub <= S); 8: CTA-owned dense bit-vector window.
+constexpr int SYM_WARP_BINS = 7;
+constexpr int SYM_DENSE_BIN = 8;
+constexpr int SYM_NBINS = 9;
+// Numeric bins (by exact nnz(C_i)):
+//   0: empty; b = 1..5: warp-owned shared hash with S = 32 << b slots (nnz <= S/2);
+//   6: CTA-owned dense scalar window (column-windowed dense accumulator).
+constexpr int NUM_WARP_BINS = 5;
+constexpr int NUM_DENSE_BIN = 6;
+constexpr int NUM_NBINS = 7;
+
+// Device-side status block.  Written by the kernels, copied to pinned host memory
+// once at the end of the symbolic phase (the phase's only device->host sync).
+struct DevStatus {
+    unsigned long long total_flops;   // sum_i flops_i
+    unsigned long long total_words;   // |B_C| (pairs written by compression)
+    unsigned long long nnz_c;         // row_map[m]
+    int b_sorted;                     // every B row non-decreasing
+    int b_strict;                     // every B row strictly increasing
+    int bad_index;                    // validate: a column index out of range
+    int overflow;                     // int32 row map cannot hold nnz(C)
+    int use_comp;                     // symbolic ran on B_C
+    int pad;
+    int sym_bin_start[NB + 1];        // row ranges of the symbolic bins in perm_sym
+    int num_bin_start[NB + 1];        // row ranges of the numeric bins in perm_num
+};
+
+struct MatView {
+    int64_t nrows, ncols, nnz;
+    const void* row_map;
+    const int32_t* entries;
+    const void* values;
+};
+
+struct Launch {
+    cudaStream_t stream;
+    int num_sms;
+    long long* launches;   // incremented once per kernel launch
+};
+
+// ---- host launchers (kk_kernels.cu) -------------------------------------------------
+void init_status(Launch& L, DevStatus* st);
+void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_comp, bool validate,
+                    int32_t* bc_len, uint2* pairs, DevStatus* st);
+void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, int64_t k, int comp_mode,
+                   bool validate, const int32_t* bc_len, int64_t* flops, uint8_t* binid, int32_t* counts,
+                   DevStatus* st);
+// exclusive scan of in[0..m) (int32 or int64) into out[0..m] (int32 or int64);
+// *total_dst (device, may be null) receives the sum; *overflow set when out is
+// int32 and the sum exceeds INT32_MAX.  partial: >= scan_partial_len(m) int64.
+int64_t scan_partial_len(int64_t m);
+void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out, int64_t m, int64_t* partial,
+                    unsigned long long* total_dst, int* overflow);
+void numeric_binid(Launch& L, int64_t m, const int32_t* counts, uint8_t* binid);
+// stable binning of rows by binid: perm lists rows of bin 0, then bin 1, ...
+// (each bin in increasing row order); bin_start_dst (device int[NB+1]).
+int64_t bin_scratch_len(int64_t m);
+void bin_rows(Launch& L, int64_t m, const uint8_t* binid, int32_t* scratch, int32_t* perm, int* bin_start_dst);
+
+struct SymArgs {
+    bool off64;
+    MatView A, B;
+    int64_t k;
+    const int32_t* bc_len;
+    const uint2* pairs;
+    const int32_t* perm;
+    const int* bin_start;   // device
+    int32_t* counts;
+    int32_t* cursors;       // nnz(A) scratch for windowed rows
+    const DevStatus* st;
+    int logG;
+};
+void symbolic_bins(Launch& L, const SymArgs& a, cudaStream_t dense_stream);
+
+struct NumArgs {
+    bool off64, f64, sort;
+    MatView A, B;
+    int64_t k;
+    const void* c_row_map;
+    int32_t* c_entries;
+    void* c_values;
+    const int32_t* perm;
+    const int* bin_start;        // device
+    const int* host_bin_start;   // host copy (row counts known after symbolic)
+    int32_t* cursors;
+    const DevStatus* st;
+    int logG;
+};
+void numeric_bins(Launch& L, const NumArgs& a, cudaStream_t dense_stream);
+
+}  // namespace kk

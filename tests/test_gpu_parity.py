@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Row maps and sorted column indices must be bit-exact; values within the north-star
+bound |c - c_ref| <= tau * sum|a||b| (tau 1e-12 fp64, 1e-5 fp32), and exactly equal on
+integer-valued workloads.
+"""
+import numpy as np
+import pytest
+import torch
+
+from workloads import generators as g
+
+from .helpers import assert_parity, gpu_spgemm, to_device
+
+pytestmark = pytest.mark.gpu
+
+RANDOM_CASES = [
+    (17, 23, 31, 6, 5, {}),
+    (40, 40, 40, 8, 8, {}),
+    (64, 9, 64, 5, 40, {}),
+    (5, 64, 3, 40, 3, {}),
+    (33, 20, 50, 7, 9, dict(sorted_rows=False)),
+    (30, 25, 45, 10, 10, dict(duplicates=True, sorted_rows=False)),
+    (30, 25, 45, 10, 10, dict(explicit_zeros=True)),
+    (20, 1, 20, 3, 20, dict(duplicates=True)),
+    (300, 200, 5000, 12, 60, {}),
+    (0, 5, 7, 3, 3, {}),
+    (6, 0, 7, 3, 3, {}),
+    (6, 5, 0, 3, 3, {}),
+]
+
+
+@pytest.mark.parametrize("vt", [torch.float64, torch.float32])
+@pytest.mark.parametrize("ot", [torch.int32, torch.int64])
+@pytest.mark.parametrize("case", range(len(RANDOM_CASES)))
+def test_random_small(oracle_mod, case, ot, vt):
+    m, n, k, ma, mb, kw = RANDOM_CASES[case]
+    A = g.random_csr(m, n, ma, seed=case + 1, **kw)
+    B = g.random_csr(n, k, mb, seed=case + 101, **kw)
+    got = gpu_spgemm(A, B, value_dtype=vt, offset_dtype=ot)
+    assert_parity(oracle_mod, A, B, got, value_dtype=vt)
+
+
+@pytest.mark.parametrize("compression", ["auto", "on", "off"])
+@pytest.mark.parametrize("sort_rows", [True, False])
+def test_options_same_result(oracle_mod, compression, sort_rows):
+    A, B = g.config("C2", size=12)
+    got = gpu_spgemm(A, B, compression=compression, sort_rows=sort_rows)
+    assert_parity(oracle_mod, A, B, got, exact=True, sorted_rows=sort_rows)
+    st = got[3]
+    assert st["compression_used"] == (compression != "off")
+
+
+@pytest.mark.parametrize("vt", [torch.float64, torch.float32])
+def test_C1(oracle_mod, vt):
+    A, B = g.config("C1")
+    got = gpu_spgemm(A, B, value_dtype=vt, offset_dtype=torch.int32)
+    assert_parity(oracle_mod, A, B, got, value_dtype=vt, exact=True)
+    assert got[3]["muladds"] == 24456 and got[3]["nnz_c"] == 12676
+
+
+@pytest.mark.parametrize("values", ["int", "random"])
+def test_C2_small(oracle_mod, values):
+    A, B = g.config("C2", size=22, values=values)
+    got = gpu_spgemm(A, B, offset_dtype=torch.int32)
+    assert_parity(oracle_mod, A, B, got, exact=(values == "int"))
+    n = 22
+    assert got[3]["nnz_c"] == (5 * n - 6) ** 3 and got[3]["muladds"] == (9 * n - 10) ** 3
+
+
+def test_C2_f32_random(oracle_mod):
+    A, B = g.config("C2", size=16, values="random")
+    got = gpu_spgemm(A, B, value_dtype=torch.float32, offset_dtype=torch.int32)
+    assert_parity(oracle_mod, A, B, got, value_dtype=torch.float32)
+
+
+def test_C3_galerkin(oracle_mod):
+    n = 33
+    A, P, R = g.config("C3", size=n)
+    from paper_2103_11991_b200 import SpGEMM, CsrMatrix
+
+    Ad, Pd, Rd = (to_device(M) for M in (A, P, R))
+    h = SpGEMM()
+    T = h(Ad, Pd)
+    h2 = SpGEMM()
+    Ac = h2(Rd, T)
+    torch.cuda.synchronize()
+    # T parity
+    got_T = (T.row_map.cpu().numpy(), T.entries.cpu().numpy(), T.values.cpu().numpy())
+    assert_parity(oracle_mod, A, P, got_T, exact=True)
+    # Ac parity against the oracle's R*(A*P), computed entirely on the CPU
+    orm, oent, oval, _ = oracle_mod.spgemm(A, P)
+    To = g.CSR(A.nrows, P.ncols, torch.tensor(orm), torch.tensor(oent), torch.tensor(oval))
+    got_Ac = (Ac.row_map.cpu().numpy(), Ac.entries.cpu().numpy(), Ac.values.cpu().numpy())
+    assert_parity(oracle_mod, R, To, got_Ac, exact=True)
+
+
+def test_C4_rmat_small(oracle_mod):
+    A, B = g.config("C4", size=13)
+    got = gpu_spgemm(A, B, offset_dtype=torch.int64)
+    assert_parity(oracle_mod, A, B, got, exact=True)
+
+
+def test_C5_block(oracle_mod):
+    A, B = g.config("C5", size=10)
+    got = gpu_spgemm(A, B, offset_dtype=torch.int64)
+    assert_parity(oracle_mod, A, B, got, exact=True)
+    assert got[3]["nnz_c"] == 9 * (5 * 10 - 6) ** 3
+
+
+def _long_rows(seed, m=40, n=400, k=200000, sorted_rows=True, dup=False):
+    """A few rows with thousands of products over a wide column range: exercises the
+    dense (windowed) symbolic and numeric tiers, cursors and multiple windows."""
+    A = g.random_csr(m, n, 120, seed=seed, empty_row_frac=0.0)
+    B = g.random_csr(n, k, 400, seed=seed + 9, sorted_rows=sorted_rows, duplicates=dup, empty_row_frac=0.0)
+    return A, B
+
+
+@pytest.mark.parametrize("sorted_rows", [True, False])
+@pytest.mark.parametrize("vt", [torch.float64, torch.float32])
+def test_dense_tiers(oracle_mod, sorted_rows, vt):
+    A, B = _long_rows(7, sorted_rows=sorted_rows)
+    got = gpu_spgemm(A, B, value_dtype=vt)
+    st = got[3]
+    assert st["numeric_bin_rows"][6] > 0 and st["symbolic_bin_rows"][8] > 0, st
+    assert_parity(oracle_mod, A, B, got, value_dtype=vt)
+
+
+def test_dense_tiers_duplicates(oracle_mod):
+    A, B = _long_rows(8, sorted_rows=True, dup=True)
+    got = gpu_spgemm(A, B)
+    assert_parity(oracle_mod, A, B, got)
+
+
+def test_symbolic_dense_multiwindow(oracle_mod):
+    # k > 1.6M bits: the symbolic bit vector needs several windows
+    A = g.random_csr(30, 300, 80, seed=3, empty_row_frac=0.0)
+    B = g.random_csr(300, 3_500_000, 300, seed=4, empty_row_frac=0.0)
+    for comp in ("on", "off"):
+        got = gpu_spgemm(A, B, compression=comp)
+        assert got[3]["symbolic_bin_rows"][8] > 0
+        assert_parity(oracle_mod, A, B, got)
+
+
+def test_row_flops_and_compress(oracle_mod):
+    from paper_2103_11991_b200 import SpGEMM
+
+    A, B = g.config("C4", size=12)
+    Ad, Bd = to_device(A), to_device(B)
+    h = SpGEMM()
+    f, F, tot = h.row_flops(Ad, Bd)
+    of, otot = oracle_mod.row_flops(A, B)
+    assert tot == otot and np.array_equal(f.cpu().numpy(), of)
+    assert np.array_equal(F.cpu().numpy(), np.concatenate([[0], np.cumsum(of)]))
+    ln, w, mk = h.compress(Bd)
+    torch.cuda.synchronize()
+    brm, ow, om = oracle_mod.compress(B)
+    ln, w, mk = ln.cpu().numpy(), w.cpu().numpy(), mk.cpu().numpy().view(np.uint32)
+    assert np.array_equal(ln, np.diff(brm))
+    rm = B.row_map.numpy()
+    got_w = np.concatenate([w[rm[j]:rm[j] + ln[j]] for j in range(B.nrows)])
+    got_m = np.concatenate([mk[rm[j]:rm[j] + ln[j]] for j in range(B.nrows)])
+    assert np.array_equal(got_w, ow) and np.array_equal(got_m, om)
+
+
+def test_symbolic_reuse_new_values(oracle_mod):
+    from paper_2103_11991_b200 import SpGEMM
+
+    A, B = g.config("C2", size=10, values="random")
+    Ad, Bd = to_device(A), to_device(B)
+    h = SpGEMM()
+    rm, nnz = h.symbolic(Ad, Bd)
+    h.numeric(Ad, Bd, rm, nnz=nnz)
+    Ad.values.mul_(2.0)  # new values, same pattern
+    ent, val = h.numeric(Ad, Bd, rm, nnz=nnz)
+    torch.cuda.synchronize()
+    A2 = g.CSR(A.nrows, A.ncols, A.row_map, A.entries, A.values * 2.0)
+    assert_parity(oracle_mod, A2, B, (rm.cpu().numpy(), ent.cpu().numpy(), val.cpu().numpy()))
+
+
+def test_errors():
+    from paper_2103_11991_b200 import SpGEMM, CsrMatrix
+    from paper_2103_11991_b200._ffi import KKError, KK_ERR_DIM_MISMATCH, KK_ERR_STALE_HANDLE, \
+        KK_ERR_UNSUPPORTED_TYPE, KK_ERR_INDEX_OVERFLOW
+
+    A = to_device(g.random_csr(10, 8, 3, seed=1))
+    B = to_device(g.random_csr(9, 8, 3, seed=2))
+    h = SpGEMM()
+    with pytest.raises(KKError) as e:
+        h.symbolic(A, B)
+    assert e.value.status == KK_ERR_DIM_MISMATCH
+    B2 = to_device(g.random_csr(8, 8, 3, seed=2))
+    rm, nnz = h.symbolic(A, B2)
+    B3 = to_device(g.random_csr(8, 8, 3, seed=3))
+    with pytest.raises(KKError) as e:
+        h.numeric(A, B3, rm, nnz=nnz)
+    assert e.value.status == KK_ERR_STALE_HANDLE
+    B4 = to_device(g.random_csr(8, 8, 3, seed=2), offset_dtype=torch.int32)
+    with pytest.raises(KKError) as e:
+        h.symbolic(A, B4)
+    assert e.value.status == KK_ERR_UNSUPPORTED_TYPE
+    # int32 offsets cannot hold nnz(C) > 2^31-1 -> caught on a large product only; here
+    # check validate catches an out-of-range column instead
+    bad = g.random_csr(8, 8, 3, seed=5)
+    bad.entries[0] = 100
+    hv = SpGEMM(validate=True)
+    with pytest.raises(KKError) as e:
+        hv.symbolic(A, to_device(bad))
+    assert e.value.status == KK_ERR_INDEX_OVERFLOW
+
+
+@pytest.mark.slow
+def test_C2_full_sampled(oracle_mod):
+    """BASELINE configs[1] at full size in the bench's launch configuration: bit-exact
+    counts/columns and exact integer values on a sample of rows (boundary + random)."""
+    A, B = g.config("C2", device="cuda")
+    from paper_2103_11991_b200 import SpGEMM
+
+    Ad, Bd = A.to(offset_dtype=torch.int32), B.to(offset_dtype=torch.int32)
+    h = SpGEMM()
+    rm, nnz = h.symbolic(Ad, Bd)
+    ent, val = h.numeric(Ad, Bd, rm, nnz=nnz)
+    torch.cuda.synchronize()
+    assert nnz == 120553784 and h.stats()["muladds"] == 704969000
+    rng = np.random.default_rng(0)
+    rows = np.concatenate([np.arange(0, 300), np.arange(A.nrows - 300, A.nrows), rng.integers(0, A.nrows, 1500)])
+    Ac, Bc = A.to(device="cpu"), B.to(device="cpu")
+    got = (rm.cpu().numpy().astype(np.int64), ent.cpu().numpy(), val.cpu().numpy())
+    assert_parity(oracle_mod, Ac, Bc, got, rows=rows, exact=True)
+    # properties that hold at any size: rows strictly increasing, interior row sums zero
+    lens = np.diff(got[0])
+    assert lens.max() == 125 and int((lens == 125).sum()) == 96 ** 3
