@@ -81,6 +81,8 @@ typedef struct {
     int compression;   /* -1 (default) auto, 0 off, 1 on: compress B into B_C */
     int validate;      /* 1: check column indices of A and B are in range (error otherwise) */
     int num_streams;   /* internal streams used to overlap work bins (default 2, 1 = none) */
+    int timing;        /* 1: bracket every kernel launch with CUDA events on the stream it is
+                          launched on (read with kk_spgemm_kernel_times); default 0 */
     kk_alloc_fn alloc;
     kk_free_fn free;
     void* alloc_ctx;
@@ -142,6 +144,22 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t handle, const kk_csr_t* A, con
  * (symbolic reuse). */
 kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t handle, const kk_csr_t* A, const kk_csr_t* B,
                               const void* c_row_map, int32_t* c_entries, void* c_values, void* stream);
+
+/* Per-kernel device times (opts.timing = 1).  One record per kernel (or fixed group of
+ * launches, e.g. the three launches of a scan), accumulated since the last
+ * kk_spgemm_timing_reset: number of launches, total and maximum duration in ms, from
+ * CUDA events recorded on the launching stream.  Synchronises on those events.
+ * Writes min(*count_inout, number of records) records into `out` (host) and sets
+ * *count_inout to the number of records available. */
+typedef struct {
+    char name[48];
+    int64_t launches;
+    double total_ms;
+    double max_ms;
+} kk_kernel_time_t;
+kk_status_t kk_spgemm_kernel_times(kk_spgemm_handle_t handle, kk_kernel_time_t* out, int* count_inout);
+/* Drop the accumulated kernel times (after synchronising the pending events). */
+kk_status_t kk_spgemm_timing_reset(kk_spgemm_handle_t handle);
 
 /* Statistics of the last symbolic/numeric pair. */
 kk_status_t kk_spgemm_stats(kk_spgemm_handle_t handle, kk_spgemm_stats_t* stats);

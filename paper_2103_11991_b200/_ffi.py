@@ -33,7 +33,7 @@ FREE_FN = ctypes.CFUNCTYPE(None, _vp, ctypes.c_size_t, _vp, _vp)
 
 class kk_spgemm_opts_t(ctypes.Structure):
     _fields_ = [("sort_rows", ctypes.c_int), ("compression", ctypes.c_int), ("validate", ctypes.c_int),
-                ("num_streams", ctypes.c_int), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", _vp)]
+                ("num_streams", ctypes.c_int), ("timing", ctypes.c_int), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", _vp)]
 
 
 class kk_spgemm_stats_t(ctypes.Structure):
@@ -41,6 +41,11 @@ class kk_spgemm_stats_t(ctypes.Structure):
                 ("b_sorted", ctypes.c_int), ("b_strict", ctypes.c_int), ("num_symbolic_bins", ctypes.c_int),
                 ("num_numeric_bins", ctypes.c_int), ("symbolic_bin_rows", _i64 * 16),
                 ("numeric_bin_rows", _i64 * 16), ("kernel_launches", _i64), ("workspace_bytes", _i64)]
+
+
+class kk_kernel_time_t(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 48), ("launches", _i64), ("total_ms", ctypes.c_double),
+                ("max_ms", ctypes.c_double)]
 
 
 class KKError(RuntimeError):
@@ -72,8 +77,11 @@ def load() -> ctypes.CDLL:
         lib.kk_spgemm_symbolic.argtypes = [H, P(kk_csr_t), P(kk_csr_t), _vp, P(_i64), _vp]
         lib.kk_spgemm_numeric.argtypes = [H, P(kk_csr_t), P(kk_csr_t), _vp, _vp, _vp, _vp]
         lib.kk_spgemm_stats.argtypes = [H, P(kk_spgemm_stats_t)]
+        lib.kk_spgemm_kernel_times.argtypes = [H, P(kk_kernel_time_t), P(ctypes.c_int)]
+        lib.kk_spgemm_timing_reset.argtypes = [H]
         for fn in ("kk_spgemm_create", "kk_spgemm_destroy", "kk_spgemm_row_flops", "kk_spgemm_compress",
-                   "kk_spgemm_symbolic", "kk_spgemm_numeric", "kk_spgemm_stats"):
+                   "kk_spgemm_symbolic", "kk_spgemm_numeric", "kk_spgemm_stats", "kk_spgemm_kernel_times",
+                   "kk_spgemm_timing_reset"):
             getattr(lib, fn).restype = ctypes.c_int
         lib.kk_status_string.argtypes = [ctypes.c_int]
         lib.kk_status_string.restype = ctypes.c_char_p
@@ -151,3 +159,18 @@ def kk_spgemm_stats(h) -> dict:
     d["symbolic_bin_rows"] = list(s.symbolic_bin_rows)
     d["numeric_bin_rows"] = list(s.numeric_bin_rows)
     return d
+
+
+def kk_spgemm_kernel_times(h) -> list:
+    """[(name, launches, total_ms, max_ms)] accumulated since the last reset (opts.timing=1)."""
+    n = ctypes.c_int(0)
+    _check(h, load().kk_spgemm_kernel_times(h, None, ctypes.byref(n)))
+    arr = (kk_kernel_time_t * max(n.value, 1))()
+    n2 = ctypes.c_int(n.value)
+    _check(h, load().kk_spgemm_kernel_times(h, arr, ctypes.byref(n2)))
+    return [(arr[i].name.decode(), int(arr[i].launches), float(arr[i].total_ms), float(arr[i].max_ms))
+            for i in range(min(n.value, n2.value))]
+
+
+def kk_spgemm_timing_reset(h) -> None:
+    _check(h, load().kk_spgemm_timing_reset(h))

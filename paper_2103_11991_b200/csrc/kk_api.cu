@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/kk_spgemm.h"
 #include "kk_internal.cuh"
@@ -27,6 +28,72 @@ struct Buf {
 };
 
 }  // namespace
+
+// Per-kernel CUDA-event timing (opts.timing): events are recorded around each launch on
+// its stream and resolved lazily, so the launches themselves stay asynchronous.
+struct kk::KTimer {
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    struct Acc {
+        std::string name;
+        int64_t n = 0;
+        double tot = 0, mx = 0;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    std::vector<Acc> acc;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void resolve() {
+        for (Rec& r : pending) {
+            if (!r.b) continue;
+            cudaEventSynchronize(r.b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            Acc* a = nullptr;
+            for (Acc& x : acc)
+                if (x.name == r.name) a = &x;
+            if (!a) {
+                acc.push_back(Acc());
+                a = &acc.back();
+                a->name = r.name;
+            }
+            a->n += 1;
+            a->tot += ms;
+            if (ms > a->mx) a->mx = ms;
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        pending.clear();
+    }
+    ~KTimer() {
+        resolve();
+        for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    }
+};
+
+void kk::ktimer_begin(KTimer* t, const char* name, cudaStream_t s) {
+    if (t->pending.size() > 4096) t->resolve();
+    KTimer::Rec r{name, t->get(), nullptr};
+    cudaEventRecord(r.a, s);
+    t->pending.push_back(r);
+}
+
+void kk::ktimer_end(KTimer* t, cudaStream_t s) {
+    KTimer::Rec& r = t->pending.back();
+    r.b = t->get();
+    cudaEventRecord(r.b, s);
+}
 
 struct kk_spgemm_handle_s {
     int device = 0;
@@ -49,6 +116,7 @@ struct kk_spgemm_handle_s {
     } rec;
     int host_num_bin_start[kk::NB + 1] = {0};
     kk_spgemm_stats_t stats;
+    kk::KTimer* timer = nullptr;
 };
 
 static kk_status_t fail(kk_spgemm_handle_t h, kk_status_t s, const char* fmt, ...) {
@@ -214,6 +282,7 @@ kk_status_t kk_spgemm_create(kk_spgemm_handle_t* out, int device, const kk_spgem
         cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
     }
     memset(&h->stats, 0, sizeof(h->stats));
+    if (o.timing) h->timer = new kk::KTimer();
     *out = h;
     return KK_OK;
 }
@@ -225,6 +294,7 @@ kk_status_t kk_spgemm_destroy(kk_spgemm_handle_t h) {
     Buf* bufs[] = {&h->flops, &h->fscan, &h->binid, &h->perm_sym, &h->perm_num, &h->counts, &h->binscratch,
                    &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status};
     for (Buf* b : bufs) release(h, *b);
+    delete h->timer;
     if (h->h_status) cudaFreeHost(h->h_status);
     if (h->side) cudaStreamDestroy(h->side);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
@@ -239,6 +309,7 @@ static kk::Launch make_launch(kk_spgemm_handle_t h, cudaStream_t s) {
     L.stream = s;
     L.num_sms = h->num_sms;
     L.launches = &h->launches;
+    L.timer = h->timer;
     return L;
 }
 
@@ -459,6 +530,34 @@ kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
         cudaStreamWaitEvent(s, h->ev_join, 0);
     }
     return cuda_check(h, cudaGetLastError(), "kk_spgemm_numeric launch");
+}
+
+kk_status_t kk_spgemm_kernel_times(kk_spgemm_handle_t h, kk_kernel_time_t* out, int* count_inout) {
+    if (!h || !count_inout || (*count_inout > 0 && !out)) return KK_ERR_INVALID_ARG;
+    if (!h->timer) return fail(h, KK_ERR_INVALID_ARG, "timing is off (kk_spgemm_opts_t.timing = 0)");
+    cudaSetDevice(h->device);
+    h->timer->resolve();
+    const int n = (int)h->timer->acc.size();
+    const int w = *count_inout < n ? *count_inout : n;
+    for (int i = 0; i < w; ++i) {
+        const auto& a = h->timer->acc[i];
+        memset(out[i].name, 0, sizeof(out[i].name));
+        strncpy(out[i].name, a.name.c_str(), sizeof(out[i].name) - 1);
+        out[i].launches = a.n;
+        out[i].total_ms = a.tot;
+        out[i].max_ms = a.mx;
+    }
+    *count_inout = n;
+    return cuda_check(h, cudaGetLastError(), "kk_spgemm_kernel_times");
+}
+
+kk_status_t kk_spgemm_timing_reset(kk_spgemm_handle_t h) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    if (!h->timer) return fail(h, KK_ERR_INVALID_ARG, "timing is off (kk_spgemm_opts_t.timing = 0)");
+    cudaSetDevice(h->device);
+    h->timer->resolve();
+    h->timer->acc.clear();
+    return cuda_check(h, cudaGetLastError(), "kk_spgemm_timing_reset");
 }
 
 kk_status_t kk_spgemm_stats(kk_spgemm_handle_t h, kk_spgemm_stats_t* out) {

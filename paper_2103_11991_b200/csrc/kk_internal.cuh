@@ -46,10 +46,24 @@ struct MatView {
     const void* values;
 };
 
+// Optional per-kernel CUDA-event timing (kk_spgemm_opts_t.timing; kk_api.cu).
+struct KTimer;
+void ktimer_begin(KTimer* t, const char* name, cudaStream_t s);
+void ktimer_end(KTimer* t, cudaStream_t s);
+
 struct Launch {
     cudaStream_t stream;
     int num_sms;
     long long* launches;   // incremented once per kernel launch
+    KTimer* timer;         // null unless timing is on
+    // bracket every launch (or fixed group of launches) with begin/end
+    void begin(const char* name, cudaStream_t s) const {
+        if (timer) ktimer_begin(timer, name, s);
+    }
+    void end(cudaStream_t s, int nlaunch = 1) const {
+        *launches += nlaunch;
+        if (timer) ktimer_end(timer, s);
+    }
 };
 
 // ---- host launchers (kk_kernels.cu) -------------------------------------------------

@@ -16,6 +16,7 @@
 #include <climits>
 #include <cstdio>
 #include <mutex>
+#include <string>
 #include <unordered_map>
 
 namespace kk {
@@ -103,8 +104,9 @@ __global__ void k_init_status(DevStatus* st) {
 }
 
 void init_status(Launch& L, DevStatus* st) {
+    L.begin("init_status", L.stream);
     k_init_status<<<1, 32, 0, L.stream>>>(st);
-    ++*L.launches;
+    L.end(L.stream);
 }
 
 // ------------------------------------------------------------------------------------
@@ -199,13 +201,14 @@ void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_
     if (B.nrows == 0) return;
     const int threads = 256;
     const int grid = grid_for(B.nrows, threads, L.num_sms, 16);
+    L.begin(do_comp ? "check_compress" : "check_sorted", L.stream);
     if (off64)
         k_check_compress<int64_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int64_t*)B.row_map, B.entries,
                                                                   do_comp, validate, bc_len, pairs, st);
     else
         k_check_compress<int32_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int32_t*)B.row_map, B.entries,
                                                                   do_comp, validate, bc_len, pairs, st);
-    ++*L.launches;
+    L.end(L.stream);
 }
 
 // ------------------------------------------------------------------------------------
@@ -274,6 +277,7 @@ void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, in
     if (A.nrows == 0) return;
     const int threads = 256;
     const int grid = grid_for(A.nrows, threads, L.num_sms, 16);
+    L.begin("row_flops_bin", L.stream);
     if (off64)
         k_row_flops<int64_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int64_t*)A.row_map,
                                                              A.entries, (const int64_t*)B.row_map, bc_len,
@@ -282,7 +286,7 @@ void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, in
         k_row_flops<int32_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int32_t*)A.row_map,
                                                              A.entries, (const int32_t*)B.row_map, bc_len,
                                                              comp_mode, B.nnz, validate, flops, binid, counts, st);
-    ++*L.launches;
+    L.end(L.stream);
 }
 
 // ------------------------------------------------------------------------------------
@@ -399,6 +403,7 @@ void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out,
         if (total_dst) cudaMemsetAsync(total_dst, 0, 8, L.stream);
         return;
     }
+    L.begin("exclusive_scan", L.stream);
     if (in64)
         k_scan_reduce<int64_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int64_t*)in, partial);
     else
@@ -416,7 +421,7 @@ void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out,
     else
         k_scan_down<int32_t, int32_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int32_t*)in, partial,
                                                                                   (int32_t*)out, nb, overflow);
-    *L.launches += 3;
+    L.end(L.stream, 3);
 }
 
 // ------------------------------------------------------------------------------------
@@ -442,8 +447,9 @@ __global__ void __launch_bounds__(256) k_numeric_binid(int64_t m, const int32_t*
 void numeric_binid(Launch& L, int64_t m, const int32_t* counts, uint8_t* binid) {
     if (m == 0) return;
     int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)L.num_sms * 16);
+    L.begin("numeric_binid", L.stream);
     k_numeric_binid<<<grid, 256, 0, L.stream>>>(m, counts, binid);
-    ++*L.launches;
+    L.end(L.stream);
 }
 
 constexpr int BCHUNK = 2048;  // rows per warp in the binning passes
@@ -528,10 +534,11 @@ void bin_rows(Launch& L, int64_t m, const uint8_t* binid, int32_t* scratch, int3
         return;
     }
     const int grid = (int)((nchunks * 32 + 255) / 256);
+    L.begin("bin_rows", L.stream);
     k_bin_count<<<grid, 256, 0, L.stream>>>(m, binid, scratch);
     k_bin_offsets<<<1, 1024, 0, L.stream>>>(nchunks, scratch, bin_start_dst);
     k_bin_scatter<<<grid, 256, 0, L.stream>>>(m, binid, scratch, bin_start_dst, perm);
-    *L.launches += 3;
+    L.end(L.stream, 3);
 }
 
 // ------------------------------------------------------------------------------------
@@ -743,6 +750,17 @@ static KCfg kernel_cfg(K kern, int threads, size_t smem, int num_sms) {
     return c;
 }
 
+// stable names for the timing table: "<base>_S<slots>"
+static const char* kname(const char* base, int S) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, std::string> names;
+    std::lock_guard<std::mutex> lk(mu);
+    std::string key = std::string(base) + "_S" + std::to_string(S);
+    auto it = names.find(key);
+    if (it == names.end()) it = names.emplace(key, key).first;
+    return it->second.c_str();
+}
+
 static int sym_warps_for(int S) { return S <= 512 ? 8 : (S == 1024 ? 4 : (S == 2048 ? 2 : 1)); }
 
 template <typename OffT, int S>
@@ -754,10 +772,11 @@ static void launch_sym_warp(Launch& L, const SymArgs& a, int bin) {
     int grid = c.grid_cap;
     int64_t need = (a.A.nrows + warps - 1) / warps;
     if (need < grid) grid = (int)(need > 0 ? need : 1);
+    L.begin(kname("sym_warp", S), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.logG,
                                                a.counts, a.st);
-    ++*L.launches;
+    L.end(L.stream);
 }
 
 template <typename OffT>
@@ -772,10 +791,11 @@ static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stre
         auto kern = k_sym_dense<OffT>;
         KCfg c = kernel_cfg(kern, threads, smem, L.num_sms);
         cudaStream_t s = dense_stream ? dense_stream : L.stream;
+        L.begin("sym_dense", s);
         kern<<<c.grid_cap, threads, smem, s>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, SYM_DENSE_BIN,
                                                a.k, wbits, a.cursors, a.counts, a.st);
-        ++*L.launches;
+        L.end(s);
     }
     launch_sym_warp<OffT, 4096>(L, a, 7);
     launch_sym_warp<OffT, 2048>(L, a, 6);
@@ -1044,11 +1064,12 @@ static void launch_num_warp(Launch& L, const NumArgs& a, int bin) {
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (rows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
+    L.begin(kname("num_warp", S), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                                (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
                                                a.bin_start, bin, a.logG, a.st);
-    ++*L.launches;
+    L.end(L.stream);
 }
 
 template <typename OffT, typename ValT, bool SORT>
@@ -1065,11 +1086,12 @@ static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_strea
         KCfg c = kernel_cfg(kern, threads, smem, L.num_sms);
         const int grid = (int)std::min<int64_t>(drows, c.grid_cap);
         cudaStream_t s = dense_stream ? dense_stream : L.stream;
+        L.begin("num_dense", s);
         kern<<<grid, threads, smem, s>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                          (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                          (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm, a.bin_start,
                                          NUM_DENSE_BIN, a.k, (int)W, a.cursors, a.st);
-        ++*L.launches;
+        L.end(s);
     }
     launch_num_warp<OffT, ValT, 1024, SORT>(L, a, 5);
     launch_num_warp<OffT, ValT, 512, SORT>(L, a, 4);

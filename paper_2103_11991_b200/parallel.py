@@ -1,0 +1,120 @@
+"""Row-sharded multi-GPU SpGEMM: one process per GPU, torch.distributed.
+
+C(i,:) depends only on A(i,:) and all of B (Eq. 1), so rows of A
+are split into contiguous, flop-balanced blocks; B is replicated with one broadcast
+(NCCL over NVLink/NVSwitch); after the local symbolic phase the ranks all-gather their
+nnz(C_p) so each knows the global offset O_p of its block of C (the layout of a
+row-distributed Tpetra matrix).  The numeric phase is local.
+
+Everything here is plumbing around the single-GPU C ABI (include/kk_spgemm.h): row
+ranges, collectives and offsets.  The arithmetic of every step runs in
+libkk_spgemm.so.
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+from .spgemm import CsrMatrix, SpGEMM
+
+_DT = [torch.int32, torch.int64, torch.float32, torch.float64]
+
+
+def flop_balanced_cuts(F: Sequence[int], world: int) -> List[int]:
+    """Split points r_0=0 <= r_1 <= ... <= r_P=m of rows, from the exclusive prefix F
+    (length m+1) of per-row multiply-adds: r_p is the first row whose prefix reaches
+    p*F[m]/P."""
+    import numpy as np
+
+    F = np.asarray(F, dtype=np.int64)
+    m = len(F) - 1
+    total = int(F[m]) if m >= 0 else 0
+    cuts = [0]
+    for p in range(1, world):
+        cuts.append(int(np.searchsorted(F, (total * p) // world, side="left")))
+    cuts.append(max(m, 0))
+    out = [min(max(c, 0), max(m, 0)) for c in cuts]
+    for i in range(1, len(out)):
+        out[i] = max(out[i], out[i - 1])
+    return out
+
+
+def global_offsets(nnz_per_rank: Sequence[int]) -> List[int]:
+    """Exclusive prefix of the gathered per-rank nnz: O_p = sum_{q<p} nnz_q."""
+    out, run = [], 0
+    for v in nnz_per_rank:
+        out.append(run)
+        run += int(v)
+    return out
+
+
+def slice_rows(M: CsrMatrix, r0: int, r1: int) -> CsrMatrix:
+    """Rows [r0, r1) of M as a CSR matrix of its own (row map rebased to 0; entries and
+    values are views, no copy)."""
+    rm = M.row_map
+    s = int(rm[r0].item())
+    e = int(rm[r1].item())
+    sub_rm = (rm[r0:r1 + 1] - rm[r0]).contiguous()
+    vals = M.values[s:e] if M.values is not None else None
+    return CsrMatrix(r1 - r0, M.ncols, sub_rm, M.entries[s:e], vals)
+
+
+def broadcast_csr(M: Optional[CsrMatrix], src: int = 0, device=None, group=None) -> CsrMatrix:
+    """Replicate a CSR matrix from rank `src` to every rank: a small header broadcast,
+    then row map + entries (the pattern, so symbolic could start), then values."""
+    rank = dist.get_rank(group)
+    dev = torch.device(device) if device is not None else (
+        M.row_map.device if M is not None else torch.device("cpu"))
+    hdr = torch.zeros(6, dtype=torch.int64, device=dev)
+    if rank == src:
+        hdr[0], hdr[1], hdr[2] = M.nrows, M.ncols, M.nnz
+        hdr[3] = _DT.index(M.row_map.dtype)
+        hdr[4] = _DT.index(M.values.dtype) if M.values is not None else -1
+    dist.broadcast(hdr, src, group=group)
+    nrows, ncols, nnz, od, vd = (int(x) for x in hdr[:5].tolist())
+    if rank == src:
+        rm, ent = M.row_map.to(dev).contiguous(), M.entries.to(dev).contiguous()
+        val = M.values.to(dev).contiguous() if M.values is not None else None
+    else:
+        rm = torch.empty(nrows + 1, dtype=_DT[od], device=dev)
+        ent = torch.empty(nnz, dtype=torch.int32, device=dev)
+        val = torch.empty(nnz, dtype=_DT[vd], device=dev) if vd >= 0 else None
+    dist.broadcast(rm, src, group=group)
+    if nnz:
+        dist.broadcast(ent, src, group=group)
+        if val is not None:
+            dist.broadcast(val, src, group=group)
+    return CsrMatrix(nrows, ncols, rm, ent, val)
+
+
+def allgather_nnz(nnz_local: int, device, group=None) -> List[int]:
+    """All-gather one int64 nnz(C_p) per rank."""
+    world = dist.get_world_size(group)
+    mine = torch.tensor([int(nnz_local)], dtype=torch.int64, device=device)
+    allv = torch.zeros(world, dtype=torch.int64, device=device)
+    dist.all_gather_into_tensor(allv, mine, group=group)
+    return [int(x) for x in allv.tolist()]
+
+
+class ShardedSpGEMM:
+    """C = A*B with rows of A block-distributed over the ranks of `group`.
+
+    Each rank passes its local row block A_p (rows [r_p, r_{p+1}) of A) and the full B.
+    Returns (C_p, O_p, nnz_total): the local rows of C and their global entry offset."""
+
+    def __init__(self, device=None, group=None, **opts):
+        self.group = group
+        self.h = SpGEMM(device=device, **opts)
+
+    def __call__(self, A_local: CsrMatrix, B: CsrMatrix) -> Tuple[CsrMatrix, int, int]:
+        rm, nnz = self.h.symbolic(A_local, B)
+        counts = allgather_nnz(nnz, rm.device, self.group)
+        offs = global_offsets(counts)
+        ent, val = self.h.numeric(A_local, B, rm, nnz=nnz)
+        rank = dist.get_rank(self.group)
+        return CsrMatrix(A_local.nrows, B.ncols, rm, ent, val), offs[rank], sum(counts)
+
+    def close(self):
+        self.h.close()

@@ -87,7 +87,7 @@ class SpGEMM:
     """Kernel handle: options + the symbolic state reused by numeric."""
 
     def __init__(self, device=None, sort_rows: bool = True, compression="auto", validate: bool = False,
-                 num_streams: int = 2):
+                 num_streams: int = 2, timing: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2103_11991_b200 needs a CUDA device (there is no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
@@ -97,6 +97,7 @@ class SpGEMM:
         o.compression = {"auto": -1, "off": 0, "on": 1, -1: -1, 0: 0, 1: 1, True: 1, False: 0}[compression]
         o.validate = int(bool(validate))
         o.num_streams = int(num_streams)
+        o.timing = int(bool(timing))
         self._h = _ffi.kk_spgemm_create(self.device.index, o)
 
     # -- phases ------------------------------------------------------------------------
@@ -130,6 +131,61 @@ class SpGEMM:
         ent, val = self.numeric(A, B, rm, nnz=nnz, stream=stream)
         return CsrMatrix(A.nrows, B.ncols, rm, ent, val)
 
+    # -- end to end from host memory ------------------------------------------------------
+    def multiply_host(self, A, B, stream=None) -> "CsrMatrix":
+        """C = A*B for CSR operands in (pinned) HOST memory: host->device copies of A and B,
+        both phases on the device, device->host copy of C into pinned host tensors.  Device
+        staging buffers are cached on the handle and reused when the sizes allow.  Returns
+        a host CsrMatrix (valid until the next call on this handle)."""
+        A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
+        dev = self.device
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        cache = self.__dict__.setdefault("_host_cache", {})
+
+        def dbuf(key, t):
+            b = cache.get(key)
+            if b is None or b.numel() < t.numel() or b.dtype != t.dtype:
+                b = torch.empty(max(t.numel(), 1), dtype=t.dtype, device=dev)
+                cache[key] = b
+            v = b[:t.numel()]
+            with torch.cuda.stream(st):
+                v.copy_(t, non_blocking=True)
+            return v
+
+        def hbuf(key, n, dtype):
+            b = cache.get(key)
+            if b is None or b.numel() < n or b.dtype != dtype:
+                b = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
+                cache[key] = b
+            return b[:n]
+
+        Ad = CsrMatrix(A.nrows, A.ncols, dbuf("arm", A.row_map), dbuf("aent", A.entries), dbuf("aval", A.values))
+        Bd = CsrMatrix(B.nrows, B.ncols, dbuf("brm", B.row_map), dbuf("bent", B.entries), dbuf("bval", B.values))
+        crm = cache.get("crm")
+        if crm is None or crm.numel() < A.nrows + 1 or crm.dtype != A.row_map.dtype:
+            crm = torch.empty(A.nrows + 1, dtype=A.row_map.dtype, device=dev)
+            cache["crm"] = crm
+        crm = crm[:A.nrows + 1]
+        crm, nnz = self.symbolic(Ad, Bd, c_row_map=crm, stream=st)
+        cent = cache.get("cent")
+        if cent is None or cent.numel() < nnz:
+            cent = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+            cache["cent"] = cent
+        cval = cache.get("cval")
+        if cval is None or cval.numel() < nnz or cval.dtype != A.values.dtype:
+            cval = torch.empty(max(nnz, 1), dtype=A.values.dtype, device=dev)
+            cache["cval"] = cval
+        cent, cval = self.numeric(Ad, Bd, crm, nnz=nnz, c_entries=cent[:nnz], c_values=cval[:nnz], stream=st)
+        h_rm = hbuf("h_crm", A.nrows + 1, crm.dtype)
+        h_ent = hbuf("h_cent", nnz, torch.int32)
+        h_val = hbuf("h_cval", nnz, cval.dtype)
+        with torch.cuda.stream(st):
+            h_rm.copy_(crm, non_blocking=True)
+            h_ent.copy_(cent, non_blocking=True)
+            h_val.copy_(cval, non_blocking=True)
+        st.synchronize()
+        return CsrMatrix(A.nrows, B.ncols, h_rm, h_ent, h_val)
+
     # -- individual steps ----------------------------------------------------------------
     def row_flops(self, A, B, scan: bool = True, total: bool = True, stream=None):
         """a1+a2: per-row multiply-adds, their exclusive scan, and the total."""
@@ -154,6 +210,13 @@ class SpGEMM:
         _ffi.kk_spgemm_compress(self._h, b, ln.data_ptr() if B.nrows else 0, pairs.data_ptr() if B.nnz else 0,
                                 _stream_ptr(self.device, stream))
         return ln[:B.nrows], pairs[:B.nnz, 0], pairs[:B.nnz, 1]
+
+    def kernel_times(self) -> list:
+        """Per-kernel CUDA-event times since the last reset (needs timing=True)."""
+        return _ffi.kk_spgemm_kernel_times(self._h)
+
+    def timing_reset(self) -> None:
+        _ffi.kk_spgemm_timing_reset(self._h)
 
     def stats(self) -> dict:
         return _ffi.kk_spgemm_stats(self._h)
