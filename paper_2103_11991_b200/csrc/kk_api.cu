@@ -505,6 +505,7 @@ kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
     na.off64 = A->offset_type == KK_I64;
     na.f64 = A->value_type == KK_F64;
     na.sort = h->opts.sort_rows != 0;
+    na.strict = h->stats.b_strict != 0;
     na.A = view(A);
     na.B = view(B);
     na.k = B->ncols;

@@ -1,0 +1,183 @@
+// kk_device.cuh -- device helpers and launch-config helpers shared by the kernel TUs.
+//
+// Product code only: nothing here is shared with oracle/ (DESIGN.md Sec. 2).
+#pragma once
+#include "kk_internal.cuh"
+
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+namespace kk {
+
+#define FULL 0xffffffffu
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned lanemask_le() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_le;" : "=r"(r));
+    return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+    return v;
+}
+
+template <typename OffT>
+__device__ __forceinline__ int64_t ld(const OffT* p, int64_t i) {
+    return (int64_t)__ldg(p + i);
+}
+
+constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x >> 1); }
+
+template <int S>
+__device__ __forceinline__ uint32_t hslot(uint32_t key) {
+    return (key * 0x9E3779B1u) >> (32 - ilog2(S));
+}
+
+// Claim-or-find `key` in an open-addressing table (linear probing).  Returns the slot;
+// *fresh = true when this call inserted the key.  The table never overflows: the
+// number of distinct keys of a row is bounded by the bin's capacity.
+template <int S>
+__device__ __forceinline__ uint32_t probe_claim(uint32_t* keys, uint32_t key, bool* fresh) {
+    uint32_t h = hslot<S>(key);
+    *fresh = false;
+    while (true) {
+        uint32_t cur = ((volatile uint32_t*)keys)[h];
+        if (cur == key) return h;
+        if (cur == EMPTY) {
+            cur = atomicCAS(&keys[h], EMPTY, key);
+            if (cur == EMPTY) {
+                *fresh = true;
+                return h;
+            }
+            if (cur == key) return h;
+        }
+        h = (h + 1) & (S - 1);
+    }
+}
+
+template <int S>
+__device__ __forceinline__ uint32_t probe_find(const uint32_t* keys, uint32_t key) {
+    uint32_t h = hslot<S>(key);
+    while (keys[h] != key) h = (h + 1) & (S - 1);
+    return h;
+}
+
+// Walk the part of a SORTED row [q0, qe) whose keys are below `hi`, 32 entries per step;
+// calls f(q) for each such entry, returns the first position not processed.
+template <typename KeyF, typename F>
+__device__ __forceinline__ int64_t walk_sorted(int64_t q0, int64_t qe, int64_t hi, KeyF key, F f) {
+    const int lane = threadIdx.x & 31;
+    while (q0 < qe) {
+        const int64_t q = q0 + lane;
+        const int64_t kq = q < qe ? key(q) : INT64_MAX;
+        const bool in = kq < hi;
+        if (in) f(q, kq);
+        const unsigned bal = __ballot_sync(FULL, in);
+        q0 += __popc(bal);
+        if (bal != FULL) break;
+    }
+    return q0;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v) {
+    __shared__ T red[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    T t = 0;
+    for (int w = 0; w < nw; ++w) t += red[w];
+    return t;
+}
+
+// ------------------------------------------------------------------------------------
+// a8: warp bitonic sort of 32*E keys held E per lane (element e = lane*E + r)
+// (team-level bitonic sort, mapped to one warp's registers)
+// ------------------------------------------------------------------------------------
+template <int E>
+__device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= E) {
+                const int lj = j / E;
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const int e = lane * E + r;
+                    const uint32_t o = __shfl_xor_sync(FULL, v[r], lj);
+                    const bool up = (e & k) == 0;
+                    const bool lower = (e & j) == 0;
+                    v[r] = (up == lower) ? min(v[r], o) : max(v[r], o);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < E; ++r) {
+                    const int pr = r ^ j;
+                    if (pr > r) {
+                        const int e = lane * E + r;
+                        const bool up = (e & k) == 0;
+                        const uint32_t x = v[r], y = v[pr];
+                        const bool sw = up ? (x > y) : (x < y);
+                        v[r] = sw ? y : x;
+                        v[pr] = sw ? x : y;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// launch configuration helpers
+// ------------------------------------------------------------------------------------
+struct KCfg {
+    int threads;
+    size_t smem;
+    int grid_cap;  // max resident CTAs on the device
+};
+
+
+template <typename K>
+inline KCfg kernel_cfg(K kern, int threads, size_t smem, int num_sms) {
+    static std::mutex g_cfg_mu;
+    static std::unordered_map<const void*, KCfg> g_cfg;
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    auto it = g_cfg.find((const void*)kern);
+    if (it != g_cfg.end() && it->second.threads == threads && it->second.smem == smem) return it->second;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    KCfg c{threads, smem, per_sm * num_sms};
+    g_cfg[(const void*)kern] = c;
+    return c;
+}
+
+// stable names for the timing table: "<base>_S<slots>"
+inline const char* kname(const char* base, int S) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, std::string> names;
+    std::lock_guard<std::mutex> lk(mu);
+    std::string key = std::string(base) + "_S" + std::to_string(S);
+    auto it = names.find(key);
+    if (it == names.end()) it = names.emplace(key, key).first;
+    return it->second.c_str();
+}
+
+}  // namespace kk

@@ -102,6 +102,7 @@ void symbolic_bins(Launch& L, const SymArgs& a, cudaStream_t dense_stream);
 
 struct NumArgs {
     bool off64, f64, sort;
+    bool strict;                 // every B row strictly increasing (host copy of the a4 flag)
     MatView A, B;
     int64_t k;
     const void* c_row_map;

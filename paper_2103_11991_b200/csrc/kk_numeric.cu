@@ -1,0 +1,588 @@
+// kk_numeric.cu -- a7 + a8: numeric phase (Eq. 1, 174, 178) with fused row sort
+// (PAPER.md:621-647).
+#include "kk_device.cuh"
+
+namespace kk {
+// ------------------------------------------------------------------------------------
+// a7: numeric, warp-owned shared hash (accum = +).  With G = 32
+// lanes on one strictly increasing B row the keys of a step are distinct, so values
+// are updated with plain shared loads/stores; otherwise with shared atomicAdd.
+// The compaction is followed by the fused per-row sort (a8) and a coalesced write.
+// ------------------------------------------------------------------------------------
+template <typename OffT, typename ValT, int S, bool SORT>
+__global__ void __launch_bounds__(256) k_num_warp(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                  const ValT* __restrict__ aval, const OffT* __restrict__ brm,
+                                                  const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                                  const OffT* __restrict__ crm, int32_t* __restrict__ cent,
+                                                  ValT* __restrict__ cval, const int32_t* __restrict__ perm,
+                                                  const int* __restrict__ bin_start, int bin, int logG,
+                                                  const DevStatus* __restrict__ st) {
+    extern __shared__ __align__(16) unsigned char sm_num[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    constexpr size_t WB = (size_t)S * sizeof(ValT) + (size_t)S * 4 + (size_t)S * 2;
+    ValT* vals = (ValT*)(sm_num + (size_t)warp * WB);
+    uint32_t* keys = (uint32_t*)(vals + S);
+    uint32_t* stage = keys + S;
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    if (r0 + blockIdx.x * warps + warp >= r1) return;
+    for (int t = lane; t < S; t += 32) {
+        keys[t] = EMPTY;
+        vals[t] = (ValT)0;
+    }
+    __syncwarp();
+    const bool plain = (logG == 5) && (st->b_strict != 0);
+    const int G = 1 << logG, per = 32 >> logG, gl = lane & (G - 1), sub = lane >> logG;
+    for (int r = r0 + blockIdx.x * warps + warp; r < r1; r += gridDim.x * warps) {
+        const int i = perm[r];
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        const int64_t cb = ld(crm, i);
+        const int clen = (int)(ld(crm, i + 1) - cb);
+        for (int64_t p0 = s; p0 < e; p0 += per) {
+            const int64_t p = p0 + sub;
+            if (p < e) {
+                const int j = __ldg(aent + p);
+                const ValT a = __ldg(aval + p);
+                const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+                bool fresh;
+                for (int64_t q = bs + gl; q < be; q += G) {
+                    const uint32_t col = (uint32_t)__ldg(bent + q);
+                    const ValT prod = a * __ldg(bval + q);
+                    const uint32_t h = probe_claim<S>(keys, col, &fresh);
+                    if (plain)
+                        vals[h] += prod;
+                    else
+                        atomicAdd(&vals[h], prod);
+                }
+            }
+            if (plain) __syncwarp();
+        }
+        __syncwarp();
+        // compaction (slot order) into stage: keys when sorting, slots otherwise
+        int n = 0;
+#pragma unroll 4
+        for (int c = 0; c < S; c += 32) {
+            const uint32_t kk = keys[c + lane];
+            const bool occ = kk != EMPTY;
+            const unsigned bal = __ballot_sync(FULL, occ);
+            if (occ) stage[n + __popc(bal & lanemask_lt())] = SORT ? kk : (uint32_t)(c + lane);
+            n += __popc(bal);
+        }
+        __syncwarp();
+        if (n > clen) n = clen;  // guard: never write past the row (row map from another product)
+        if (SORT) {
+            constexpr int E = S / 64;
+            uint32_t v[E];
+#pragma unroll
+            for (int r2 = 0; r2 < E; ++r2) {
+                const int idx = lane * E + r2;
+                v[r2] = idx < n ? stage[idx] : EMPTY;
+            }
+            warp_bitonic_sort<E>(v);
+            __syncwarp();
+#pragma unroll
+            for (int r2 = 0; r2 < E; ++r2) {
+                const int idx = lane * E + r2;
+                if (idx < n) stage[idx] = v[r2];
+            }
+            __syncwarp();
+            for (int t = lane; t < n; t += 32) {
+                const uint32_t col = stage[t];
+                const uint32_t h = probe_find<S>(keys, col);
+                cent[cb + t] = (int32_t)col;
+                cval[cb + t] = vals[h];
+            }
+        } else {
+            for (int t = lane; t < n; t += 32) {
+                const uint32_t h = stage[t];
+                cent[cb + t] = (int32_t)keys[h];
+                cval[cb + t] = vals[h];
+            }
+        }
+        __syncwarp();
+        for (int t = lane; t < S; t += 32) {
+            keys[t] = EMPTY;
+            vals[t] = (ValT)0;
+        }
+        __syncwarp();
+    }
+}
+
+// a7 for rows above the warp tables: column-windowed dense scalar accumulator (the
+// paper's dense numeric accumulator, held per CTA in shared memory
+// instead of per thread) with a presence bitmap; compaction walks the bitmap in
+// column order, so the output row is sorted without a sort.
+template <typename OffT, typename ValT>
+__global__ void __launch_bounds__(256) k_num_dense(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                   const ValT* __restrict__ aval, const OffT* __restrict__ brm,
+                                                   const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                                   const OffT* __restrict__ crm, int32_t* __restrict__ cent,
+                                                   ValT* __restrict__ cval, const int32_t* __restrict__ perm,
+                                                   const int* __restrict__ bin_start, int bin, int64_t k, int W,
+                                                   int32_t* __restrict__ cursors, const DevStatus* __restrict__ st) {
+    extern __shared__ __align__(16) unsigned char sm_dense[];
+    ValT* win = (ValT*)sm_dense;
+    uint32_t* bmp = (uint32_t*)(win + W);
+    __shared__ int wcnt[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    if (r0 + (int)blockIdx.x >= r1) return;
+    for (int t = threadIdx.x; t < W; t += blockDim.x) win[t] = (ValT)0;
+    for (int t = threadIdx.x; t < (W >> 5); t += blockDim.x) bmp[t] = 0;
+    __syncthreads();
+    const bool sorted = st->b_sorted != 0;
+    for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+        const int i = perm[r];
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        const int64_t cb = ld(crm, i);
+        const int64_t clen = ld(crm, i + 1) - cb;
+        int64_t outpos = 0;
+        for (int64_t lo = 0; lo < k; lo += W) {
+            const int64_t hi = min(k, lo + (int64_t)W);
+            const bool single = (lo == 0 && hi == k);
+            for (int64_t p = s + warp; p < e; p += warps) {
+                const int j = __ldg(aent + p);
+                const ValT a = __ldg(aval + p);
+                const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+                auto ins = [&](int64_t q, int64_t c) {
+                    const int x = (int)(c - lo);
+                    atomicAdd(&win[x], a * __ldg(bval + q));
+                    atomicOr(&bmp[x >> 5], 1u << (x & 31));
+                };
+                if (single) {
+                    for (int64_t q = bs + lane; q < be; q += 32) ins(q, __ldg(bent + q));
+                } else if (sorted) {
+                    const int64_t q0 = bs + (lo == 0 ? 0 : cursors[p]);
+                    const int64_t qn = walk_sorted(
+                        q0, be, hi, [&](int64_t q) { return (int64_t)__ldg(bent + q); }, ins);
+                    if (lane == 0) cursors[p] = (int32_t)(qn - bs);
+                } else {
+                    for (int64_t q = bs + lane; q < be; q += 32) {
+                        const int c = __ldg(bent + q);
+                        if (c >= lo && c < hi) ins(q, c);
+                    }
+                }
+            }
+            __syncthreads();
+            // compaction in column order: warp w owns words [w0, w1)
+            const int nw = (int)((hi - lo + 31) >> 5);
+            const int w0 = (int)((int64_t)warp * nw / warps), w1 = (int)((int64_t)(warp + 1) * nw / warps);
+            int c = 0;
+            for (int t = w0 + lane; t < w1; t += 32) c += __popc(bmp[t]);
+            c = warp_sum(c);
+            if (lane == 0) wcnt[warp] = c;
+            __syncthreads();
+            int off = 0, tot = 0;
+            for (int w = 0; w < warps; ++w) {
+                if (w < warp) off += wcnt[w];
+                tot += wcnt[w];
+            }
+            for (int t0 = w0; t0 < w1; t0 += 32) {
+                const int t = t0 + lane;
+                const uint32_t wv = t < w1 ? bmp[t] : 0u;
+                unsigned nz = __ballot_sync(FULL, wv != 0);
+                while (nz) {
+                    const int src = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    const uint32_t word = __shfl_sync(FULL, wv, src);
+                    const int tw = t0 + src;
+                    if ((word >> lane) & 1u) {
+                        const int64_t pos = outpos + off + __popc(word & lanemask_lt());
+                        const int x = tw * 32 + lane;
+                        if (pos < clen) {
+                            cent[cb + pos] = (int32_t)(lo + x);
+                            cval[cb + pos] = win[x];
+                        }
+                        win[x] = (ValT)0;
+                    }
+                    off += __popc(word);
+                }
+                if (t < w1 && wv) bmp[t] = 0;
+            }
+            outpos += tot;
+            __syncthreads();
+        }
+    }
+}
+
+
+// ------------------------------------------------------------------------------------
+// a7 (strict B): numeric, warp-owned shared hash with atomic-free claims.
+//
+// Used when every row of B is strictly increasing (checked in a4), so the <= 32 products
+// of one warp step -- 32 consecutive entries of ONE B row -- have distinct keys:
+//   * claims use write-then-verify (a lane writes its key into an EMPTY slot, the warp
+//     syncs, the lane re-reads; one writer wins, the others probe on) -- no ATOMS.CAS;
+//   * values are updated with a plain shared load / add / store (slots are distinct).
+// Slot layout is bank-major: probe position L in [0,S) maps to slot (L % R)*32 + L / R
+// (R = S/32 rows of 32 banks), and a key starts at L0 = (col & 31)*R + hash(col >> 5),
+// so keys of consecutive columns sit in different banks (stencil rows are runs of
+// consecutive columns) and a probe sequence stays in its bank until the bank is full.
+// The A row is staged per 32-entry chunk in shared memory (B row start/length, a_ij),
+// and the B row of the next step is loaded while the current step is inserted.
+// Epilogue (a8): compaction by ballot into (col - cmin) << log2(S) | slot, a warp bitonic
+// sort of those 32-bit words in registers, coalesced writes, and the table is reset at
+// exactly the slots that were used.
+// ------------------------------------------------------------------------------------
+template <int S>
+__device__ __forceinline__ uint32_t bm_slot(uint32_t L) {
+    constexpr int R = S / 32, LOGR = ilog2(R);
+    return (L & (R - 1)) * 32u + (L >> LOGR);
+}
+
+template <int S>
+__device__ __forceinline__ uint32_t bm_start(uint32_t col) {
+    constexpr int R = S / 32, LOGR = ilog2(R);
+    return (col & 31u) * R + (((col >> 5) * 0x9E3779B1u) >> (32 - LOGR));
+}
+
+// Find or claim `col` (lanes with act); returns its slot.  Keys of active lanes must be
+// distinct.  Warp-synchronous: all 32 lanes call it.  Lanes first probe on their own (a
+// hit needs no synchronisation); lanes that reach an EMPTY slot then claim it together:
+// write, __syncwarp, re-read; a lane whose write lost continues probing.  *won is set
+// for the lanes whose claim stuck (fresh keys).
+template <int S>
+__device__ __forceinline__ uint32_t strict_claim(uint32_t* keys, uint32_t col, bool act, bool* won) {
+    uint32_t L = bm_start<S>(col);
+    uint32_t h = bm_slot<S>(L);
+    bool need = false;
+    *won = false;
+    if (act) {
+        uint32_t k = keys[h];
+        while (k != col && k != EMPTY) {
+            L = (L + 1) & (S - 1);
+            h = bm_slot<S>(L);
+            k = keys[h];
+        }
+        need = (k == EMPTY);
+    }
+    while (__any_sync(FULL, need)) {
+        if (need) keys[h] = col;
+        __syncwarp();
+        if (need) {
+            uint32_t k = keys[h];
+            if (k == col) {
+                need = false;
+                *won = true;
+            } else {
+                do {
+                    L = (L + 1) & (S - 1);
+                    h = bm_slot<S>(L);
+                    k = keys[h];
+                } while (k != col && k != EMPTY);
+                need = (k == EMPTY);
+            }
+        }
+        __syncwarp();
+    }
+    return h;
+}
+
+template <int S>
+__device__ __forceinline__ uint32_t strict_find(const uint32_t* keys, uint32_t col) {
+    uint32_t L = bm_start<S>(col);
+    uint32_t h = bm_slot<S>(L);
+    while (keys[h] != col) {
+        L = (L + 1) & (S - 1);
+        h = bm_slot<S>(L);
+    }
+    return h;
+}
+
+// Per A entry of the current 32-entry chunk: start and length of its B row.
+template <typename OffT>
+struct StepInfoT {
+    OffT bb;
+    int bl;
+};
+template <>
+struct StepInfoT<int64_t> {
+    long long bb;
+    int bl;
+    int pad;
+};
+
+// Shared-memory layout of one warp: vals[S] | info[32] | av[32] | keys[S] | list[CAP]
+template <typename OffT, typename ValT, int S, int CAP>
+struct StrictLayout {
+    static constexpr size_t vals = 0;
+    static constexpr size_t info = vals + (size_t)S * sizeof(ValT);
+    static constexpr size_t av = info + 32 * sizeof(StepInfoT<OffT>);
+    static constexpr size_t keys = (av + 32 * sizeof(ValT) + 15) / 16 * 16;
+    static constexpr size_t list = keys + (size_t)S * 4;
+    static constexpr size_t bytes = (list + (size_t)CAP * 4 + 15) / 16 * 16;
+};
+
+template <typename OffT, typename ValT, int S, int CAP, bool SORT>
+__global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                    const ValT* __restrict__ aval, const OffT* __restrict__ brm,
+                                                    const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                                    const OffT* __restrict__ crm, int32_t* __restrict__ cent,
+                                                    ValT* __restrict__ cval, const int32_t* __restrict__ perm,
+                                                    const int* __restrict__ bin_start, int bin) {
+    using LY = StrictLayout<OffT, ValT, S, CAP>;
+    using SI = StepInfoT<OffT>;
+    constexpr int LOGS = ilog2(S);
+    constexpr int E = CAP / 32;  // sort elements per lane
+    extern __shared__ __align__(16) unsigned char sm_num[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    unsigned char* base = sm_num + (size_t)warp * LY::bytes;
+    ValT* vals = (ValT*)(base + LY::vals);
+    SI* info = (SI*)(base + LY::info);
+    ValT* av = (ValT*)(base + LY::av);
+    uint32_t* keys = (uint32_t*)(base + LY::keys);
+    uint32_t* list = (uint32_t*)(base + LY::list);
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    if (r0 + blockIdx.x * warps + warp >= r1) return;
+    for (int t = lane; t < S; t += 32) {
+        keys[t] = EMPTY;
+        vals[t] = (ValT)0;
+    }
+    __syncwarp();
+    for (int r = r0 + blockIdx.x * warps + warp; r < r1; r += gridDim.x * warps) {
+        const int i = perm[r];
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        const int64_t cb = ld(crm, i);
+        const int clen = (int)(ld(crm, i + 1) - cb);
+        int n = 0;  // keys claimed so far (warp-uniform)
+        for (int64_t c0 = s; c0 < e; c0 += 32) {
+            const int na = (int)min((int64_t)32, e - c0);
+            int bl = 0;
+            if (lane < na) {
+                const int j = __ldg(aent + c0 + lane);
+                const ValT a = __ldg(aval + c0 + lane);
+                const OffT bb = __ldg(brm + j);
+                bl = (int)(__ldg(brm + j + 1) - bb);
+                info[lane].bb = bb;
+                info[lane].bl = bl;
+                av[lane] = a;
+            }
+            unsigned rem = __ballot_sync(FULL, bl > 0);
+            const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
+            __syncwarp();
+            if (!rem) continue;
+            auto insert = [&](uint32_t col, ValT prod) {
+                const bool act = col != EMPTY;
+                bool won;
+                const uint32_t h = strict_claim<S>(keys, col, act, &won);
+                const unsigned wb = __ballot_sync(FULL, won);
+                if (won) list[n + __popc(wb & lanemask_lt())] = h;
+                n += __popc(wb);
+                if (act) vals[h] += prod;
+            };
+            if (maxbl <= 32) {
+                // one step per B row: steps are the set bits of rem, loads two steps ahead
+                auto fetch = [&](unsigned& m, uint32_t& col, ValT& bv, ValT& a) {
+                    col = EMPTY;
+                    bv = (ValT)0;
+                    a = (ValT)0;
+                    if (m) {
+                        const int t = __ffs(m) - 1;
+                        m &= m - 1;
+                        const SI si = info[t];
+                        a = av[t];
+                        if (lane < si.bl) {
+                            col = (uint32_t)__ldg(bent + si.bb + lane);
+                            bv = __ldg(bval + si.bb + lane);
+                        }
+                        return true;
+                    }
+                    return false;
+                };
+                uint32_t c0_, c1_, c2_;
+                ValT v0, v1, v2, a0, a1, a2;
+                bool h0 = fetch(rem, c0_, v0, a0);
+                bool h1 = fetch(rem, c1_, v1, a1);
+                while (h0) {
+                    const bool h2 = fetch(rem, c2_, v2, a2);
+                    insert(c0_, a0 * v0);
+                    h0 = h1;
+                    c0_ = c1_;
+                    v0 = v1;
+                    a0 = a1;
+                    h1 = h2;
+                    c1_ = c2_;
+                    v1 = v2;
+                    a1 = a2;
+                }
+            } else {
+                // long B rows: 32-entry segments, one ahead
+                while (rem) {
+                    const int t = __ffs(rem) - 1;
+                    rem &= rem - 1;
+                    const SI si = info[t];
+                    const ValT a = av[t];
+                    for (int q0 = 0; q0 < si.bl; q0 += 32) {
+                        uint32_t col = EMPTY;
+                        ValT bv = (ValT)0;
+                        if (q0 + lane < si.bl) {
+                            col = (uint32_t)__ldg(bent + si.bb + q0 + lane);
+                            bv = __ldg(bval + si.bb + q0 + lane);
+                        }
+                        insert(col, a * bv);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        // ---- epilogue: gather claimed slots, sort, write, reset ----
+        const int nn = min(n, clen);  // guard: never write past the row
+        if (SORT) {
+            uint32_t sv[E], kk[E];
+            uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int idx = lane * E + q;
+                sv[q] = idx < n ? list[idx] : 0u;
+                kk[q] = idx < n ? keys[sv[q]] : 0u;
+                if (idx < n) {
+                    mn = min(mn, kk[q]);
+                    mx = max(mx, kk[q]);
+                }
+            }
+            mn = __reduce_min_sync(FULL, mn);
+            mx = __reduce_max_sync(FULL, mx);
+            const bool packed = (mx - mn) < ((1u << (32 - LOGS)) - 1u);
+            uint32_t v[E];
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int idx = lane * E + q;
+                v[q] = idx < n ? (packed ? (((kk[q] - mn) << LOGS) | sv[q]) : kk[q]) : 0xffffffffu;
+            }
+            warp_bitonic_sort<E>(v);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int idx = lane * E + q;
+                if (idx < n) list[idx] = v[q];
+            }
+            __syncwarp();
+            for (int t = lane; t < n; t += 32) {
+                const uint32_t w = list[t];
+                uint32_t slot, col;
+                if (packed) {
+                    slot = w & (S - 1);
+                    col = (w >> LOGS) + mn;
+                } else {
+                    col = w;
+                    slot = strict_find<S>(keys, col);
+                }
+                if (t < nn) {
+                    cent[cb + t] = (int32_t)col;
+                    cval[cb + t] = vals[slot];
+                }
+                list[t] = slot;
+            }
+            __syncwarp();
+        } else {
+            for (int t = lane; t < nn; t += 32) {
+                const uint32_t slot = list[t];
+                cent[cb + t] = (int32_t)keys[slot];
+                cval[cb + t] = vals[slot];
+            }
+        }
+        __syncwarp();
+        for (int t = lane; t < n; t += 32) {
+            const uint32_t slot = list[t];
+            keys[slot] = EMPTY;
+            vals[slot] = (ValT)0;
+        }
+        __syncwarp();
+    }
+}
+
+// rows of numeric bin `bin` hold nnz(C_i) <= CAP = 16 << bin; the table has S = 4*CAP slots
+template <typename OffT, typename ValT, int CAP, bool SORT>
+static void launch_num_strict(Launch& L, const NumArgs& a, int bin) {
+    constexpr int S = 4 * CAP;
+    const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
+    if (rows <= 0) return;
+    const int warps = CAP <= 128 ? 8 : 4;
+    const size_t smem = (size_t)warps * StrictLayout<OffT, ValT, S, CAP>::bytes;
+    auto kern = k_num_strict<OffT, ValT, S, CAP, SORT>;
+    KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    int64_t need = (rows + warps - 1) / warps;
+    int grid = (int)std::min<int64_t>(need, c.grid_cap);
+    L.begin(kname("num_strict", S), L.stream);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
+                                               (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
+                                               (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
+                                               a.bin_start, bin);
+    L.end(L.stream);
+}
+
+template <typename OffT, typename ValT, int S, bool SORT>
+static void launch_num_warp(Launch& L, const NumArgs& a, int bin) {
+    const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
+    if (rows <= 0) return;
+    const int warps = (S <= 256) ? 8 : 4;
+    const size_t smem = (size_t)warps * ((size_t)S * sizeof(ValT) + (size_t)S * 6);
+    auto kern = k_num_warp<OffT, ValT, S, SORT>;
+    KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    int64_t need = (rows + warps - 1) / warps;
+    int grid = (int)std::min<int64_t>(need, c.grid_cap);
+    L.begin(kname("num_warp", S), L.stream);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
+                                               (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
+                                               (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
+                                               a.bin_start, bin, a.logG, a.st);
+    L.end(L.stream);
+}
+
+template <typename OffT, typename ValT, bool SORT>
+static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_stream) {
+    const int drows = a.host_bin_start[NUM_DENSE_BIN + 1] - a.host_bin_start[NUM_DENSE_BIN];
+    if (drows > 0) {
+        const int threads = 256;
+        const size_t budget = 200 * 1024;
+        int64_t W = (int64_t)(budget / (sizeof(ValT) + 0.125)) & ~31ll;
+        const int64_t k32 = ((a.k + 31) / 32) * 32;
+        if (k32 < W) W = k32 > 0 ? k32 : 32;
+        const size_t smem = (size_t)W * sizeof(ValT) + (size_t)(W / 32) * 4;
+        auto kern = k_num_dense<OffT, ValT>;
+        KCfg c = kernel_cfg(kern, threads, smem, L.num_sms);
+        const int grid = (int)std::min<int64_t>(drows, c.grid_cap);
+        cudaStream_t s = dense_stream ? dense_stream : L.stream;
+        L.begin("num_dense", s);
+        kern<<<grid, threads, smem, s>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
+                                         (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
+                                         (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm, a.bin_start,
+                                         NUM_DENSE_BIN, a.k, (int)W, a.cursors, a.st);
+        L.end(s);
+    }
+    if (a.strict && a.logG == 5) {
+        launch_num_strict<OffT, ValT, 512, SORT>(L, a, 5);
+        launch_num_strict<OffT, ValT, 256, SORT>(L, a, 4);
+        launch_num_strict<OffT, ValT, 128, SORT>(L, a, 3);
+        launch_num_strict<OffT, ValT, 64, SORT>(L, a, 2);
+        launch_num_strict<OffT, ValT, 32, SORT>(L, a, 1);
+    } else {
+        launch_num_warp<OffT, ValT, 1024, SORT>(L, a, 5);
+        launch_num_warp<OffT, ValT, 512, SORT>(L, a, 4);
+        launch_num_warp<OffT, ValT, 256, SORT>(L, a, 3);
+        launch_num_warp<OffT, ValT, 128, SORT>(L, a, 2);
+        launch_num_warp<OffT, ValT, 64, SORT>(L, a, 1);
+    }
+}
+
+void numeric_bins(Launch& L, const NumArgs& a, cudaStream_t dense_stream) {
+    if (a.A.nrows == 0) return;
+    if (a.off64) {
+        if (a.f64) {
+            if (a.sort) numeric_bins_t<int64_t, double, true>(L, a, dense_stream);
+            else numeric_bins_t<int64_t, double, false>(L, a, dense_stream);
+        } else {
+            if (a.sort) numeric_bins_t<int64_t, float, true>(L, a, dense_stream);
+            else numeric_bins_t<int64_t, float, false>(L, a, dense_stream);
+        }
+    } else {
+        if (a.f64) {
+            if (a.sort) numeric_bins_t<int32_t, double, true>(L, a, dense_stream);
+            else numeric_bins_t<int32_t, double, false>(L, a, dense_stream);
+        } else {
+            if (a.sort) numeric_bins_t<int32_t, float, true>(L, a, dense_stream);
+            else numeric_bins_t<int32_t, float, false>(L, a, dense_stream);
+        }
+    }
+}
+
+}  // namespace kk

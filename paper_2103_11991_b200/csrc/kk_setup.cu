@@ -1,0 +1,469 @@
+// kk_setup.cu -- a1-a4, a6: status block, B check/compression, row flops + bins, scans, binning.
+//
+//   a4 k_check_compress   B -> B_C (word, mask) pairs + sortedness flags
+//   a1 k_row_flops        per-row multiply-adds + symbolic work bin
+//   a2/a6 k_scan_*        device exclusive scans (flops, row map)
+//   a3 k_bin_*            stable row binning by work
+#include "kk_device.cuh"
+
+namespace kk {
+// ------------------------------------------------------------------------------------
+// status init
+// ------------------------------------------------------------------------------------
+__global__ void k_init_status(DevStatus* st) {
+    if (threadIdx.x == 0) {
+        st->total_flops = 0;
+        st->total_words = 0;
+        st->nnz_c = 0;
+        st->b_sorted = 1;
+        st->b_strict = 1;
+        st->bad_index = 0;
+        st->overflow = 0;
+        st->use_comp = 0;
+        st->pad = 0;
+    }
+    if (threadIdx.x <= NB) {
+        st->sym_bin_start[threadIdx.x] = 0;
+        st->num_bin_start[threadIdx.x] = 0;
+    }
+}
+
+void init_status(Launch& L, DevStatus* st) {
+    L.begin("init_status", L.stream);
+    k_init_status<<<1, 32, 0, L.stream>>>(st);
+    L.end(L.stream);
+}
+
+// ------------------------------------------------------------------------------------
+// a4: sortedness check + compression of B into B_C
+// One warp per row of B, 32 entries per step.  Adjacent equal words are merged with a
+// segmented OR scan; a word run that crosses a 32-entry chunk is carried in registers.
+// ------------------------------------------------------------------------------------
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_check_compress(int64_t n, int64_t k, const OffT* __restrict__ brm,
+                                                        const int32_t* __restrict__ bent, int do_comp,
+                                                        int validate, int32_t* __restrict__ bc_len,
+                                                        uint2* __restrict__ pairs, DevStatus* st) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    bool unsorted = false, nonstrict = false, bad = false;
+    unsigned long long words = 0;
+    for (int64_t j = gw; j < n; j += nw) {
+        const int64_t s = ld(brm, j), e = ld(brm, j + 1);
+        int prev_last = INT_MIN;
+        int cw = -1;
+        unsigned cm = 0;
+        int outn = 0;
+        for (int64_t c0 = s; c0 < e; c0 += 32) {
+            const int64_t q = c0 + lane;
+            const bool act = q < e;
+            const int nact = (int)min((int64_t)32, e - c0);
+            const int col = act ? __ldg(bent + q) : INT_MAX;
+            int prev = __shfl_up_sync(FULL, col, 1);
+            if (lane == 0) prev = prev_last;
+            if (act) {
+                unsorted |= col < prev;
+                nonstrict |= col <= prev;
+                bad |= (col < 0) || ((int64_t)col >= k);
+            }
+            prev_last = __shfl_sync(FULL, col, nact - 1);
+            if (do_comp) {
+                const int w = act ? (col >> 5) : INT_MAX;
+                const unsigned bit = act ? (1u << (col & 31)) : 0u;
+                int pw = __shfl_up_sync(FULL, w, 1);
+                if (lane == 0) pw = cw;
+                const bool head = act && (w != pw);
+                const unsigned heads = __ballot_sync(FULL, head);
+                if (cw >= 0 && (heads & 1u)) {  // the carried run ends before this chunk
+                    if (lane == 0) pairs[s + outn] = make_uint2((unsigned)cw, cm);
+                    ++outn;
+                    cw = -1;
+                    cm = 0;
+                }
+                const unsigned le = heads & lanemask_le();
+                const int seg = le ? (31 - __clz(le)) : 0;
+                unsigned v = bit;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const unsigned t = __shfl_up_sync(FULL, v, d);
+                    if (lane >= d && lane - d >= seg) v |= t;
+                }
+                if (!le) v |= cm;  // continuation of the carried run
+                const bool flush = act && lane != nact - 1 && ((heads >> (lane + 1)) & 1u);
+                const unsigned fb = __ballot_sync(FULL, flush);
+                if (flush) pairs[s + outn + __popc(fb & lanemask_lt())] = make_uint2((unsigned)w, v);
+                outn += __popc(fb);
+                cw = __shfl_sync(FULL, w, nact - 1);
+                cm = __shfl_sync(FULL, v, nact - 1);
+            }
+        }
+        if (do_comp) {
+            if (cw >= 0) {
+                if (lane == 0) pairs[s + outn] = make_uint2((unsigned)cw, cm);
+                ++outn;
+            }
+            if (lane == 0) bc_len[j] = outn;
+            words += (unsigned long long)outn;
+        }
+    }
+    if (__any_sync(FULL, unsorted) && lane == 0) atomicAnd(&st->b_sorted, 0);
+    if (__any_sync(FULL, nonstrict) && lane == 0) atomicAnd(&st->b_strict, 0);
+    if (validate && __any_sync(FULL, bad) && lane == 0) atomicOr(&st->bad_index, 1);
+    if (do_comp && lane == 0 && words) atomicAdd(&st->total_words, words);
+}
+
+static int grid_for(int64_t warps_needed, int threads, int num_sms, int per_sm = 8) {
+    int64_t blocks = (warps_needed * 32 + threads - 1) / threads;
+    int64_t cap = (int64_t)num_sms * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    return (int)blocks;
+}
+
+void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_comp, bool validate,
+                    int32_t* bc_len, uint2* pairs, DevStatus* st) {
+    if (B.nrows == 0) return;
+    const int threads = 256;
+    const int grid = grid_for(B.nrows, threads, L.num_sms, 16);
+    L.begin(do_comp ? "check_compress" : "check_sorted", L.stream);
+    if (off64)
+        k_check_compress<int64_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int64_t*)B.row_map, B.entries,
+                                                                  do_comp, validate, bc_len, pairs, st);
+    else
+        k_check_compress<int32_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int32_t*)B.row_map, B.entries,
+                                                                  do_comp, validate, bc_len, pairs, st);
+    L.end(L.stream);
+}
+
+// ------------------------------------------------------------------------------------
+// a1: per-row flops and the symbolic work bin of each row.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int sym_bin_of(int64_t ub) {
+    if (ub <= 0) return 0;
+    int b = 1;
+    int64_t cap = 64;
+    while (cap < ub && b < SYM_DENSE_BIN) {
+        cap <<= 1;
+        ++b;
+    }
+    return b;
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t k, const OffT* __restrict__ arm,
+                                                   const int32_t* __restrict__ aent, const OffT* __restrict__ brm,
+                                                   const int32_t* __restrict__ bc_len, int comp_mode, int64_t nnzB,
+                                                   int validate, int64_t* __restrict__ flops,
+                                                   uint8_t* __restrict__ binid, int32_t* __restrict__ counts,
+                                                   DevStatus* st) {
+    bool comp = false;
+    if (comp_mode == 1)
+        comp = true;
+    else if (comp_mode == -1)
+        comp = nnzB > 0 && (st->total_words * 4ull <= (unsigned long long)nnzB * 3ull);
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->use_comp = comp ? 1 : 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t kw = (k + 31) >> 5;
+    unsigned long long tot = 0;
+    bool bad = false;
+    for (int64_t i = gw; i < m; i += nw) {
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        int64_t f = 0, fc = 0;
+        for (int64_t p = s + lane; p < e; p += 32) {
+            const int j = __ldg(aent + p);
+            if (validate && (j < 0 || (int64_t)j >= n)) {
+                bad = true;
+                continue;
+            }
+            f += ld(brm, (int64_t)j + 1) - ld(brm, (int64_t)j);
+            if (comp) fc += __ldg(bc_len + j);
+        }
+        f = warp_sum(f);
+        if (comp) fc = warp_sum(fc);
+        if (lane == 0) {
+            flops[i] = f;
+            const int64_t ub = comp ? min(fc, kw) : min(f, k);
+            const int b = sym_bin_of(ub);
+            binid[i] = (uint8_t)b;
+            if (b == 0) counts[i] = 0;
+            tot += (unsigned long long)f;
+        }
+    }
+    if (validate && __any_sync(FULL, bad) && lane == 0) atomicOr(&st->bad_index, 1);
+    if (lane == 0 && tot) atomicAdd(&st->total_flops, tot);
+}
+
+void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, int64_t k, int comp_mode,
+                   bool validate, const int32_t* bc_len, int64_t* flops, uint8_t* binid, int32_t* counts,
+                   DevStatus* st) {
+    if (A.nrows == 0) return;
+    const int threads = 256;
+    const int grid = grid_for(A.nrows, threads, L.num_sms, 16);
+    L.begin("row_flops_bin", L.stream);
+    if (off64)
+        k_row_flops<int64_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int64_t*)A.row_map,
+                                                             A.entries, (const int64_t*)B.row_map, bc_len,
+                                                             comp_mode, B.nnz, validate, flops, binid, counts, st);
+    else
+        k_row_flops<int32_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int32_t*)A.row_map,
+                                                             A.entries, (const int32_t*)B.row_map, bc_len,
+                                                             comp_mode, B.nnz, validate, flops, binid, counts, st);
+    L.end(L.stream);
+}
+
+// ------------------------------------------------------------------------------------
+// a2 / a6: exclusive scan (reduce -> scan partials -> downsweep), int64 accumulation.
+// ------------------------------------------------------------------------------------
+constexpr int SCAN_THREADS = 512;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+int64_t scan_partial_len(int64_t m) { return (m + SCAN_TILE - 1) / SCAN_TILE + 2; }
+
+// block-wide exclusive scan of one int64 per thread; returns the block total
+__device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* excl) {
+    __shared__ int64_t wsum[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    int64_t x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int64_t t = __shfl_up_sync(FULL, x, d);
+        if (lane >= d) x += t;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = lane < nwarp ? wsum[lane] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int64_t t = __shfl_up_sync(FULL, w, d);
+            if (lane >= d) w += t;
+        }
+        wsum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int64_t wbase = warp ? wsum[warp - 1] : 0;
+    const int64_t total = wsum[nwarp - 1];
+    *excl = wbase + x - v;
+    __syncthreads();
+    return total;
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(int64_t m, const InT* __restrict__ in,
+                                                              int64_t* __restrict__ partial) {
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+    int64_t s = 0;
+#pragma unroll
+    for (int t = 0; t < SCAN_ITEMS; ++t) {
+        const int64_t i = base + t * SCAN_THREADS + threadIdx.x;
+        if (i < m) s += (int64_t)in[i];
+    }
+    s = warp_sum(s);
+    __shared__ int64_t ws[SCAN_THREADS / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int64_t v = threadIdx.x < SCAN_THREADS / 32 ? ws[threadIdx.x] : 0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) partial[blockIdx.x] = v;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_partials(int64_t nb, int64_t* __restrict__ partial,
+                                                        unsigned long long* total_dst) {
+    int64_t carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += blockDim.x) {
+        const int64_t b = b0 + threadIdx.x;
+        const int64_t v = b < nb ? partial[b] : 0;
+        int64_t ex;
+        const int64_t tot = block_exclusive_scan(v, &ex);
+        if (b < nb) partial[b] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) {
+        partial[nb] = carry;
+        if (total_dst) *total_dst = (unsigned long long)carry;
+    }
+}
+
+template <typename InT, typename OutT>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(int64_t m, const InT* __restrict__ in,
+                                                            const int64_t* __restrict__ partial,
+                                                            OutT* __restrict__ out, int64_t nb, int* overflow) {
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    int64_t v[SCAN_ITEMS];
+    int64_t s = 0;
+#pragma unroll
+    for (int t = 0; t < SCAN_ITEMS; ++t) {
+        const int64_t i = base + t;
+        v[t] = i < m ? (int64_t)in[i] : 0;
+        s += v[t];
+    }
+    int64_t ex;
+    block_exclusive_scan(s, &ex);
+    int64_t run = partial[blockIdx.x] + ex;
+#pragma unroll
+    for (int t = 0; t < SCAN_ITEMS; ++t) {
+        const int64_t i = base + t;
+        if (i < m) out[i] = (OutT)run;
+        run += v[t];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        const int64_t total = partial[nb];
+        out[m] = (OutT)total;
+        if (sizeof(OutT) == 4 && total > (int64_t)INT_MAX && overflow) *overflow = 1;
+    }
+}
+
+void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out, int64_t m, int64_t* partial,
+                    unsigned long long* total_dst, int* overflow) {
+    const int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
+    if (nb == 0) {
+        // m == 0: out[0] = 0, total = 0
+        cudaMemsetAsync(out, 0, out64 ? 8 : 4, L.stream);
+        if (total_dst) cudaMemsetAsync(total_dst, 0, 8, L.stream);
+        return;
+    }
+    L.begin("exclusive_scan", L.stream);
+    if (in64)
+        k_scan_reduce<int64_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int64_t*)in, partial);
+    else
+        k_scan_reduce<int32_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int32_t*)in, partial);
+    k_scan_partials<<<1, 1024, 0, L.stream>>>(nb, partial, total_dst);
+    if (in64 && out64)
+        k_scan_down<int64_t, int64_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int64_t*)in, partial,
+                                                                                  (int64_t*)out, nb, overflow);
+    else if (in64)
+        k_scan_down<int64_t, int32_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int64_t*)in, partial,
+                                                                                  (int32_t*)out, nb, overflow);
+    else if (out64)
+        k_scan_down<int32_t, int64_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int32_t*)in, partial,
+                                                                                  (int64_t*)out, nb, overflow);
+    else
+        k_scan_down<int32_t, int32_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int32_t*)in, partial,
+                                                                                  (int32_t*)out, nb, overflow);
+    L.end(L.stream, 3);
+}
+
+// ------------------------------------------------------------------------------------
+// a3: numeric bin ids from exact row counts, and stable binning of rows.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int num_bin_of(int64_t nnz) {
+    if (nnz <= 0) return 0;
+    int b = 1;
+    int64_t cap = 32;
+    while (cap < nnz && b < NUM_DENSE_BIN) {
+        cap <<= 1;
+        ++b;
+    }
+    return b;
+}
+
+__global__ void __launch_bounds__(256) k_numeric_binid(int64_t m, const int32_t* __restrict__ counts,
+                                                       uint8_t* __restrict__ binid) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        binid[i] = (uint8_t)num_bin_of(counts[i]);
+}
+
+void numeric_binid(Launch& L, int64_t m, const int32_t* counts, uint8_t* binid) {
+    if (m == 0) return;
+    int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)L.num_sms * 16);
+    L.begin("numeric_binid", L.stream);
+    k_numeric_binid<<<grid, 256, 0, L.stream>>>(m, counts, binid);
+    L.end(L.stream);
+}
+
+constexpr int BCHUNK = 2048;  // rows per warp in the binning passes
+
+int64_t bin_scratch_len(int64_t m) { return ((m + BCHUNK - 1) / BCHUNK) * NB + NB + 1; }
+
+// pass 1: per-chunk bin histogram (warp per chunk; lane b counts bin b)
+__global__ void __launch_bounds__(256) k_bin_count(int64_t m, const uint8_t* __restrict__ binid,
+                                                   int32_t* __restrict__ chunkcnt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nchunks = (m + BCHUNK - 1) / BCHUNK;
+    if (c >= nchunks) return;
+    const int64_t r0 = c * BCHUNK, r1 = min(m, r0 + BCHUNK);
+    int cnt = 0;
+    for (int64_t base = r0; base < r1; base += 32) {
+        const int64_t r = base + lane;
+        const int b = r < r1 ? (int)binid[r] : 255;
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+            const unsigned bal = __ballot_sync(FULL, b == t);
+            if (lane == t) cnt += __popc(bal);
+        }
+    }
+    if (lane < NB) chunkcnt[c * NB + lane] = cnt;
+}
+
+// pass 2: per bin, exclusive scan over chunks (+ bin start); one block
+__global__ void __launch_bounds__(1024) k_bin_offsets(int64_t nchunks, int32_t* __restrict__ chunkcnt,
+                                                      int* __restrict__ bin_start_dst) {
+    __shared__ int64_t totals[NB];
+    for (int b = 0; b < NB; ++b) {
+        int64_t carry = 0;
+        for (int64_t c0 = 0; c0 < nchunks; c0 += blockDim.x) {
+            const int64_t c = c0 + threadIdx.x;
+            const int64_t v = c < nchunks ? chunkcnt[c * NB + b] : 0;
+            int64_t ex;
+            const int64_t tot = block_exclusive_scan(v, &ex);
+            if (c < nchunks) chunkcnt[c * NB + b] = (int32_t)(carry + ex);
+            carry += tot;
+        }
+        if (threadIdx.x == 0) totals[b] = carry;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        int64_t run = 0;
+        for (int b = 0; b < NB; ++b) {
+            bin_start_dst[b] = (int)run;
+            run += totals[b];
+        }
+        bin_start_dst[NB] = (int)run;
+    }
+}
+
+// pass 3: stable scatter of rows into perm
+__global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const uint8_t* __restrict__ binid,
+                                                     const int32_t* __restrict__ chunkcnt,
+                                                     const int* __restrict__ bin_start, int32_t* __restrict__ perm) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nchunks = (m + BCHUNK - 1) / BCHUNK;
+    if (c >= nchunks) return;
+    const int64_t r0 = c * BCHUNK, r1 = min(m, r0 + BCHUNK);
+    int run = lane < NB ? bin_start[lane] + chunkcnt[c * NB + lane] : 0;
+    for (int64_t base = r0; base < r1; base += 32) {
+        const int64_t r = base + lane;
+        const int b = r < r1 ? (int)binid[r] : 255;
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+            const unsigned bal = __ballot_sync(FULL, b == t);
+            const int base_t = __shfl_sync(FULL, run, t);
+            if (b == t) perm[base_t + __popc(bal & lanemask_lt())] = (int32_t)r;
+            if (lane == t) run += __popc(bal);
+        }
+    }
+}
+
+void bin_rows(Launch& L, int64_t m, const uint8_t* binid, int32_t* scratch, int32_t* perm, int* bin_start_dst) {
+    const int64_t nchunks = (m + BCHUNK - 1) / BCHUNK;
+    if (nchunks == 0) {
+        cudaMemsetAsync(bin_start_dst, 0, sizeof(int) * (NB + 1), L.stream);
+        return;
+    }
+    const int grid = (int)((nchunks * 32 + 255) / 256);
+    L.begin("bin_rows", L.stream);
+    k_bin_count<<<grid, 256, 0, L.stream>>>(m, binid, scratch);
+    k_bin_offsets<<<1, 1024, 0, L.stream>>>(nchunks, scratch, bin_start_dst);
+    k_bin_scatter<<<grid, 256, 0, L.stream>>>(m, binid, scratch, bin_start_dst, perm);
+    L.end(L.stream, 3);
+}
+
+}  // namespace kk

@@ -1,0 +1,214 @@
+// kk_symbolic.cu -- a5: symbolic phase (bit vector PAPER.md:180).
+//
+//   k_sym_warp<S>   warp-owned shared-memory hash over B_C words, accum = OR
+//   k_sym_dense     CTA-owned dense bit vector over column windows
+#include "kk_device.cuh"
+
+namespace kk {
+// ------------------------------------------------------------------------------------
+// a5: symbolic, warp-owned shared hash ("HashmapAccumulator"; accum = OR
+// with compression, set insert without).  Each warp owns one row at a time; G lanes
+// walk one B row, 32/G rows of B in flight per step ("entries in each
+// referenced row of B are processed using vector parallelism").
+// ------------------------------------------------------------------------------------
+template <typename OffT, int S>
+__global__ void __launch_bounds__(256) k_sym_warp(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                  const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                                  const int32_t* __restrict__ bc_len, const uint2* __restrict__ pairs,
+                                                  const int32_t* __restrict__ perm, const int* __restrict__ bin_start,
+                                                  int bin, int logG, int32_t* __restrict__ counts,
+                                                  const DevStatus* __restrict__ st) {
+    extern __shared__ uint32_t sm_sym[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    uint32_t* keys = sm_sym + (size_t)warp * 2 * S;
+    uint32_t* masks = keys + S;
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    if (r0 + blockIdx.x * warps + warp >= r1) return;
+    for (int t = lane; t < S; t += 32) {
+        keys[t] = EMPTY;
+        masks[t] = 0;
+    }
+    __syncwarp();
+    const bool comp = st->use_comp != 0;
+    const int G = 1 << logG, per = 32 >> logG, gl = lane & (G - 1), sub = lane >> logG;
+    for (int r = r0 + blockIdx.x * warps + warp; r < r1; r += gridDim.x * warps) {
+        const int i = perm[r];
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        int cnt = 0;
+        for (int64_t p0 = s; p0 < e; p0 += per) {
+            const int64_t p = p0 + sub;
+            if (p < e) {
+                const int j = __ldg(aent + p);
+                const int64_t bs = ld(brm, j);
+                bool fresh;
+                if (comp) {
+                    const int64_t be = bs + __ldg(bc_len + j);
+                    for (int64_t q = bs + gl; q < be; q += G) {
+                        const uint2 pr = __ldg(pairs + q);
+                        const uint32_t h = probe_claim<S>(keys, pr.x, &fresh);
+                        atomicOr(&masks[h], pr.y);
+                    }
+                } else {
+                    const int64_t be = ld(brm, j + 1);
+                    for (int64_t q = bs + gl; q < be; q += G) {
+                        probe_claim<S>(keys, (uint32_t)__ldg(bent + q), &fresh);
+                        cnt += fresh;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        for (int t = lane; t < S; t += 32) {
+            if (keys[t] != EMPTY) {
+                if (comp) cnt += __popc(masks[t]);
+                keys[t] = EMPTY;
+                masks[t] = 0;
+            }
+        }
+        cnt = warp_sum(cnt);
+        if (lane == 0) counts[i] = cnt;
+        __syncwarp();
+    }
+}
+
+// a5 for rows whose bound exceeds the warp tables: the paper's dense bit-vector
+// accumulator in one CTA's shared memory, over windows of `wbits`
+// columns when k is larger.  Sorted B rows are resumed from per-entry cursors.
+template <typename OffT>
+__global__ void __launch_bounds__(512) k_sym_dense(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                   const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                                   const int32_t* __restrict__ bc_len,
+                                                   const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
+                                                   const int* __restrict__ bin_start, int bin, int64_t k,
+                                                   int64_t wbits, int32_t* __restrict__ cursors,
+                                                   int32_t* __restrict__ counts, const DevStatus* __restrict__ st) {
+    extern __shared__ uint32_t bmp[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    if (r0 + (int)blockIdx.x >= r1) return;
+    const int64_t maxw = wbits >> 5;
+    for (int64_t t = threadIdx.x; t < maxw; t += blockDim.x) bmp[t] = 0;
+    __syncthreads();
+    const bool comp = st->use_comp != 0;
+    const bool sorted = st->b_sorted != 0;
+    for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+        const int i = perm[r];
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        long long cnt = 0;
+        for (int64_t lo = 0; lo < k; lo += wbits) {
+            const int64_t hi = min(k, lo + wbits);
+            const bool single = (lo == 0 && hi == k);
+            const int64_t low = lo >> 5, hiw = (hi + 31) >> 5;
+            for (int64_t p = s + warp; p < e; p += warps) {
+                const int j = __ldg(aent + p);
+                const int64_t bs = ld(brm, j);
+                if (comp) {
+                    const int64_t be = bs + __ldg(bc_len + j);
+                    if (single) {
+                        for (int64_t q = bs + lane; q < be; q += 32) {
+                            const uint2 pr = __ldg(pairs + q);
+                            atomicOr(&bmp[pr.x], pr.y);
+                        }
+                    } else if (sorted) {
+                        const int64_t q0 = bs + (lo == 0 ? 0 : cursors[p]);
+                        const int64_t qn = walk_sorted(
+                            q0, be, hiw, [&](int64_t q) { return (int64_t)__ldg(&pairs[q].x); },
+                            [&](int64_t q, int64_t w) { atomicOr(&bmp[w - low], __ldg(&pairs[q].y)); });
+                        if (lane == 0) cursors[p] = (int32_t)(qn - bs);
+                    } else {
+                        for (int64_t q = bs + lane; q < be; q += 32) {
+                            const uint2 pr = __ldg(pairs + q);
+                            if ((int64_t)pr.x >= low && (int64_t)pr.x < hiw) atomicOr(&bmp[pr.x - low], pr.y);
+                        }
+                    }
+                } else {
+                    const int64_t be = ld(brm, j + 1);
+                    if (single) {
+                        for (int64_t q = bs + lane; q < be; q += 32) {
+                            const int c = __ldg(bent + q);
+                            atomicOr(&bmp[c >> 5], 1u << (c & 31));
+                        }
+                    } else if (sorted) {
+                        const int64_t q0 = bs + (lo == 0 ? 0 : cursors[p]);
+                        const int64_t qn = walk_sorted(
+                            q0, be, hi, [&](int64_t q) { return (int64_t)__ldg(bent + q); },
+                            [&](int64_t q, int64_t c) { atomicOr(&bmp[(c - lo) >> 5], 1u << (c & 31)); });
+                        if (lane == 0) cursors[p] = (int32_t)(qn - bs);
+                    } else {
+                        for (int64_t q = bs + lane; q < be; q += 32) {
+                            const int c = __ldg(bent + q);
+                            if (c >= lo && c < hi) atomicOr(&bmp[(c - lo) >> 5], 1u << (c & 31));
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            const int64_t nw = hiw - low;
+            for (int64_t t = threadIdx.x; t < nw; t += blockDim.x) {
+                const uint32_t v = bmp[t];
+                if (v) {
+                    cnt += __popc(v);
+                    bmp[t] = 0;
+                }
+            }
+            __syncthreads();
+        }
+        cnt = block_sum(cnt);
+        if (threadIdx.x == 0) counts[i] = (int32_t)cnt;
+    }
+}
+
+static int sym_warps_for(int S) { return S <= 512 ? 8 : (S == 1024 ? 4 : (S == 2048 ? 2 : 1)); }
+
+template <typename OffT, int S>
+static void launch_sym_warp(Launch& L, const SymArgs& a, int bin) {
+    const int warps = sym_warps_for(S);
+    const size_t smem = (size_t)warps * 2 * S * sizeof(uint32_t);
+    auto kern = k_sym_warp<OffT, S>;
+    KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    int grid = c.grid_cap;
+    int64_t need = (a.A.nrows + warps - 1) / warps;
+    if (need < grid) grid = (int)(need > 0 ? need : 1);
+    L.begin(kname("sym_warp", S), L.stream);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+                                               a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.logG,
+                                               a.counts, a.st);
+    L.end(L.stream);
+}
+
+template <typename OffT>
+static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stream) {
+    // dense rows first (heaviest), on their own stream when given
+    {
+        const int threads = 512;
+        int64_t wbits = 200 * 1024 * 8;  // 200 KB bit vector
+        const int64_t k32 = ((a.k + 31) / 32) * 32;
+        if (k32 < wbits) wbits = k32 > 0 ? k32 : 32;
+        const size_t smem = (size_t)(wbits / 8);
+        auto kern = k_sym_dense<OffT>;
+        KCfg c = kernel_cfg(kern, threads, smem, L.num_sms);
+        cudaStream_t s = dense_stream ? dense_stream : L.stream;
+        L.begin("sym_dense", s);
+        kern<<<c.grid_cap, threads, smem, s>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+                                               a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, SYM_DENSE_BIN,
+                                               a.k, wbits, a.cursors, a.counts, a.st);
+        L.end(s);
+    }
+    launch_sym_warp<OffT, 4096>(L, a, 7);
+    launch_sym_warp<OffT, 2048>(L, a, 6);
+    launch_sym_warp<OffT, 1024>(L, a, 5);
+    launch_sym_warp<OffT, 512>(L, a, 4);
+    launch_sym_warp<OffT, 256>(L, a, 3);
+    launch_sym_warp<OffT, 128>(L, a, 2);
+    launch_sym_warp<OffT, 64>(L, a, 1);
+}
+
+void symbolic_bins(Launch& L, const SymArgs& a, cudaStream_t dense_stream) {
+    if (a.A.nrows == 0) return;
+    if (a.off64)
+        symbolic_bins_t<int64_t>(L, a, dense_stream);
+    else
+        symbolic_bins_t<int32_t>(L, a, dense_stream);
+}
+
+}  // namespace kk

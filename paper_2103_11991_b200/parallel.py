@@ -93,9 +93,13 @@ def allgather_nnz(nnz_local: int, device, group=None) -> List[int]:
     """All-gather one int64 nnz(C_p) per rank."""
     world = dist.get_world_size(group)
     mine = torch.tensor([int(nnz_local)], dtype=torch.int64, device=device)
-    allv = torch.zeros(world, dtype=torch.int64, device=device)
-    dist.all_gather_into_tensor(allv, mine, group=group)
-    return [int(x) for x in allv.tolist()]
+    if dist.get_backend(group) == "nccl":
+        allv = torch.zeros(world, dtype=torch.int64, device=device)
+        dist.all_gather_into_tensor(allv, mine, group=group)
+        return [int(x) for x in allv.tolist()]
+    parts = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    return [int(p.item()) for p in parts]
 
 
 class ShardedSpGEMM:

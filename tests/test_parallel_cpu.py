@@ -1,0 +1,114 @@
+"""Multi-GPU host logic on CPU: the flop-balanced row split, global offsets,
+and the collectives of paper_2103_11991_b200.parallel over gloo with world size 2.
+
+The partition arithmetic is checked without any GPU: the oracle's product of each row
+block, stitched with the all-gathered offsets, must equal the oracle's full product."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from workloads import generators as g
+
+
+def test_flop_balanced_cuts_basic():
+    from paper_2103_11991_b200.parallel import flop_balanced_cuts
+
+    F = np.concatenate([[0], np.cumsum([5, 5, 5, 5, 100, 5, 5, 5])])
+    cuts = flop_balanced_cuts(F, 2)
+    assert cuts[0] == 0 and cuts[-1] == 8 and cuts == sorted(cuts)
+    for world in (1, 2, 3, 8, 16):
+        c = flop_balanced_cuts(F, world)
+        assert len(c) == world + 1 and c[0] == 0 and c[-1] == 8 and c == sorted(c)
+    assert flop_balanced_cuts(np.zeros(1, dtype=np.int64), 4) == [0, 0, 0, 0, 0]
+
+
+def test_global_offsets():
+    from paper_2103_11991_b200.parallel import global_offsets
+
+    assert global_offsets([3, 0, 5, 2]) == [0, 3, 3, 8]
+    assert global_offsets([]) == []
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_row_split_stitches_to_full_product(oracle_mod, world):
+    """Oracle on each flop-balanced row block, stitched by global offsets == full oracle."""
+    from paper_2103_11991_b200.parallel import flop_balanced_cuts, global_offsets
+
+    A, B = g.config("C2", size=9, values="random")
+    f, tot = oracle_mod.row_flops(A, B)
+    F = np.concatenate([[0], np.cumsum(f)])
+    cuts = flop_balanced_cuts(F, world)
+    rm_full, ent_full, val_full, _ = oracle_mod.spgemm(A, B)
+    rms, ents, vals, nnzs = [], [], [], []
+    arm = A.row_map.numpy()
+    for p in range(world):
+        r0, r1 = cuts[p], cuts[p + 1]
+        s, e = int(arm[r0]), int(arm[r1])
+        Ap = g.CSR(r1 - r0, A.ncols, torch.tensor(arm[r0:r1 + 1] - s), A.entries[s:e], A.values[s:e])
+        rm, ent, val, _ = oracle_mod.spgemm(Ap, B)
+        rms.append(rm)
+        ents.append(ent)
+        vals.append(val)
+        nnzs.append(int(rm[-1]))
+    offs = global_offsets(nnzs)
+    stitched = np.concatenate([[0]] + [rms[p][1:] + offs[p] for p in range(world)])
+    assert np.array_equal(stitched, rm_full)
+    assert np.array_equal(np.concatenate(ents), ent_full)
+    assert np.array_equal(np.concatenate(vals), val_full)
+    # balance: no block carries more than its share plus one row's work
+    blk = [F[cuts[p + 1]] - F[cuts[p]] for p in range(world)]
+    assert max(blk) <= tot / world + f.max()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2103_11991_b200.parallel import allgather_nnz, broadcast_csr, global_offsets
+        from paper_2103_11991_b200.spgemm import CsrMatrix
+
+        if rank == 0:
+            A, _ = g.config("C1", size=6, values="random")
+            M = CsrMatrix(A.nrows, A.ncols, A.row_map, A.entries, A.values)
+        else:
+            M = None
+        R = broadcast_csr(M, src=0, device="cpu")
+        counts = allgather_nnz(10 * rank + 7, "cpu")
+        q.put((rank, R.nrows, R.ncols, R.row_map.tolist(), R.entries.tolist(), R.values.tolist(), counts,
+               global_offsets(counts)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_broadcast_and_allgather():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    A, _ = g.config("C1", size=6, values="random")
+    for r in res:
+        assert r[1] == A.nrows and r[2] == A.ncols
+        assert r[3] == A.row_map.tolist() and r[4] == A.entries.tolist() and r[5] == A.values.tolist()
+        assert r[6] == [7, 17] and r[7] == [0, 7]
