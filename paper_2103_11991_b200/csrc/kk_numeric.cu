@@ -2,6 +2,8 @@
 // (PAPER.md:621-647).
 #include "kk_device.cuh"
 
+#include <cstdlib>
+
 namespace kk {
 // ------------------------------------------------------------------------------------
 // a7: numeric, warp-owned shared hash (accum = +).  With G = 32
@@ -223,10 +225,15 @@ __global__ void __launch_bounds__(256) k_num_dense(const OffT* __restrict__ arm,
 // sort of those 32-bit words in registers, coalesced writes, and the table is reset at
 // exactly the slots that were used.
 // ------------------------------------------------------------------------------------
+// Probe position L in [0,S) (L = bank*R + row, R = S/32) -> slot row*32 + ((bank + 7*row) & 31).
+// A key starts at bank = col & 31, row = hash(col >> 5): consecutive columns of one
+// 32-column word sit in consecutive banks, and the 7*row rotation spreads keys of the
+// same bank (e.g. stencil planes 32k columns apart) over different physical banks.
 template <int S>
 __device__ __forceinline__ uint32_t bm_slot(uint32_t L) {
     constexpr int R = S / 32, LOGR = ilog2(R);
-    return (L & (R - 1)) * 32u + (L >> LOGR);
+    const uint32_t row = L & (R - 1);
+    return row * 32u + (((L >> LOGR) + 7u * row) & 31u);
 }
 
 template <int S>
@@ -235,44 +242,43 @@ __device__ __forceinline__ uint32_t bm_start(uint32_t col) {
     return (col & 31u) * R + (((col >> 5) * 0x9E3779B1u) >> (32 - LOGR));
 }
 
-// Find or claim `col` (lanes with act); returns its slot.  Keys of active lanes must be
-// distinct.  Warp-synchronous: all 32 lanes call it.  Lanes first probe on their own (a
-// hit needs no synchronisation); lanes that reach an EMPTY slot then claim it together:
-// write, __syncwarp, re-read; a lane whose write lost continues probing.  *won is set
-// for the lanes whose claim stuck (fresh keys).
+// Lane-local probe from position *L: stops at `col` or at an EMPTY slot; returns the key seen.
 template <int S>
-__device__ __forceinline__ uint32_t strict_claim(uint32_t* keys, uint32_t col, bool act, bool* won) {
+__device__ __forceinline__ uint32_t probe_local(const uint32_t* keys, uint32_t col, uint32_t& L, uint32_t& h) {
+    uint32_t k = keys[h];
+    while (k != col && k != EMPTY) {
+        L = (L + 1) & (S - 1);
+        h = bm_slot<S>(L);
+        k = keys[h];
+    }
+    return k;
+}
+
+// Find or claim `col` for the lanes with act; returns the slot.  Keys of the active
+// lanes may repeat (equal keys walk the same probe sequence and agree on the slot).
+// Lanes probe on their own; lanes that reach an EMPTY slot write their key, the warp
+// syncs, the lanes re-read, and a lane whose write lost probes on (rare).
+template <int S>
+__device__ __forceinline__ uint32_t strict_claim(uint32_t* keys, uint32_t col, bool act) {
     uint32_t L = bm_start<S>(col);
     uint32_t h = bm_slot<S>(L);
     bool need = false;
-    *won = false;
-    if (act) {
-        uint32_t k = keys[h];
-        while (k != col && k != EMPTY) {
+    if (act) need = probe_local<S>(keys, col, L, h) == EMPTY;
+    if (need) keys[h] = col;
+    __syncwarp();
+    bool lost = false;
+    if (need) lost = keys[h] != col;
+    while (__any_sync(FULL, lost)) {
+        __syncwarp();
+        bool again = false;
+        if (lost) {
             L = (L + 1) & (S - 1);
             h = bm_slot<S>(L);
-            k = keys[h];
-        }
-        need = (k == EMPTY);
-    }
-    while (__any_sync(FULL, need)) {
-        if (need) keys[h] = col;
-        __syncwarp();
-        if (need) {
-            uint32_t k = keys[h];
-            if (k == col) {
-                need = false;
-                *won = true;
-            } else {
-                do {
-                    L = (L + 1) & (S - 1);
-                    h = bm_slot<S>(L);
-                    k = keys[h];
-                } while (k != col && k != EMPTY);
-                need = (k == EMPTY);
-            }
+            again = probe_local<S>(keys, col, L, h) == EMPTY;
+            if (again) keys[h] = col;
         }
         __syncwarp();
+        lost = again && keys[h] != col;
     }
     return h;
 }
@@ -288,28 +294,23 @@ __device__ __forceinline__ uint32_t strict_find(const uint32_t* keys, uint32_t c
     return h;
 }
 
-// Per A entry of the current 32-entry chunk: start and length of its B row.
-template <typename OffT>
-struct StepInfoT {
-    OffT bb;
-    int bl;
-};
-template <>
-struct StepInfoT<int64_t> {
-    long long bb;
-    int bl;
-    int pad;
+// Per A entry of the current 32-entry chunk: pointers to its B row and the row length.
+template <typename ValT>
+struct StepPtr {
+    const int32_t* ent;
+    const ValT* val;
 };
 
-// Shared-memory layout of one warp: vals[S] | info[32] | av[32] | keys[S] | list[CAP]
-template <typename OffT, typename ValT, int S, int CAP>
+// Shared-memory layout of one warp: vals[S] | ptr[32] | av[32] | len[32] | keys[S] | stage[CAP]
+template <typename ValT, int S, int CAP>
 struct StrictLayout {
     static constexpr size_t vals = 0;
-    static constexpr size_t info = vals + (size_t)S * sizeof(ValT);
-    static constexpr size_t av = info + 32 * sizeof(StepInfoT<OffT>);
-    static constexpr size_t keys = (av + 32 * sizeof(ValT) + 15) / 16 * 16;
-    static constexpr size_t list = keys + (size_t)S * 4;
-    static constexpr size_t bytes = (list + (size_t)CAP * 4 + 15) / 16 * 16;
+    static constexpr size_t ptr = vals + (size_t)S * sizeof(ValT);
+    static constexpr size_t av = ptr + 32 * sizeof(StepPtr<ValT>);
+    static constexpr size_t len = av + 32 * sizeof(ValT);
+    static constexpr size_t keys = len + 32 * 4;
+    static constexpr size_t stage = keys + (size_t)S * 4;
+    static constexpr size_t bytes = (stage + (size_t)CAP * 4 + 15) / 16 * 16;
 };
 
 template <typename OffT, typename ValT, int S, int CAP, bool SORT>
@@ -319,42 +320,59 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
                                                     const OffT* __restrict__ crm, int32_t* __restrict__ cent,
                                                     ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                     const int* __restrict__ bin_start, int bin) {
-    using LY = StrictLayout<OffT, ValT, S, CAP>;
-    using SI = StepInfoT<OffT>;
+    using LY = StrictLayout<ValT, S, CAP>;
+    using SP = StepPtr<ValT>;
     constexpr int LOGS = ilog2(S);
     constexpr int E = CAP / 32;  // sort elements per lane
     extern __shared__ __align__(16) unsigned char sm_num[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     unsigned char* base = sm_num + (size_t)warp * LY::bytes;
     ValT* vals = (ValT*)(base + LY::vals);
-    SI* info = (SI*)(base + LY::info);
+    SP* ptr = (SP*)(base + LY::ptr);
     ValT* av = (ValT*)(base + LY::av);
+    int* len = (int*)(base + LY::len);
     uint32_t* keys = (uint32_t*)(base + LY::keys);
-    uint32_t* list = (uint32_t*)(base + LY::list);
+    uint32_t* stage = (uint32_t*)(base + LY::stage);
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
-    if (r0 + blockIdx.x * warps + warp >= r1) return;
+    const int stride = gridDim.x * warps;
+    int r = r0 + blockIdx.x * warps + warp;
+    if (r >= r1) return;
     for (int t = lane; t < S; t += 32) {
         keys[t] = EMPTY;
         vals[t] = (ValT)0;
     }
     __syncwarp();
-    for (int r = r0 + blockIdx.x * warps + warp; r < r1; r += gridDim.x * warps) {
-        const int i = perm[r];
-        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+    // software pipeline over rows: the next row's bounds and first 32 A entries are
+    // loaded during the current row's epilogue
+    int i = perm[r];
+    int64_t s = ld(arm, i), e = ld(arm, i + 1);
+    int jn = 0;
+    ValT an = (ValT)0;
+    if (lane < e - s) {
+        jn = __ldg(aent + s + lane);
+        an = __ldg(aval + s + lane);
+    }
+    while (true) {
         const int64_t cb = ld(crm, i);
         const int clen = (int)(ld(crm, i + 1) - cb);
-        int n = 0;  // keys claimed so far (warp-uniform)
+        const int rn = r + stride;
+        const int inext = rn < r1 ? perm[rn] : -1;
         for (int64_t c0 = s; c0 < e; c0 += 32) {
             const int na = (int)min((int64_t)32, e - c0);
+            int j = jn;
+            ValT a = an;
+            if (c0 != s && lane < na) {
+                j = __ldg(aent + c0 + lane);
+                a = __ldg(aval + c0 + lane);
+            }
             int bl = 0;
             if (lane < na) {
-                const int j = __ldg(aent + c0 + lane);
-                const ValT a = __ldg(aval + c0 + lane);
-                const OffT bb = __ldg(brm + j);
-                bl = (int)(__ldg(brm + j + 1) - bb);
-                info[lane].bb = bb;
-                info[lane].bl = bl;
+                const int64_t bb = ld(brm, j);
+                bl = (int)(ld(brm, j + 1) - bb);
+                ptr[lane].ent = bent + bb;
+                ptr[lane].val = bval + bb;
                 av[lane] = a;
+                len[lane] = bl;
             }
             unsigned rem = __ballot_sync(FULL, bl > 0);
             const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
@@ -362,83 +380,98 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
             if (!rem) continue;
             auto insert = [&](uint32_t col, ValT prod) {
                 const bool act = col != EMPTY;
-                bool won;
-                const uint32_t h = strict_claim<S>(keys, col, act, &won);
-                const unsigned wb = __ballot_sync(FULL, won);
-                if (won) list[n + __popc(wb & lanemask_lt())] = h;
-                n += __popc(wb);
+                const uint32_t h = strict_claim<S>(keys, col, act);
                 if (act) vals[h] += prod;
             };
             if (maxbl <= 32) {
-                // one step per B row: steps are the set bits of rem, loads two steps ahead
-                auto fetch = [&](unsigned& m, uint32_t& col, ValT& bv, ValT& a) {
+                // one step per B row (the set bits of rem); loads run 3 steps ahead
+                // (the product is formed at insert time, so no load is waited on early)
+                auto fetch = [&](uint32_t& col, ValT& bv, ValT& at) {
                     col = EMPTY;
                     bv = (ValT)0;
-                    a = (ValT)0;
-                    if (m) {
-                        const int t = __ffs(m) - 1;
-                        m &= m - 1;
-                        const SI si = info[t];
-                        a = av[t];
-                        if (lane < si.bl) {
-                            col = (uint32_t)__ldg(bent + si.bb + lane);
-                            bv = __ldg(bval + si.bb + lane);
-                        }
-                        return true;
+                    at = (ValT)0;
+                    if (!rem) return false;
+                    const int t = __ffs(rem) - 1;
+                    rem &= rem - 1;
+                    const SP sp = ptr[t];
+                    at = av[t];
+                    if (lane < len[t]) {
+                        col = (uint32_t)__ldg(sp.ent + lane);
+                        bv = __ldg(sp.val + lane);
                     }
-                    return false;
+                    return true;
                 };
-                uint32_t c0_, c1_, c2_;
-                ValT v0, v1, v2, a0, a1, a2;
-                bool h0 = fetch(rem, c0_, v0, a0);
-                bool h1 = fetch(rem, c1_, v1, a1);
-                while (h0) {
-                    const bool h2 = fetch(rem, c2_, v2, a2);
-                    insert(c0_, a0 * v0);
-                    h0 = h1;
-                    c0_ = c1_;
-                    v0 = v1;
-                    a0 = a1;
-                    h1 = h2;
-                    c1_ = c2_;
-                    v1 = v2;
-                    a1 = a2;
+                uint32_t k0, k1, k2, k3;
+                ValT b0, b1, b2, b3, a0, a1, a2, a3;
+                fetch(k0, b0, a0);
+                bool h1 = fetch(k1, b1, a1);
+                bool h2 = fetch(k2, b2, a2);
+                bool h3 = fetch(k3, b3, a3);
+                while (true) {
+                    insert(k0, a0 * b0);
+                    if (!h1) break;
+                    const bool h0 = fetch(k0, b0, a0);
+                    insert(k1, a1 * b1);
+                    if (!h2) break;
+                    h1 = fetch(k1, b1, a1);
+                    insert(k2, a2 * b2);
+                    if (!h3) break;
+                    h2 = fetch(k2, b2, a2);
+                    insert(k3, a3 * b3);
+                    if (!h0) break;
+                    h3 = fetch(k3, b3, a3);
                 }
             } else {
-                // long B rows: 32-entry segments, one ahead
+                // long B rows: 32-entry segments
                 while (rem) {
                     const int t = __ffs(rem) - 1;
                     rem &= rem - 1;
-                    const SI si = info[t];
-                    const ValT a = av[t];
-                    for (int q0 = 0; q0 < si.bl; q0 += 32) {
+                    const SP sp = ptr[t];
+                    const ValT at = av[t];
+                    const int blt = len[t];
+                    for (int q0 = 0; q0 < blt; q0 += 32) {
                         uint32_t col = EMPTY;
-                        ValT bv = (ValT)0;
-                        if (q0 + lane < si.bl) {
-                            col = (uint32_t)__ldg(bent + si.bb + q0 + lane);
-                            bv = __ldg(bval + si.bb + q0 + lane);
+                        ValT p = (ValT)0;
+                        if (q0 + lane < blt) {
+                            col = (uint32_t)__ldg(sp.ent + q0 + lane);
+                            p = at * __ldg(sp.val + q0 + lane);
                         }
-                        insert(col, a * bv);
+                        insert(col, p);
                     }
                 }
             }
             __syncwarp();
         }
-        // ---- epilogue: gather claimed slots, sort, write, reset ----
-        const int nn = min(n, clen);  // guard: never write past the row
-        if (SORT) {
-            uint32_t sv[E], kk[E];
-            uint32_t mn = 0xffffffffu, mx = 0u;
-#pragma unroll
-            for (int q = 0; q < E; ++q) {
-                const int idx = lane * E + q;
-                sv[q] = idx < n ? list[idx] : 0u;
-                kk[q] = idx < n ? keys[sv[q]] : 0u;
-                if (idx < n) {
-                    mn = min(mn, kk[q]);
-                    mx = max(mx, kk[q]);
-                }
+        // next row's bounds (their loads overlap the epilogue)
+        int64_t sn = 0, en = 0;
+        if (inext >= 0) {
+            sn = ld(arm, inext);
+            en = ld(arm, inext + 1);
+        }
+        // ---- epilogue: compaction (slot order), sort, coalesced write, reset ----
+        int n = 0;
+        uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll 4
+        for (int c = 0; c < S / 32; ++c) {
+            const uint32_t k = keys[c * 32 + lane];
+            const bool occ = k != EMPTY;
+            const unsigned bal = __ballot_sync(FULL, occ);
+            if (occ) {
+                const int pos = n + __popc(bal & lanemask_lt());
+                if (pos < CAP) stage[pos] = (uint32_t)(c * 32 + lane);
+                mn = min(mn, k);
+                mx = max(mx, k);
             }
+            n += __popc(bal);
+        }
+        __syncwarp();
+        // next row's first A entries
+        if (inext >= 0 && lane < en - sn) {
+            jn = __ldg(aent + sn + lane);
+            an = __ldg(aval + sn + lane);
+        }
+        const int nn = min(min(n, clen), CAP);  // guard: never write past the row
+        if (SORT) {
             mn = __reduce_min_sync(FULL, mn);
             mx = __reduce_max_sync(FULL, mx);
             const bool packed = (mx - mn) < ((1u << (32 - LOGS)) - 1u);
@@ -446,18 +479,24 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
 #pragma unroll
             for (int q = 0; q < E; ++q) {
                 const int idx = lane * E + q;
-                v[q] = idx < n ? (packed ? (((kk[q] - mn) << LOGS) | sv[q]) : kk[q]) : 0xffffffffu;
+                uint32_t w = 0xffffffffu;
+                if (idx < nn) {
+                    const uint32_t slot = stage[idx];
+                    const uint32_t k = keys[slot];
+                    w = packed ? (((k - mn) << LOGS) | slot) : k;
+                }
+                v[q] = w;
             }
             warp_bitonic_sort<E>(v);
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < E; ++q) {
                 const int idx = lane * E + q;
-                if (idx < n) list[idx] = v[q];
+                if (idx < nn) stage[idx] = v[q];
             }
             __syncwarp();
-            for (int t = lane; t < n; t += 32) {
-                const uint32_t w = list[t];
+            for (int t = lane; t < nn; t += 32) {
+                const uint32_t w = stage[t];
                 uint32_t slot, col;
                 if (packed) {
                     slot = w & (S - 1);
@@ -466,38 +505,39 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
                     col = w;
                     slot = strict_find<S>(keys, col);
                 }
-                if (t < nn) {
-                    cent[cb + t] = (int32_t)col;
-                    cval[cb + t] = vals[slot];
-                }
-                list[t] = slot;
+                cent[cb + t] = (int32_t)col;
+                cval[cb + t] = vals[slot];
             }
-            __syncwarp();
         } else {
             for (int t = lane; t < nn; t += 32) {
-                const uint32_t slot = list[t];
+                const uint32_t slot = stage[t];
                 cent[cb + t] = (int32_t)keys[slot];
                 cval[cb + t] = vals[slot];
             }
         }
         __syncwarp();
-        for (int t = lane; t < n; t += 32) {
-            const uint32_t slot = list[t];
-            keys[slot] = EMPTY;
-            vals[slot] = (ValT)0;
+#pragma unroll 4
+        for (int c = 0; c < S / 32; ++c) {
+            keys[c * 32 + lane] = EMPTY;
+            vals[c * 32 + lane] = (ValT)0;
         }
         __syncwarp();
+        if (inext < 0) break;
+        r = rn;
+        i = inext;
+        s = sn;
+        e = en;
     }
 }
 
 // rows of numeric bin `bin` hold nnz(C_i) <= CAP = 16 << bin; the table has S = 4*CAP slots
-template <typename OffT, typename ValT, int CAP, bool SORT>
-static void launch_num_strict(Launch& L, const NumArgs& a, int bin) {
-    constexpr int S = 4 * CAP;
+template <typename OffT, typename ValT, int CAP, int F, bool SORT>
+static void launch_num_strict_f(Launch& L, const NumArgs& a, int bin) {
+    constexpr int S = F * CAP;
     const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
     if (rows <= 0) return;
     const int warps = CAP <= 128 ? 8 : 4;
-    const size_t smem = (size_t)warps * StrictLayout<OffT, ValT, S, CAP>::bytes;
+    const size_t smem = (size_t)warps * StrictLayout<ValT, S, CAP>::bytes;
     auto kern = k_num_strict<OffT, ValT, S, CAP, SORT>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (rows + warps - 1) / warps;
@@ -508,6 +548,24 @@ static void launch_num_strict(Launch& L, const NumArgs& a, int bin) {
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
                                                a.bin_start, bin);
     L.end(L.stream);
+}
+
+// table factor S / CAP (load factor <= 1/F).  F = 2 measured faster than 4 on C2 (smaller
+// tables -> more resident warps); KK_NUM_TABLE_FACTOR=4 selects 4 (experiments).
+static int num_table_factor() {
+    static int f = [] {
+        const char* v = getenv("KK_NUM_TABLE_FACTOR");
+        return (v && atoi(v) == 4) ? 4 : 2;
+    }();
+    return f;
+}
+
+template <typename OffT, typename ValT, int CAP, bool SORT>
+static void launch_num_strict(Launch& L, const NumArgs& a, int bin) {
+    if (num_table_factor() == 4)
+        launch_num_strict_f<OffT, ValT, CAP, 4, SORT>(L, a, bin);
+    else
+        launch_num_strict_f<OffT, ValT, CAP, 2, SORT>(L, a, bin);
 }
 
 template <typename OffT, typename ValT, int S, bool SORT>
