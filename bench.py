@@ -203,8 +203,14 @@ def cpu_baseline(A, B, seconds, rows):
     oracle.build()
     cores = len(os.sched_getaffinity(0))
     oracle.set_num_threads(cores)
-    Bh = B.to(device="cpu", value_dtype=torch.float64, offset_dtype=torch.int64)
-    As, r0 = oracle_sample(A.to(device="cpu", value_dtype=torch.float64, offset_dtype=torch.int64), rows)
+    from workloads import generators as g
+
+    def host(M):
+        return g.CSR(M.nrows, M.ncols, M.row_map.to(torch.int64).cpu(), M.entries.cpu(),
+                     M.values.to(torch.float64).cpu())
+
+    Bh = host(B)
+    As, r0 = oracle_sample(host(A), rows)
     f, muladds = oracle.row_flops(As, Bh)
     tot, reps = 0.0, 0
     while reps < 1 or (tot < seconds and reps < 50):

@@ -83,6 +83,10 @@ typedef struct {
     int num_streams;   /* internal streams used to overlap work bins (default 2, 1 = none) */
     int timing;        /* 1: bracket every kernel launch with CUDA events on the stream it is
                           launched on (read with kk_spgemm_kernel_times); default 0 */
+    int patterns;      /* 1 (default): symbolic keeps the compressed pattern of rows that fit
+                          (sorted (word, mask) pairs, <= 64 words) in the handle, and numeric
+                          accumulates those rows by rank lookup; 0: numeric re-derives every
+                          row.  Costs up to 48 * 8 bytes of workspace per row of A. */
     kk_alloc_fn alloc;
     kk_free_fn free;
     void* alloc_ctx;

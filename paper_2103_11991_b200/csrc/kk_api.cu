@@ -103,7 +103,7 @@ struct kk_spgemm_handle_s {
     long long launches = 0;
     // workspace
     Buf flops, fscan, binid, perm_sym, perm_num, counts, binscratch, binstart, bc_len, pairs, cursors, partial,
-        status;
+        status, bfirst, blast, wlo, pat, pat_off, pat_len;
     DevStatus* h_status = nullptr;  // pinned
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -233,6 +233,7 @@ void kk_spgemm_opts_default(kk_spgemm_opts_t* o) {
     o->compression = -1;
     o->validate = 0;
     o->num_streams = 2;
+    o->patterns = 1;
 }
 
 const char* kk_status_string(kk_status_t s) {
@@ -292,7 +293,8 @@ kk_status_t kk_spgemm_destroy(kk_spgemm_handle_t h) {
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     Buf* bufs[] = {&h->flops, &h->fscan, &h->binid, &h->perm_sym, &h->perm_num, &h->counts, &h->binscratch,
-                   &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status};
+                   &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status,
+                   &h->bfirst, &h->blast, &h->wlo, &h->pat, &h->pat_off, &h->pat_len};
     for (Buf* b : bufs) release(h, *b);
     delete h->timer;
     if (h->h_status) cudaFreeHost(h->h_status);
@@ -327,7 +329,7 @@ kk_status_t kk_spgemm_compress(kk_spgemm_handle_t h, const kk_csr_t* B, int32_t*
     DevStatus* dst = (DevStatus*)h->status.p;
     kk::init_status(L, dst);
     kk::check_compress(L, B->offset_type == KK_I64, view(B), B->ncols, true, h->opts.validate != 0, len,
-                       (uint2*)pairs, dst);
+                       (uint2*)pairs, nullptr, nullptr, dst);
     return cuda_check(h, cudaGetLastError(), "kk_spgemm_compress launch");
 }
 
@@ -352,8 +354,8 @@ kk_status_t kk_spgemm_row_flops(kk_spgemm_handle_t h, const kk_csr_t* A, const k
     kk::Launch L = make_launch(h, s);
     DevStatus* dst = (DevStatus*)h->status.p;
     kk::init_status(L, dst);
-    kk::row_flops_bin(L, off64, view(A), view(B), B->ncols, 0, h->opts.validate != 0, nullptr, f,
-                      (uint8_t*)h->binid.p, (int32_t*)h->counts.p, dst);
+    kk::row_flops_bin(L, off64, view(A), view(B), B->ncols, 0, h->opts.validate != 0, nullptr, nullptr, nullptr,
+                      f, (uint8_t*)h->binid.p, (int32_t*)h->counts.p, nullptr, dst);
     if (flops_scan) kk::exclusive_scan(L, true, f, true, flops_scan, m, (int64_t*)h->partial.p, nullptr, nullptr);
     if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_row_flops launch")) != KK_OK) return st;
     if (total) {
@@ -391,6 +393,17 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     if ((st = ensure(h, h->binstart, sizeof(int) * 2 * (kk::NB + 1), s)) != KK_OK) return st;
     if ((st = ensure(h, h->partial, (size_t)kk::scan_partial_len(m) * 8, s)) != KK_OK) return st;
     if ((st = ensure(h, h->cursors, (size_t)A->nnz * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->bfirst, (size_t)n * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->blast, (size_t)n * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->wlo, (size_t)m * 4, s)) != KK_OK) return st;
+    const bool keep_pat = h->opts.patterns != 0;
+    const int64_t pat_cap = keep_pat ? 48 * m : 0;
+    if (keep_pat) {
+        if ((st = ensure(h, h->pat, (size_t)pat_cap * 8, s)) != KK_OK) return st;
+        if ((st = ensure(h, h->pat_off, (size_t)m * 8, s)) != KK_OK) return st;
+        if ((st = ensure(h, h->pat_len, (size_t)m * 4, s)) != KK_OK) return st;
+        if (m > 0) cudaMemsetAsync(h->pat_off.p, 0xff, (size_t)m * 8, s);
+    }
     if (comp_mode != 0) {
         if ((st = ensure(h, h->bc_len, (size_t)n * 4, s)) != KK_OK) return st;
         if ((st = ensure(h, h->pairs, (size_t)B->nnz * 8, s)) != KK_OK) return st;
@@ -404,10 +417,11 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     kk::init_status(L, dst);
     // a4: sortedness flags (+ B_C unless compression is off)
     kk::check_compress(L, off64, Bv, k, comp_mode != 0, h->opts.validate != 0, (int32_t*)h->bc_len.p,
-                       (uint2*)h->pairs.p, dst);
+                       (uint2*)h->pairs.p, (int32_t*)h->bfirst.p, (int32_t*)h->blast.p, dst);
     // a1: flops per row, symbolic bins
     kk::row_flops_bin(L, off64, Av, Bv, k, comp_mode, h->opts.validate != 0, (const int32_t*)h->bc_len.p,
-                      (int64_t*)h->flops.p, (uint8_t*)h->binid.p, (int32_t*)h->counts.p, dst);
+                      (const int32_t*)h->bfirst.p, (const int32_t*)h->blast.p, (int64_t*)h->flops.p,
+                      (uint8_t*)h->binid.p, (int32_t*)h->counts.p, (int32_t*)h->wlo.p, dst);
     // a2: F = exclusive scan of flops (kept in the handle for flop-balanced partitioning)
     kk::exclusive_scan(L, true, h->flops.p, true, h->fscan.p, m, (int64_t*)h->partial.p, nullptr, nullptr);
     // a3: bin rows by symbolic work
@@ -424,6 +438,12 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     sa.bin_start = sym_start;
     sa.counts = (int32_t*)h->counts.p;
     sa.cursors = (int32_t*)h->cursors.p;
+    sa.wlo = (const int32_t*)h->wlo.p;
+    sa.host_bin_start = nullptr;
+    sa.pat.pat = keep_pat ? (uint2*)h->pat.p : nullptr;
+    sa.pat.cap = pat_cap;
+    sa.pat.off = keep_pat ? (long long*)h->pat_off.p : nullptr;
+    sa.pat.len = keep_pat ? (int*)h->pat_len.p : nullptr;
     sa.st = dst;
     sa.logG = pick_logG(n > 0 ? (double)B->nnz / (double)n / (comp_mode != 0 ? 2.0 : 1.0) : 1.0);
     cudaStream_t side = nullptr;
@@ -441,7 +461,8 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     kk::exclusive_scan(L, false, h->counts.p, off64, c_row_map, m, (int64_t*)h->partial.p, &dst->nnz_c,
                        &dst->overflow);
     // numeric bins from exact counts
-    kk::numeric_binid(L, m, (const int32_t*)h->counts.p, (uint8_t*)h->binid.p);
+    kk::numeric_binid(L, m, (const int32_t*)h->counts.p, keep_pat ? (const long long*)h->pat_off.p : nullptr,
+                      (uint8_t*)h->binid.p, dst);
     kk::bin_rows(L, m, (const uint8_t*)h->binid.p, (int32_t*)h->binscratch.p, (int32_t*)h->perm_num.p, num_start);
     // copy bin starts next to the status block, then the single device->host read
     cudaMemcpyAsync(dst->sym_bin_start, sym_start, sizeof(int) * (kk::NB + 1), cudaMemcpyDeviceToDevice, s);
@@ -506,6 +527,9 @@ kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
     na.f64 = A->value_type == KK_F64;
     na.sort = h->opts.sort_rows != 0;
     na.strict = h->stats.b_strict != 0;
+    na.pat = (const uint2*)h->pat.p;
+    na.pat_off = (const long long*)h->pat_off.p;
+    na.pat_len = (const int*)h->pat_len.p;
     na.A = view(A);
     na.B = view(B);
     na.k = B->ncols;
@@ -567,7 +591,8 @@ kk_status_t kk_spgemm_stats(kk_spgemm_handle_t h, kk_spgemm_stats_t* out) {
     out->kernel_launches = h->launches;
     int64_t ws = 0;
     const Buf* bufs[] = {&h->flops, &h->fscan, &h->binid, &h->perm_sym, &h->perm_num, &h->counts, &h->binscratch,
-                         &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status};
+                         &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status,
+                         &h->bfirst, &h->blast, &h->wlo, &h->pat, &h->pat_off, &h->pat_len};
     for (const Buf* b : bufs) ws += (int64_t)b->bytes;
     out->workspace_bytes = ws;
     return KK_OK;

@@ -15,13 +15,20 @@ constexpr uint32_t EMPTY = 0xffffffffu;      // empty hash slot (column indices 
 //   slots (ub <= S); 8: CTA-owned dense bit-vector window.
 constexpr int SYM_WARP_BINS = 7;
 constexpr int SYM_DENSE_BIN = 8;
-constexpr int SYM_NBINS = 9;
+// 9..11: warp-owned dense bit vector over the row's column window [wlo, wlo + W) with
+// W = 8K, 32K, 64K bits (sorted B only; the window comes from the first/last column of
+// each B row, "bit vector for symbolic")
+constexpr int SYM_WIN_BIN0 = 9;
+constexpr int SYM_NBINS = 12;
 // Numeric bins (by exact nnz(C_i)):
 //   0: empty; b = 1..5: warp-owned shared hash with S = 32 << b slots (nnz <= S/2);
 //   6: CTA-owned dense scalar window (column-windowed dense accumulator).
 constexpr int NUM_WARP_BINS = 5;
 constexpr int NUM_DENSE_BIN = 6;
-constexpr int NUM_NBINS = 7;
+//   7..11: rows with a pattern kept by symbolic (nnz <= 32 << (b - 7)): word-table rank
+//   lookup into a dense per-row value array (no claims, no sort)
+constexpr int NUM_PAT_BIN0 = 7;
+constexpr int NUM_NBINS = 12;
 
 // Device-side status block.  Written by the kernels, copied to pinned host memory
 // once at the end of the symbolic phase (the phase's only device->host sync).
@@ -29,6 +36,7 @@ struct DevStatus {
     unsigned long long total_flops;   // sum_i flops_i
     unsigned long long total_words;   // |B_C| (pairs written by compression)
     unsigned long long nnz_c;         // row_map[m]
+    unsigned long long pat_used;      // pairs taken from the row-pattern pool
     int b_sorted;                     // every B row non-decreasing
     int b_strict;                     // every B row strictly increasing
     int bad_index;                    // validate: a column index out of range
@@ -37,6 +45,15 @@ struct DevStatus {
     int pad;
     int sym_bin_start[NB + 1];        // row ranges of the symbolic bins in perm_sym
     int num_bin_start[NB + 1];        // row ranges of the numeric bins in perm_num
+};
+
+// Row patterns kept by the symbolic window kernels for the numeric phase: the sorted
+// (word, mask) pairs of row i are pat[off[i] .. off[i] + len[i]); off[i] = -1: none.
+struct PatOut {
+    uint2* pat;
+    long long cap;
+    long long* off;
+    int* len;
 };
 
 struct MatView {
@@ -68,18 +85,23 @@ struct Launch {
 
 // ---- host launchers (kk_kernels.cu) -------------------------------------------------
 void init_status(Launch& L, DevStatus* st);
+// bfirst/blast (may be null): first and last column of each B row (INT_MAX / -1 if empty)
 void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_comp, bool validate,
-                    int32_t* bc_len, uint2* pairs, DevStatus* st);
+                    int32_t* bc_len, uint2* pairs, int32_t* bfirst, int32_t* blast, DevStatus* st);
+// wlo (may be null): word-aligned first column of the window of rows in window bins
 void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, int64_t k, int comp_mode,
-                   bool validate, const int32_t* bc_len, int64_t* flops, uint8_t* binid, int32_t* counts,
-                   DevStatus* st);
+                   bool validate, const int32_t* bc_len, const int32_t* bfirst, const int32_t* blast,
+                   int64_t* flops, uint8_t* binid, int32_t* counts, int32_t* wlo, DevStatus* st);
 // exclusive scan of in[0..m) (int32 or int64) into out[0..m] (int32 or int64);
 // *total_dst (device, may be null) receives the sum; *overflow set when out is
 // int32 and the sum exceeds INT32_MAX.  partial: >= scan_partial_len(m) int64.
 int64_t scan_partial_len(int64_t m);
 void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out, int64_t m, int64_t* partial,
                     unsigned long long* total_dst, int* overflow);
-void numeric_binid(Launch& L, int64_t m, const int32_t* counts, uint8_t* binid);
+// pat_off (may be null): rows with a stored pattern (and strictly sorted B) go to the
+// pattern bins NUM_PAT_BIN0 + (b - 1)
+void numeric_binid(Launch& L, int64_t m, const int32_t* counts, const long long* pat_off, uint8_t* binid,
+                   const DevStatus* st);
 // stable binning of rows by binid: perm lists rows of bin 0, then bin 1, ...
 // (each bin in increasing row order); bin_start_dst (device int[NB+1]).
 int64_t bin_scratch_len(int64_t m);
@@ -93,6 +115,9 @@ struct SymArgs {
     const uint2* pairs;
     const int32_t* perm;
     const int* bin_start;   // device
+    const int* host_bin_start;  // host copy, or null (then every bin is launched)
+    const int32_t* wlo;     // window start per row (window bins)
+    PatOut pat;             // row-pattern pool (pat.pat may be null: keep none)
     int32_t* counts;
     int32_t* cursors;       // nnz(A) scratch for windowed rows
     const DevStatus* st;
@@ -114,6 +139,9 @@ struct NumArgs {
     int32_t* cursors;
     const DevStatus* st;
     int logG;
+    const uint2* pat;            // row patterns (see PatOut)
+    const long long* pat_off;
+    const int* pat_len;
 };
 void numeric_bins(Launch& L, const NumArgs& a, cudaStream_t dense_stream);
 

@@ -313,6 +313,101 @@ struct StrictLayout {
     static constexpr size_t bytes = (stage + (size_t)CAP * 4 + 15) / 16 * 16;
 };
 
+// The products of one row, one B row (or 32-entry segment of it) per warp step: the A
+// row is staged per 32-entry chunk (B row pointers, lengths, a_ij in shared memory), the
+// first chunk's A entries (jn, an) come from the caller (prefetched), and B rows are
+// loaded three steps ahead of the step being inserted.  insert(col, a_ij * b_jk) is
+// called by all 32 lanes for every step (col = EMPTY on idle lanes); the <= 32 columns
+// of a step are the entries of one B row segment.
+template <typename OffT, typename ValT, typename Ins>
+__device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT an, const int32_t* __restrict__ aent,
+                                             const ValT* __restrict__ aval, const OffT* __restrict__ brm,
+                                             const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                             StepPtr<ValT>* ptr, ValT* av, int* len, Ins insert) {
+    using SP = StepPtr<ValT>;
+    const int lane = threadIdx.x & 31;
+    for (int64_t c0 = s; c0 < e; c0 += 32) {
+        const int na = (int)min((int64_t)32, e - c0);
+        int j = jn;
+        ValT a = an;
+        if (c0 != s && lane < na) {
+            j = __ldg(aent + c0 + lane);
+            a = __ldg(aval + c0 + lane);
+        }
+        int bl = 0;
+        if (lane < na) {
+            const int64_t bb = ld(brm, j);
+            bl = (int)(ld(brm, j + 1) - bb);
+            ptr[lane].ent = bent + bb;
+            ptr[lane].val = bval + bb;
+            av[lane] = a;
+            len[lane] = bl;
+        }
+        unsigned rem = __ballot_sync(FULL, bl > 0);
+        const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
+        __syncwarp();
+        if (!rem) continue;
+        if (maxbl <= 32) {
+            // one step per B row (the set bits of rem); loads run 3 steps ahead
+            // (the product is formed at insert time, so no load is waited on early)
+            auto fetch = [&](uint32_t& col, ValT& bv, ValT& at) {
+                col = EMPTY;
+                bv = (ValT)0;
+                at = (ValT)0;
+                if (!rem) return false;
+                const int t = __ffs(rem) - 1;
+                rem &= rem - 1;
+                const SP sp = ptr[t];
+                at = av[t];
+                if (lane < len[t]) {
+                    col = (uint32_t)__ldg(sp.ent + lane);
+                    bv = __ldg(sp.val + lane);
+                }
+                return true;
+            };
+            uint32_t k0, k1, k2, k3;
+            ValT b0, b1, b2, b3, a0, a1, a2, a3;
+            fetch(k0, b0, a0);
+            bool h1 = fetch(k1, b1, a1);
+            bool h2 = fetch(k2, b2, a2);
+            bool h3 = fetch(k3, b3, a3);
+            while (true) {
+                insert(k0, a0 * b0);
+                if (!h1) break;
+                const bool h0 = fetch(k0, b0, a0);
+                insert(k1, a1 * b1);
+                if (!h2) break;
+                h1 = fetch(k1, b1, a1);
+                insert(k2, a2 * b2);
+                if (!h3) break;
+                h2 = fetch(k2, b2, a2);
+                insert(k3, a3 * b3);
+                if (!h0) break;
+                h3 = fetch(k3, b3, a3);
+            }
+        } else {
+            // long B rows: 32-entry segments
+            while (rem) {
+                const int t = __ffs(rem) - 1;
+                rem &= rem - 1;
+                const SP sp = ptr[t];
+                const ValT at = av[t];
+                const int blt = len[t];
+                for (int q0 = 0; q0 < blt; q0 += 32) {
+                    uint32_t col = EMPTY;
+                    ValT p = (ValT)0;
+                    if (q0 + lane < blt) {
+                        col = (uint32_t)__ldg(sp.ent + q0 + lane);
+                        p = at * __ldg(sp.val + q0 + lane);
+                    }
+                    insert(col, p);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 template <typename OffT, typename ValT, int S, int CAP, bool SORT>
 __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                     const ValT* __restrict__ aval, const OffT* __restrict__ brm,
@@ -357,91 +452,12 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
         const int clen = (int)(ld(crm, i + 1) - cb);
         const int rn = r + stride;
         const int inext = rn < r1 ? perm[rn] : -1;
-        for (int64_t c0 = s; c0 < e; c0 += 32) {
-            const int na = (int)min((int64_t)32, e - c0);
-            int j = jn;
-            ValT a = an;
-            if (c0 != s && lane < na) {
-                j = __ldg(aent + c0 + lane);
-                a = __ldg(aval + c0 + lane);
-            }
-            int bl = 0;
-            if (lane < na) {
-                const int64_t bb = ld(brm, j);
-                bl = (int)(ld(brm, j + 1) - bb);
-                ptr[lane].ent = bent + bb;
-                ptr[lane].val = bval + bb;
-                av[lane] = a;
-                len[lane] = bl;
-            }
-            unsigned rem = __ballot_sync(FULL, bl > 0);
-            const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
-            __syncwarp();
-            if (!rem) continue;
-            auto insert = [&](uint32_t col, ValT prod) {
-                const bool act = col != EMPTY;
-                const uint32_t h = strict_claim<S>(keys, col, act);
-                if (act) vals[h] += prod;
-            };
-            if (maxbl <= 32) {
-                // one step per B row (the set bits of rem); loads run 3 steps ahead
-                // (the product is formed at insert time, so no load is waited on early)
-                auto fetch = [&](uint32_t& col, ValT& bv, ValT& at) {
-                    col = EMPTY;
-                    bv = (ValT)0;
-                    at = (ValT)0;
-                    if (!rem) return false;
-                    const int t = __ffs(rem) - 1;
-                    rem &= rem - 1;
-                    const SP sp = ptr[t];
-                    at = av[t];
-                    if (lane < len[t]) {
-                        col = (uint32_t)__ldg(sp.ent + lane);
-                        bv = __ldg(sp.val + lane);
-                    }
-                    return true;
-                };
-                uint32_t k0, k1, k2, k3;
-                ValT b0, b1, b2, b3, a0, a1, a2, a3;
-                fetch(k0, b0, a0);
-                bool h1 = fetch(k1, b1, a1);
-                bool h2 = fetch(k2, b2, a2);
-                bool h3 = fetch(k3, b3, a3);
-                while (true) {
-                    insert(k0, a0 * b0);
-                    if (!h1) break;
-                    const bool h0 = fetch(k0, b0, a0);
-                    insert(k1, a1 * b1);
-                    if (!h2) break;
-                    h1 = fetch(k1, b1, a1);
-                    insert(k2, a2 * b2);
-                    if (!h3) break;
-                    h2 = fetch(k2, b2, a2);
-                    insert(k3, a3 * b3);
-                    if (!h0) break;
-                    h3 = fetch(k3, b3, a3);
-                }
-            } else {
-                // long B rows: 32-entry segments
-                while (rem) {
-                    const int t = __ffs(rem) - 1;
-                    rem &= rem - 1;
-                    const SP sp = ptr[t];
-                    const ValT at = av[t];
-                    const int blt = len[t];
-                    for (int q0 = 0; q0 < blt; q0 += 32) {
-                        uint32_t col = EMPTY;
-                        ValT p = (ValT)0;
-                        if (q0 + lane < blt) {
-                            col = (uint32_t)__ldg(sp.ent + q0 + lane);
-                            p = at * __ldg(sp.val + q0 + lane);
-                        }
-                        insert(col, p);
-                    }
-                }
-            }
-            __syncwarp();
-        }
+        row_products<OffT, ValT>(s, e, jn, an, aent, aval, brm, bent, bval, ptr, av, len,
+                                 [&](uint32_t col, ValT prod) {
+                                     const bool act = col != EMPTY;
+                                     const uint32_t h = strict_claim<S>(keys, col, act);
+                                     if (act) vals[h] += prod;
+                                 });
         // next row's bounds (their loads overlap the epilogue)
         int64_t sn = 0, en = 0;
         if (inext >= 0) {
@@ -530,6 +546,167 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
     }
 }
 
+
+// ------------------------------------------------------------------------------------
+// a7 for rows whose pattern was kept by the symbolic phase (sorted (word, mask) pairs,
+// <= 64 words).  The pattern fixes every column's position in the sorted output row:
+// rank(c) = prefix(word(c)) + popc(mask & bits below c).  The words go into a small
+// shared hash table (key = word, value = (mask, prefix)); each product looks its word up
+// (the key is always present: no claims), computes its rank and accumulates into a
+// dense per-row value array (accum = +).  The B row of a step has distinct
+// columns (strictly sorted B), so ranks within a step are distinct and the update is a
+// plain shared load/add/store.  Entries are written straight from the pattern and the
+// values in order: the row is sorted without a sort.
+// ------------------------------------------------------------------------------------
+constexpr int PAT_W = 64;    // max words of a kept pattern (symbolic PAT_WORDS)
+constexpr int PAT_SW = 128;  // word-table slots
+
+template <typename ValT, int CAP>
+struct PatLayout {
+    static constexpr size_t vals = 0;
+    static constexpr size_t ptr = vals + (size_t)CAP * sizeof(ValT);
+    static constexpr size_t av = ptr + 32 * sizeof(StepPtr<ValT>);
+    static constexpr size_t len = av + 32 * sizeof(ValT);
+    static constexpr size_t winfo = (len + 32 * 4 + 15) / 16 * 16;
+    static constexpr size_t wkeys = winfo + (size_t)PAT_SW * 8;
+    static constexpr size_t bytes = (wkeys + (size_t)PAT_SW * 4 + 15) / 16 * 16;
+};
+
+template <typename OffT, typename ValT, int CAP>
+__global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                     const ValT* __restrict__ aval, const OffT* __restrict__ brm,
+                                                     const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                                     const OffT* __restrict__ crm, int32_t* __restrict__ cent,
+                                                     ValT* __restrict__ cval, const int32_t* __restrict__ perm,
+                                                     const int* __restrict__ bin_start, int bin,
+                                                     const uint2* __restrict__ pat, const long long* __restrict__ pat_off,
+                                                     const int* __restrict__ pat_len) {
+    using LY = PatLayout<ValT, CAP>;
+    using SP = StepPtr<ValT>;
+    extern __shared__ __align__(16) unsigned char sm_pat[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    unsigned char* base = sm_pat + (size_t)warp * LY::bytes;
+    ValT* vals = (ValT*)(base + LY::vals);
+    SP* ptr = (SP*)(base + LY::ptr);
+    ValT* av = (ValT*)(base + LY::av);
+    int* len = (int*)(base + LY::len);
+    uint2* winfo = (uint2*)(base + LY::winfo);
+    uint32_t* wkeys = (uint32_t*)(base + LY::wkeys);
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    const int stride = gridDim.x * warps;
+    int r = r0 + blockIdx.x * warps + warp;
+    if (r >= r1) return;
+    for (int t = lane; t < CAP; t += 32) vals[t] = (ValT)0;
+    for (int t = lane; t < PAT_SW; t += 32) wkeys[t] = EMPTY;
+    __syncwarp();
+    int i = perm[r];
+    int64_t s = ld(arm, i), e = ld(arm, i + 1);
+    int jn = 0;
+    ValT an = (ValT)0;
+    if (lane < e - s) {
+        jn = __ldg(aent + s + lane);
+        an = __ldg(aval + s + lane);
+    }
+    while (true) {
+        const int64_t cb = ld(crm, i);
+        const int clen = (int)(ld(crm, i + 1) - cb);
+        const long long po = pat_off[i];
+        const int pl = pat_len[i];
+        const int rn = r + stride;
+        const int inext = rn < r1 ? perm[rn] : -1;
+        // ---- the row's pattern: word table + entries ----
+        const uint2 p0 = lane < pl ? pat[po + lane] : make_uint2(0u, 0u);
+        const uint2 p1 = lane + 32 < pl ? pat[po + 32 + lane] : make_uint2(0u, 0u);
+        const int c0 = __popc(p0.y), c1 = __popc(p1.y);
+        int x0 = c0, x1 = c1;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y0 = __shfl_up_sync(FULL, x0, d), y1 = __shfl_up_sync(FULL, x1, d);
+            if (lane >= d) {
+                x0 += y0;
+                x1 += y1;
+            }
+        }
+        const int tot0 = __shfl_sync(FULL, x0, 31);
+        const uint32_t pre0 = (uint32_t)(x0 - c0), pre1 = (uint32_t)(tot0 + x1 - c1);
+        const uint32_t h0 = strict_claim<PAT_SW>(wkeys, p0.x, lane < pl);
+        const uint32_t h1 = strict_claim<PAT_SW>(wkeys, p1.x, lane + 32 < pl);
+        if (lane < pl) winfo[h0] = make_uint2(p0.y, pre0);
+        if (lane + 32 < pl) winfo[h1] = make_uint2(p1.y, pre1);
+        {
+            uint32_t m = p0.y;
+            int o = (int)pre0;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                if (o < clen) cent[cb + o] = (int32_t)(p0.x * 32u + (uint32_t)b);
+                ++o;
+            }
+            m = p1.y;
+            o = (int)pre1;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                if (o < clen) cent[cb + o] = (int32_t)(p1.x * 32u + (uint32_t)b);
+                ++o;
+            }
+        }
+        __syncwarp();
+        // ---- products: rank lookup + dense accumulate ----
+        row_products<OffT, ValT>(s, e, jn, an, aent, aval, brm, bent, bval, ptr, av, len,
+                                 [&](uint32_t col, ValT prod) {
+                                     if (col != EMPTY) {
+                                         const uint32_t h = strict_find<PAT_SW>(wkeys, col >> 5);
+                                         const uint2 wi = winfo[h];
+                                         const uint32_t rk = wi.y + __popc(wi.x & ((1u << (col & 31)) - 1u));
+                                         if (rk < (uint32_t)CAP) vals[rk] += prod;
+                                     }
+                                 });
+        int64_t sn = 0, en = 0;
+        if (inext >= 0) {
+            sn = ld(arm, inext);
+            en = ld(arm, inext + 1);
+        }
+        __syncwarp();
+        // ---- write the values in order, reset ----
+        const int nn = min(clen, CAP);
+        for (int t = lane; t < nn; t += 32) {
+            cval[cb + t] = vals[t];
+            vals[t] = (ValT)0;
+        }
+        if (lane < pl) wkeys[h0] = EMPTY;
+        if (lane + 32 < pl) wkeys[h1] = EMPTY;
+        if (inext >= 0 && lane < en - sn) {
+            jn = __ldg(aent + sn + lane);
+            an = __ldg(aval + sn + lane);
+        }
+        __syncwarp();
+        if (inext < 0) break;
+        r = rn;
+        i = inext;
+        s = sn;
+        e = en;
+    }
+}
+
+template <typename OffT, typename ValT, int CAP>
+static void launch_num_pattern(Launch& L, const NumArgs& a, int bin) {
+    const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
+    if (rows <= 0) return;
+    const int warps = 8;
+    const size_t smem = (size_t)warps * PatLayout<ValT, CAP>::bytes;
+    auto kern = k_num_pattern<OffT, ValT, CAP>;
+    KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    int64_t need = (rows + warps - 1) / warps;
+    int grid = (int)std::min<int64_t>(need, c.grid_cap);
+    L.begin(kname("num_pattern", CAP), L.stream);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
+                                               (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
+                                               (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
+                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len);
+    L.end(L.stream);
+}
+
 // rows of numeric bin `bin` hold nnz(C_i) <= CAP = 16 << bin; the table has S = 4*CAP slots
 template <typename OffT, typename ValT, int CAP, int F, bool SORT>
 static void launch_num_strict_f(Launch& L, const NumArgs& a, int bin) {
@@ -606,6 +783,13 @@ static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_strea
                                          (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm, a.bin_start,
                                          NUM_DENSE_BIN, a.k, (int)W, a.cursors, a.st);
         L.end(s);
+    }
+    if (a.pat) {
+        launch_num_pattern<OffT, ValT, 512>(L, a, NUM_PAT_BIN0 + 4);
+        launch_num_pattern<OffT, ValT, 256>(L, a, NUM_PAT_BIN0 + 3);
+        launch_num_pattern<OffT, ValT, 128>(L, a, NUM_PAT_BIN0 + 2);
+        launch_num_pattern<OffT, ValT, 64>(L, a, NUM_PAT_BIN0 + 1);
+        launch_num_pattern<OffT, ValT, 32>(L, a, NUM_PAT_BIN0);
     }
     if (a.strict && a.logG == 5) {
         launch_num_strict<OffT, ValT, 512, SORT>(L, a, 5);

@@ -15,6 +15,7 @@ __global__ void k_init_status(DevStatus* st) {
         st->total_flops = 0;
         st->total_words = 0;
         st->nnz_c = 0;
+        st->pat_used = 0;
         st->b_sorted = 1;
         st->b_strict = 1;
         st->bad_index = 0;
@@ -43,7 +44,8 @@ template <typename OffT>
 __global__ void __launch_bounds__(256) k_check_compress(int64_t n, int64_t k, const OffT* __restrict__ brm,
                                                         const int32_t* __restrict__ bent, int do_comp,
                                                         int validate, int32_t* __restrict__ bc_len,
-                                                        uint2* __restrict__ pairs, DevStatus* st) {
+                                                        uint2* __restrict__ pairs, int32_t* __restrict__ bfirst,
+                                                        int32_t* __restrict__ blast, DevStatus* st) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -52,6 +54,7 @@ __global__ void __launch_bounds__(256) k_check_compress(int64_t n, int64_t k, co
     for (int64_t j = gw; j < n; j += nw) {
         const int64_t s = ld(brm, j), e = ld(brm, j + 1);
         int prev_last = INT_MIN;
+        if (bfirst && lane == 0) bfirst[j] = s < e ? __ldg(bent + s) : INT_MAX;
         int cw = -1;
         unsigned cm = 0;
         int outn = 0;
@@ -98,6 +101,7 @@ __global__ void __launch_bounds__(256) k_check_compress(int64_t n, int64_t k, co
                 cm = __shfl_sync(FULL, v, nact - 1);
             }
         }
+        if (blast && lane == 0) blast[j] = s < e ? prev_last : -1;
         if (do_comp) {
             if (cw >= 0) {
                 if (lane == 0) pairs[s + outn] = make_uint2((unsigned)cw, cm);
@@ -122,17 +126,19 @@ static int grid_for(int64_t warps_needed, int threads, int num_sms, int per_sm =
 }
 
 void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_comp, bool validate,
-                    int32_t* bc_len, uint2* pairs, DevStatus* st) {
+                    int32_t* bc_len, uint2* pairs, int32_t* bfirst, int32_t* blast, DevStatus* st) {
     if (B.nrows == 0) return;
     const int threads = 256;
     const int grid = grid_for(B.nrows, threads, L.num_sms, 16);
     L.begin(do_comp ? "check_compress" : "check_sorted", L.stream);
     if (off64)
         k_check_compress<int64_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int64_t*)B.row_map, B.entries,
-                                                                  do_comp, validate, bc_len, pairs, st);
+                                                                  do_comp, validate, bc_len, pairs, bfirst, blast,
+                                                                  st);
     else
         k_check_compress<int32_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int32_t*)B.row_map, B.entries,
-                                                                  do_comp, validate, bc_len, pairs, st);
+                                                                  do_comp, validate, bc_len, pairs, bfirst, blast,
+                                                                  st);
     L.end(L.stream);
 }
 
@@ -150,13 +156,25 @@ __device__ __forceinline__ int sym_bin_of(int64_t ub) {
     return b;
 }
 
+// window bin for a row whose columns lie in [lo, hi] (sorted B), or 0: the smallest
+// W in {8K, 32K, 64K} bits covering [lo & ~31, hi], used when clearing the window
+// (W/32 words) costs at most ~16 words per bound insert and the row is not tiny.
+__device__ __forceinline__ int sym_win_bin_of(int lo, int hi, int64_t ub) {
+    if (hi < lo || ub <= 32) return 0;
+    const int64_t span = (int64_t)hi - (int64_t)(lo & ~31) + 1;
+    const int64_t W = span <= 8192 ? 8192 : span <= 32768 ? 32768 : span <= 65536 ? 65536 : 0;
+    if (W == 0 || W / 32 > 16 * ub) return 0;
+    return W == 8192 ? SYM_WIN_BIN0 : W == 32768 ? SYM_WIN_BIN0 + 1 : SYM_WIN_BIN0 + 2;
+}
+
 template <typename OffT>
 __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t k, const OffT* __restrict__ arm,
                                                    const int32_t* __restrict__ aent, const OffT* __restrict__ brm,
                                                    const int32_t* __restrict__ bc_len, int comp_mode, int64_t nnzB,
-                                                   int validate, int64_t* __restrict__ flops,
+                                                   int validate, const int32_t* __restrict__ bfirst,
+                                                   const int32_t* __restrict__ blast, int64_t* __restrict__ flops,
                                                    uint8_t* __restrict__ binid, int32_t* __restrict__ counts,
-                                                   DevStatus* st) {
+                                                   int32_t* __restrict__ wlo, DevStatus* st) {
     bool comp = false;
     if (comp_mode == 1)
         comp = true;
@@ -167,11 +185,13 @@ __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t kw = (k + 31) >> 5;
+    const bool win = wlo != nullptr && bfirst != nullptr && st->b_sorted != 0;
     unsigned long long tot = 0;
     bool bad = false;
     for (int64_t i = gw; i < m; i += nw) {
         const int64_t s = ld(arm, i), e = ld(arm, i + 1);
         int64_t f = 0, fc = 0;
+        int lo = INT_MAX, hi = -1;
         for (int64_t p = s + lane; p < e; p += 32) {
             const int j = __ldg(aent + p);
             if (validate && (j < 0 || (int64_t)j >= n)) {
@@ -180,13 +200,28 @@ __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t
             }
             f += ld(brm, (int64_t)j + 1) - ld(brm, (int64_t)j);
             if (comp) fc += __ldg(bc_len + j);
+            if (win) {
+                lo = min(lo, __ldg(bfirst + j));
+                hi = max(hi, __ldg(blast + j));
+            }
         }
         f = warp_sum(f);
         if (comp) fc = warp_sum(fc);
+        if (win) {
+            lo = __reduce_min_sync(FULL, lo);
+            hi = __reduce_max_sync(FULL, hi);
+        }
         if (lane == 0) {
             flops[i] = f;
             const int64_t ub = comp ? min(fc, kw) : min(f, k);
-            const int b = sym_bin_of(ub);
+            int b = sym_bin_of(ub);
+            if (win && b > 0) {
+                const int wb = sym_win_bin_of(lo, hi, ub);
+                if (wb) {
+                    b = wb;
+                    wlo[i] = lo & ~31;
+                }
+            }
             binid[i] = (uint8_t)b;
             if (b == 0) counts[i] = 0;
             tot += (unsigned long long)f;
@@ -197,8 +232,8 @@ __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t
 }
 
 void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, int64_t k, int comp_mode,
-                   bool validate, const int32_t* bc_len, int64_t* flops, uint8_t* binid, int32_t* counts,
-                   DevStatus* st) {
+                   bool validate, const int32_t* bc_len, const int32_t* bfirst, const int32_t* blast,
+                   int64_t* flops, uint8_t* binid, int32_t* counts, int32_t* wlo, DevStatus* st) {
     if (A.nrows == 0) return;
     const int threads = 256;
     const int grid = grid_for(A.nrows, threads, L.num_sms, 16);
@@ -206,11 +241,13 @@ void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, in
     if (off64)
         k_row_flops<int64_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int64_t*)A.row_map,
                                                              A.entries, (const int64_t*)B.row_map, bc_len,
-                                                             comp_mode, B.nnz, validate, flops, binid, counts, st);
+                                                             comp_mode, B.nnz, validate, bfirst, blast, flops, binid,
+                                                             counts, wlo, st);
     else
         k_row_flops<int32_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int32_t*)A.row_map,
                                                              A.entries, (const int32_t*)B.row_map, bc_len,
-                                                             comp_mode, B.nnz, validate, flops, binid, counts, st);
+                                                             comp_mode, B.nnz, validate, bfirst, blast, flops, binid,
+                                                             counts, wlo, st);
     L.end(L.stream);
 }
 
@@ -364,16 +401,22 @@ __device__ __forceinline__ int num_bin_of(int64_t nnz) {
 }
 
 __global__ void __launch_bounds__(256) k_numeric_binid(int64_t m, const int32_t* __restrict__ counts,
-                                                       uint8_t* __restrict__ binid) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        binid[i] = (uint8_t)num_bin_of(counts[i]);
+                                                       const long long* __restrict__ pat_off,
+                                                       uint8_t* __restrict__ binid, const DevStatus* st) {
+    const bool pat = pat_off != nullptr && st->b_strict != 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        int b = num_bin_of(counts[i]);
+        if (pat && b >= 1 && b <= NUM_WARP_BINS && pat_off[i] >= 0) b = NUM_PAT_BIN0 + b - 1;
+        binid[i] = (uint8_t)b;
+    }
 }
 
-void numeric_binid(Launch& L, int64_t m, const int32_t* counts, uint8_t* binid) {
+void numeric_binid(Launch& L, int64_t m, const int32_t* counts, const long long* pat_off, uint8_t* binid,
+                   const DevStatus* st) {
     if (m == 0) return;
     int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)L.num_sms * 16);
     L.begin("numeric_binid", L.stream);
-    k_numeric_binid<<<grid, 256, 0, L.stream>>>(m, counts, binid);
+    k_numeric_binid<<<grid, 256, 0, L.stream>>>(m, counts, pat_off, binid, st);
     L.end(L.stream);
 }
 

@@ -176,6 +176,228 @@ static void launch_sym_warp(Launch& L, const SymArgs& a, int bin) {
     L.end(L.stream);
 }
 
+
+// ------------------------------------------------------------------------------------
+// a5 for rows of sorted B whose columns fit a window of W bits: the paper's dense bit
+// vector, one per warp, over [wlo, wlo + W).  One B_C row per step: its
+// words are distinct (B_C of a sorted row is canonical), so each lane ORs its mask with
+// a plain shared load/store and counts the bits it adds (popc(mask & ~old)).  Without
+// compression the lanes of a step can share a word, so the OR is atomic instead.
+// Words that turn non-zero are appended to a per-warp list; at the end of the row the
+// list (<= PL words) is sorted and the row's pattern -- its (word, mask) pairs in column
+// order -- is kept in the handle for the numeric phase (symbolic state carried by the
+// handle), and only the listed words are cleared.  Rows with more
+// than PL words clear the whole window and keep no pattern.
+// ------------------------------------------------------------------------------------
+constexpr int PAT_WORDS = 64;  // max words of a stored row pattern
+
+template <typename OffT, int W, bool COMP>
+__device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                                const int32_t* __restrict__ bc_len, const uint2* __restrict__ pairs,
+                                                const int32_t* __restrict__ perm, int r0, int r1,
+                                                const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
+                                                uint32_t* bm, long long* sb, uint32_t* wl, const PatOut& po,
+                                                DevStatus* st) {
+    constexpr int NW = W / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    for (int r = r0 + blockIdx.x * warps + warp; r < r1; r += gridDim.x * warps) {
+        const int i = perm[r];
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        const uint32_t wb = (uint32_t)__ldg(wlo + i) >> 5;
+        int cnt = 0;
+        int nt = 0;  // words touched (warp-uniform)
+        auto step_or = [&](uint32_t w, uint32_t m) {
+            bool fresh = false;
+            uint32_t x = 0;
+            if (m) {
+                x = w - wb;
+                uint32_t old;
+                if (COMP) {
+                    old = bm[x];
+                    bm[x] = old | m;
+                } else {
+                    old = atomicOr(&bm[x], m);
+                }
+                cnt += __popc(m & ~old);
+                fresh = old == 0;
+            }
+            const unsigned fb = __ballot_sync(FULL, fresh);
+            if (fresh) {
+                const int pos = nt + __popc(fb & lanemask_lt());
+                if (pos < PAT_WORDS) wl[pos] = x;
+            }
+            nt += __popc(fb);
+        };
+        for (int64_t c0 = s; c0 < e; c0 += 32) {
+            const int na = (int)min((int64_t)32, e - c0);
+            int bl = 0;
+            long long bb = 0;
+            if (lane < na) {
+                const int j = __ldg(aent + c0 + lane);
+                bb = (long long)ld(brm, j);
+                bl = COMP ? __ldg(bc_len + j) : (int)(ld(brm, j + 1) - bb);
+            }
+            __syncwarp();
+            if (lane < na) sb[lane] = bb;
+            unsigned rem = __ballot_sync(FULL, bl > 0);
+            const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
+            __syncwarp();
+            if (maxbl <= 32) {
+                auto fetch = [&](uint32_t& w, uint32_t& m) {
+                    w = 0;
+                    m = 0;
+                    if (!rem) return false;
+                    const int t = __ffs(rem) - 1;
+                    rem &= rem - 1;
+                    const int blt = __shfl_sync(FULL, bl, t);
+                    const long long bbt = sb[t];
+                    if (lane < blt) {
+                        if (COMP) {
+                            const uint2 pr = __ldg(pairs + bbt + lane);
+                            w = pr.x;
+                            m = pr.y;
+                        } else {
+                            const int c = __ldg(bent + bbt + lane);
+                            w = (uint32_t)c >> 5;
+                            m = 1u << (c & 31);
+                        }
+                    }
+                    return true;
+                };
+                uint32_t w0, w1, w2, w3, m0, m1, m2, m3;
+                fetch(w0, m0);
+                bool h1 = fetch(w1, m1);
+                bool h2 = fetch(w2, m2);
+                bool h3 = fetch(w3, m3);
+                while (true) {
+                    step_or(w0, m0);
+                    if (!h1) break;
+                    __syncwarp();
+                    const bool h0 = fetch(w0, m0);
+                    step_or(w1, m1);
+                    if (!h2) break;
+                    __syncwarp();
+                    h1 = fetch(w1, m1);
+                    step_or(w2, m2);
+                    if (!h3) break;
+                    __syncwarp();
+                    h2 = fetch(w2, m2);
+                    step_or(w3, m3);
+                    if (!h0) break;
+                    __syncwarp();
+                    h3 = fetch(w3, m3);
+                }
+            } else {
+                while (rem) {
+                    const int t = __ffs(rem) - 1;
+                    rem &= rem - 1;
+                    const int blt = __shfl_sync(FULL, bl, t);
+                    const long long bbt = sb[t];
+                    for (int q0 = 0; q0 < blt; q0 += 32) {
+                        uint32_t w = 0, m = 0;
+                        if (q0 + lane < blt) {
+                            if (COMP) {
+                                const uint2 pr = __ldg(pairs + bbt + q0 + lane);
+                                w = pr.x;
+                                m = pr.y;
+                            } else {
+                                const int c = __ldg(bent + bbt + q0 + lane);
+                                w = (uint32_t)c >> 5;
+                                m = 1u << (c & 31);
+                            }
+                        }
+                        step_or(w, m);
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        cnt = warp_sum(cnt);
+        if (lane == 0) counts[i] = cnt;
+        __syncwarp();
+        if (nt <= PAT_WORDS) {
+            // sort the touched words (relative indices < NW), store the pattern, clear them
+            constexpr int E = PAT_WORDS / 32;
+            uint32_t v[E];
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int idx = lane * E + q;
+                v[q] = idx < nt ? wl[idx] : 0xffffffffu;
+            }
+            warp_bitonic_sort<E>(v);
+            long long off = -1;
+            if (po.pat) {
+                if (lane == 0) {
+                    const unsigned long long o = atomicAdd(&st->pat_used, (unsigned long long)nt);
+                    off = (o + (unsigned long long)nt <= (unsigned long long)po.cap) ? (long long)o : -1;
+                }
+                off = __shfl_sync(FULL, off, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int idx = lane * E + q;
+                if (idx < nt) {
+                    const uint32_t x = v[q];
+                    const uint32_t m = bm[x];
+                    bm[x] = 0;
+                    if (off >= 0) po.pat[off + idx] = make_uint2(x + wb, m);
+                }
+            }
+            if (po.pat && lane == 0) {
+                po.off[i] = off;
+                po.len[i] = nt;
+            }
+        } else {
+            for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
+        }
+        __syncwarp();
+    }
+}
+
+template <typename OffT, int W>
+__global__ void __launch_bounds__(256) k_sym_window(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                    const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                                    const int32_t* __restrict__ bc_len,
+                                                    const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
+                                                    const int* __restrict__ bin_start, int bin,
+                                                    const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
+                                                    PatOut po, DevStatus* st) {
+    constexpr int NW = W / 32;
+    constexpr int WB = NW + 64 + PAT_WORDS;  // words per warp: bitmap | 32 x int64 | list
+    extern __shared__ __align__(16) uint32_t sm_win[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    uint32_t* bm = sm_win + (size_t)warp * WB;
+    long long* sb = (long long*)(bm + NW);  // per A entry of the chunk: B(_C) row start
+    uint32_t* wl = (uint32_t*)(sb + 32);
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    if (r0 + blockIdx.x * warps + warp >= r1) return;
+    for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    if (st->use_comp)
+        sym_window_rows<OffT, W, true>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm, sb, wl,
+                                       po, st);
+    else
+        sym_window_rows<OffT, W, false>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm, sb, wl,
+                                        po, st);
+}
+
+template <typename OffT, int W>
+static void launch_sym_window(Launch& L, const SymArgs& a, int bin) {
+    const int warps = W <= 8192 ? 8 : 4;
+    const size_t smem = (size_t)warps * ((size_t)W / 32 + 64 + PAT_WORDS) * 4;
+    auto kern = k_sym_window<OffT, W>;
+    KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    int64_t need = (a.A.nrows + warps - 1) / warps;
+    int grid = (int)std::min<int64_t>(need, c.grid_cap);
+    L.begin(kname("sym_window", W), L.stream);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+                                               a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
+                                               a.counts, a.pat, (DevStatus*)a.st);
+    L.end(L.stream);
+}
+
 template <typename OffT>
 static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stream) {
     // dense rows first (heaviest), on their own stream when given
@@ -194,6 +416,9 @@ static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stre
                                                a.k, wbits, a.cursors, a.counts, a.st);
         L.end(s);
     }
+    launch_sym_window<OffT, 65536>(L, a, SYM_WIN_BIN0 + 2);
+    launch_sym_window<OffT, 32768>(L, a, SYM_WIN_BIN0 + 1);
+    launch_sym_window<OffT, 8192>(L, a, SYM_WIN_BIN0);
     launch_sym_warp<OffT, 4096>(L, a, 7);
     launch_sym_warp<OffT, 2048>(L, a, 6);
     launch_sym_warp<OffT, 1024>(L, a, 5);

@@ -87,7 +87,7 @@ class SpGEMM:
     """Kernel handle: options + the symbolic state reused by numeric."""
 
     def __init__(self, device=None, sort_rows: bool = True, compression="auto", validate: bool = False,
-                 num_streams: int = 2, timing: bool = False):
+                 num_streams: int = 2, timing: bool = False, patterns: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2103_11991_b200 needs a CUDA device (there is no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
@@ -98,6 +98,7 @@ class SpGEMM:
         o.validate = int(bool(validate))
         o.num_streams = int(num_streams)
         o.timing = int(bool(timing))
+        o.patterns = int(bool(patterns))
         self._h = _ffi.kk_spgemm_create(self.device.index, o)
 
     # -- phases ------------------------------------------------------------------------

@@ -15,7 +15,7 @@ timeout 600 python bench.py --kernel-table > $OUT/bench_$TAG.json 2> $OUT/bench_
 cat $OUT/bench_$TAG.json; tail -30 $OUT/bench_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_num_warp -s 3 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_num_strict -s 3 -c 3 \
     -o $OUT/prof_num_$TAG -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sym_warp -s 3 -c 3 \
     -o $OUT/prof_sym_$TAG -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full_sym_$TAG.log 2>&1; echo "ncu sym rc=$?"
