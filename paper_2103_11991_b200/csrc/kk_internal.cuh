@@ -15,11 +15,11 @@ constexpr uint32_t EMPTY = 0xffffffffu;      // empty hash slot (column indices 
 //   slots (ub <= S); 8: CTA-owned dense bit-vector window.
 constexpr int SYM_WARP_BINS = 7;
 constexpr int SYM_DENSE_BIN = 8;
-// 9..11: warp-owned dense bit vector over the row's column window [wlo, wlo + W) with
-// W = 8K, 32K, 64K bits (sorted B only; the window comes from the first/last column of
-// each B row, "bit vector for symbolic")
+// 9..13: warp-owned dense bit vector over the row's column window [wlo, wlo + W) with
+// W = 8K, 16K, 32K, 48K, 64K bits (sorted B only; the window comes from the first/last
+// column of each B row, "bit vector for symbolic")
 constexpr int SYM_WIN_BIN0 = 9;
-constexpr int SYM_NBINS = 12;
+constexpr int SYM_NBINS = 14;
 // Numeric bins (by exact nnz(C_i)):
 //   0: empty; b = 1..5: warp-owned shared hash with S = 32 << b slots (nnz <= S/2);
 //   6: CTA-owned dense scalar window (column-windowed dense accumulator).

@@ -294,28 +294,30 @@ __device__ __forceinline__ uint32_t strict_find(const uint32_t* keys, uint32_t c
     return h;
 }
 
-// Per A entry of the current 32-entry chunk: pointers to its B row and the row length.
+// Per A entry of the current 32-entry chunk: its B row (entries, values, length) and a_ij,
+// read back per step with two 16-byte shared loads.
 template <typename ValT>
-struct StepPtr {
+struct __align__(16) StepRec {
     const int32_t* ent;
     const ValT* val;
+    double a;
+    int len;
+    int pad;
 };
 
-// Shared-memory layout of one warp: vals[S] | ptr[32] | av[32] | len[32] | keys[S] | stage[CAP]
+// Shared-memory layout of one warp: vals[S] | rec[32] | keys[S] | stage[CAP]
 template <typename ValT, int S, int CAP>
 struct StrictLayout {
     static constexpr size_t vals = 0;
-    static constexpr size_t ptr = vals + (size_t)S * sizeof(ValT);
-    static constexpr size_t av = ptr + 32 * sizeof(StepPtr<ValT>);
-    static constexpr size_t len = av + 32 * sizeof(ValT);
-    static constexpr size_t keys = len + 32 * 4;
+    static constexpr size_t rec = ((size_t)S * sizeof(ValT) + 15) / 16 * 16;
+    static constexpr size_t keys = rec + 32 * sizeof(StepRec<ValT>);
     static constexpr size_t stage = keys + (size_t)S * 4;
     static constexpr size_t bytes = (stage + (size_t)CAP * 4 + 15) / 16 * 16;
 };
 
-// The products of one row, one B row (or 32-entry segment of it) per warp step: the A
-// row is staged per 32-entry chunk (B row pointers, lengths, a_ij in shared memory), the
-// first chunk's A entries (jn, an) come from the caller (prefetched), and B rows are
+// The products of one row, one B row (or 32-entry segment of it) per warp step, the
+// steps in A-entry order: the A row is staged per 32-entry chunk (StepRec per entry),
+// the first chunk's A entries (jn, an) come from the caller (prefetched), and B rows are
 // loaded three steps ahead of the step being inserted.  insert(col, a_ij * b_jk) is
 // called by all 32 lanes for every step (col = EMPTY on idle lanes); the <= 32 columns
 // of a step are the entries of one B row segment.
@@ -323,8 +325,7 @@ template <typename OffT, typename ValT, typename Ins>
 __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT an, const int32_t* __restrict__ aent,
                                              const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                              const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
-                                             StepPtr<ValT>* ptr, ValT* av, int* len, Ins insert) {
-    using SP = StepPtr<ValT>;
+                                             StepRec<ValT>* rec, Ins insert) {
     const int lane = threadIdx.x & 31;
     for (int64_t c0 = s; c0 < e; c0 += 32) {
         const int na = (int)min((int64_t)32, e - c0);
@@ -335,33 +336,35 @@ __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT 
             a = __ldg(aval + c0 + lane);
         }
         int bl = 0;
+        __syncwarp();
         if (lane < na) {
             const int64_t bb = ld(brm, j);
             bl = (int)(ld(brm, j + 1) - bb);
-            ptr[lane].ent = bent + bb;
-            ptr[lane].val = bval + bb;
-            av[lane] = a;
-            len[lane] = bl;
+            StepRec<ValT> sr;
+            sr.ent = bent + bb;
+            sr.val = bval + bb;
+            sr.a = (double)a;
+            sr.len = bl;
+            sr.pad = 0;
+            rec[lane] = sr;
         }
-        unsigned rem = __ballot_sync(FULL, bl > 0);
         const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
         __syncwarp();
-        if (!rem) continue;
+        if (maxbl == 0) continue;
         if (maxbl <= 32) {
-            // one step per B row (the set bits of rem); loads run 3 steps ahead
-            // (the product is formed at insert time, so no load is waited on early)
+            // one step per A entry; the product is formed at insert time so that no load
+            // is waited on early
+            int t = 0;
             auto fetch = [&](uint32_t& col, ValT& bv, ValT& at) {
                 col = EMPTY;
                 bv = (ValT)0;
                 at = (ValT)0;
-                if (!rem) return false;
-                const int t = __ffs(rem) - 1;
-                rem &= rem - 1;
-                const SP sp = ptr[t];
-                at = av[t];
-                if (lane < len[t]) {
-                    col = (uint32_t)__ldg(sp.ent + lane);
-                    bv = __ldg(sp.val + lane);
+                if (t >= na) return false;
+                const StepRec<ValT> sr = rec[t++];
+                at = (ValT)sr.a;
+                if (lane < sr.len) {
+                    col = (uint32_t)__ldg(sr.ent + lane);
+                    bv = __ldg(sr.val + lane);
                 }
                 return true;
             };
@@ -387,18 +390,15 @@ __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT 
             }
         } else {
             // long B rows: 32-entry segments
-            while (rem) {
-                const int t = __ffs(rem) - 1;
-                rem &= rem - 1;
-                const SP sp = ptr[t];
-                const ValT at = av[t];
-                const int blt = len[t];
-                for (int q0 = 0; q0 < blt; q0 += 32) {
+            for (int t = 0; t < na; ++t) {
+                const StepRec<ValT> sr = rec[t];
+                const ValT at = (ValT)sr.a;
+                for (int q0 = 0; q0 < sr.len; q0 += 32) {
                     uint32_t col = EMPTY;
                     ValT p = (ValT)0;
-                    if (q0 + lane < blt) {
-                        col = (uint32_t)__ldg(sp.ent + q0 + lane);
-                        p = at * __ldg(sp.val + q0 + lane);
+                    if (q0 + lane < sr.len) {
+                        col = (uint32_t)__ldg(sr.ent + q0 + lane);
+                        p = at * __ldg(sr.val + q0 + lane);
                     }
                     insert(col, p);
                 }
@@ -416,16 +416,13 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
                                                     ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                     const int* __restrict__ bin_start, int bin) {
     using LY = StrictLayout<ValT, S, CAP>;
-    using SP = StepPtr<ValT>;
     constexpr int LOGS = ilog2(S);
     constexpr int E = CAP / 32;  // sort elements per lane
     extern __shared__ __align__(16) unsigned char sm_num[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     unsigned char* base = sm_num + (size_t)warp * LY::bytes;
     ValT* vals = (ValT*)(base + LY::vals);
-    SP* ptr = (SP*)(base + LY::ptr);
-    ValT* av = (ValT*)(base + LY::av);
-    int* len = (int*)(base + LY::len);
+    StepRec<ValT>* rec = (StepRec<ValT>*)(base + LY::rec);
     uint32_t* keys = (uint32_t*)(base + LY::keys);
     uint32_t* stage = (uint32_t*)(base + LY::stage);
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
@@ -452,7 +449,7 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
         const int clen = (int)(ld(crm, i + 1) - cb);
         const int rn = r + stride;
         const int inext = rn < r1 ? perm[rn] : -1;
-        row_products<OffT, ValT>(s, e, jn, an, aent, aval, brm, bent, bval, ptr, av, len,
+        row_products<OffT, ValT>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
                                  [&](uint32_t col, ValT prod) {
                                      const bool act = col != EMPTY;
                                      const uint32_t h = strict_claim<S>(keys, col, act);
@@ -564,13 +561,43 @@ constexpr int PAT_SW = 128;  // word-table slots
 template <typename ValT, int CAP>
 struct PatLayout {
     static constexpr size_t vals = 0;
-    static constexpr size_t ptr = vals + (size_t)CAP * sizeof(ValT);
-    static constexpr size_t av = ptr + 32 * sizeof(StepPtr<ValT>);
-    static constexpr size_t len = av + 32 * sizeof(ValT);
-    static constexpr size_t winfo = (len + 32 * 4 + 15) / 16 * 16;
+    static constexpr size_t rec = ((size_t)CAP * sizeof(ValT) + 15) / 16 * 16;
+    static constexpr size_t winfo = rec + 32 * sizeof(StepRec<ValT>);
     static constexpr size_t wkeys = winfo + (size_t)PAT_SW * 8;
     static constexpr size_t bytes = (wkeys + (size_t)PAT_SW * 4 + 15) / 16 * 16;
 };
+
+// word table of a kept pattern: multiplicative hash, linear probing over PAT_SW slots
+__device__ __forceinline__ uint32_t wt_slot(uint32_t w) { return (w * 0x9E3779B1u) >> (32 - ilog2(PAT_SW)); }
+
+// insert distinct words (write-verify claims, as strict_claim); returns the slot
+__device__ __forceinline__ uint32_t wt_insert(uint32_t* keys, uint32_t w, bool act) {
+    uint32_t h = wt_slot(w);
+    bool need = false;
+    if (act) {
+        while (keys[h] != EMPTY) h = (h + 1) & (PAT_SW - 1);
+        need = true;
+    }
+    while (__any_sync(FULL, need)) {
+        if (need) keys[h] = w;
+        __syncwarp();
+        if (need) {
+            if (keys[h] == w) {
+                need = false;
+            } else {
+                while (keys[h] != EMPTY) h = (h + 1) & (PAT_SW - 1);
+            }
+        }
+        __syncwarp();
+    }
+    return h;
+}
+
+__device__ __forceinline__ uint32_t wt_find(const uint32_t* keys, uint32_t w) {
+    uint32_t h = wt_slot(w);
+    while (keys[h] != w) h = (h + 1) & (PAT_SW - 1);
+    return h;
+}
 
 template <typename OffT, typename ValT, int CAP>
 __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
@@ -582,14 +609,11 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
                                                      const uint2* __restrict__ pat, const long long* __restrict__ pat_off,
                                                      const int* __restrict__ pat_len) {
     using LY = PatLayout<ValT, CAP>;
-    using SP = StepPtr<ValT>;
     extern __shared__ __align__(16) unsigned char sm_pat[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     unsigned char* base = sm_pat + (size_t)warp * LY::bytes;
     ValT* vals = (ValT*)(base + LY::vals);
-    SP* ptr = (SP*)(base + LY::ptr);
-    ValT* av = (ValT*)(base + LY::av);
-    int* len = (int*)(base + LY::len);
+    StepRec<ValT>* rec = (StepRec<ValT>*)(base + LY::rec);
     uint2* winfo = (uint2*)(base + LY::winfo);
     uint32_t* wkeys = (uint32_t*)(base + LY::wkeys);
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
@@ -629,8 +653,8 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         }
         const int tot0 = __shfl_sync(FULL, x0, 31);
         const uint32_t pre0 = (uint32_t)(x0 - c0), pre1 = (uint32_t)(tot0 + x1 - c1);
-        const uint32_t h0 = strict_claim<PAT_SW>(wkeys, p0.x, lane < pl);
-        const uint32_t h1 = strict_claim<PAT_SW>(wkeys, p1.x, lane + 32 < pl);
+        const uint32_t h0 = wt_insert(wkeys, p0.x, lane < pl);
+        const uint32_t h1 = wt_insert(wkeys, p1.x, lane + 32 < pl);
         if (lane < pl) winfo[h0] = make_uint2(p0.y, pre0);
         if (lane + 32 < pl) winfo[h1] = make_uint2(p1.y, pre1);
         {
@@ -653,10 +677,10 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         }
         __syncwarp();
         // ---- products: rank lookup + dense accumulate ----
-        row_products<OffT, ValT>(s, e, jn, an, aent, aval, brm, bent, bval, ptr, av, len,
+        row_products<OffT, ValT>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
                                  [&](uint32_t col, ValT prod) {
                                      if (col != EMPTY) {
-                                         const uint32_t h = strict_find<PAT_SW>(wkeys, col >> 5);
+                                         const uint32_t h = wt_find(wkeys, col >> 5);
                                          const uint2 wi = winfo[h];
                                          const uint32_t rk = wi.y + __popc(wi.x & ((1u << (col & 31)) - 1u));
                                          if (rk < (uint32_t)CAP) vals[rk] += prod;

@@ -191,20 +191,33 @@ static void launch_sym_warp(Launch& L, const SymArgs& a, int bin) {
 // ------------------------------------------------------------------------------------
 constexpr int PAT_WORDS = 64;  // max words of a stored row pattern
 
+struct __align__(16) SymRec {
+    const void* row;  // B_C pairs (uint2) or B entries (int32) of the A entry's B row
+    int len;
+    int pad;
+};
+
 template <typename OffT, int W, bool COMP>
 __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                 const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
                                                 const int32_t* __restrict__ bc_len, const uint2* __restrict__ pairs,
                                                 const int32_t* __restrict__ perm, int r0, int r1,
                                                 const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
-                                                uint32_t* bm, long long* sb, uint32_t* wl, const PatOut& po,
+                                                uint32_t* bm, SymRec* rec, uint32_t* wl, const PatOut& po,
                                                 DevStatus* st) {
     constexpr int NW = W / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
-    for (int r = r0 + blockIdx.x * warps + warp; r < r1; r += gridDim.x * warps) {
-        const int i = perm[r];
-        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+    const int stride = gridDim.x * warps;
+    int r = r0 + blockIdx.x * warps + warp;
+    // software pipeline over rows: the next row's bounds and first 32 A entries are
+    // loaded while the current row finishes
+    int i = perm[r];
+    int64_t s = ld(arm, i), e = ld(arm, i + 1);
+    int jn = lane < e - s ? __ldg(aent + s + lane) : 0;
+    while (true) {
         const uint32_t wb = (uint32_t)__ldg(wlo + i) >> 5;
+        const int rn = r + stride;
+        const int inext = rn < r1 ? perm[rn] : -1;
         int cnt = 0;
         int nt = 0;  // words touched (warp-uniform)
         auto step_or = [&](uint32_t w, uint32_t m) {
@@ -231,38 +244,41 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
         };
         for (int64_t c0 = s; c0 < e; c0 += 32) {
             const int na = (int)min((int64_t)32, e - c0);
+            int j = jn;
+            if (c0 != s && lane < na) j = __ldg(aent + c0 + lane);
             int bl = 0;
-            long long bb = 0;
-            if (lane < na) {
-                const int j = __ldg(aent + c0 + lane);
-                bb = (long long)ld(brm, j);
-                bl = COMP ? __ldg(bc_len + j) : (int)(ld(brm, j + 1) - bb);
-            }
             __syncwarp();
-            if (lane < na) sb[lane] = bb;
-            unsigned rem = __ballot_sync(FULL, bl > 0);
+            if (lane < na) {
+                const int64_t bb = ld(brm, j);
+                bl = COMP ? __ldg(bc_len + j) : (int)(ld(brm, j + 1) - bb);
+                SymRec sr;
+                sr.row = COMP ? (const void*)(pairs + bb) : (const void*)(bent + bb);
+                sr.len = bl;
+                sr.pad = 0;
+                rec[lane] = sr;
+            }
             const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
             __syncwarp();
+            if (maxbl == 0) continue;
+            auto load = [&](const SymRec& sr, int q, uint32_t& w, uint32_t& m) {
+                if (COMP) {
+                    const uint2 pr = __ldg((const uint2*)sr.row + q);
+                    w = pr.x;
+                    m = pr.y;
+                } else {
+                    const int c = __ldg((const int32_t*)sr.row + q);
+                    w = (uint32_t)c >> 5;
+                    m = 1u << (c & 31);
+                }
+            };
             if (maxbl <= 32) {
+                int t = 0;
                 auto fetch = [&](uint32_t& w, uint32_t& m) {
                     w = 0;
                     m = 0;
-                    if (!rem) return false;
-                    const int t = __ffs(rem) - 1;
-                    rem &= rem - 1;
-                    const int blt = __shfl_sync(FULL, bl, t);
-                    const long long bbt = sb[t];
-                    if (lane < blt) {
-                        if (COMP) {
-                            const uint2 pr = __ldg(pairs + bbt + lane);
-                            w = pr.x;
-                            m = pr.y;
-                        } else {
-                            const int c = __ldg(bent + bbt + lane);
-                            w = (uint32_t)c >> 5;
-                            m = 1u << (c & 31);
-                        }
-                    }
+                    if (t >= na) return false;
+                    const SymRec sr = rec[t++];
+                    if (lane < sr.len) load(sr, lane, w, m);
                     return true;
                 };
                 uint32_t w0, w1, w2, w3, m0, m1, m2, m3;
@@ -289,30 +305,22 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
                     h3 = fetch(w3, m3);
                 }
             } else {
-                while (rem) {
-                    const int t = __ffs(rem) - 1;
-                    rem &= rem - 1;
-                    const int blt = __shfl_sync(FULL, bl, t);
-                    const long long bbt = sb[t];
-                    for (int q0 = 0; q0 < blt; q0 += 32) {
+                for (int t = 0; t < na; ++t) {
+                    const SymRec sr = rec[t];
+                    for (int q0 = 0; q0 < sr.len; q0 += 32) {
                         uint32_t w = 0, m = 0;
-                        if (q0 + lane < blt) {
-                            if (COMP) {
-                                const uint2 pr = __ldg(pairs + bbt + q0 + lane);
-                                w = pr.x;
-                                m = pr.y;
-                            } else {
-                                const int c = __ldg(bent + bbt + q0 + lane);
-                                w = (uint32_t)c >> 5;
-                                m = 1u << (c & 31);
-                            }
-                        }
+                        if (q0 + lane < sr.len) load(sr, q0 + lane, w, m);
                         step_or(w, m);
                         __syncwarp();
                     }
                 }
             }
             __syncwarp();
+        }
+        int64_t sn = 0, en = 0;
+        if (inext >= 0) {
+            sn = ld(arm, inext);
+            en = ld(arm, inext + 1);
         }
         cnt = warp_sum(cnt);
         if (lane == 0) counts[i] = cnt;
@@ -352,7 +360,13 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
         } else {
             for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
         }
+        if (inext >= 0) jn = lane < en - sn ? __ldg(aent + sn + lane) : 0;
         __syncwarp();
+        if (inext < 0) break;
+        r = rn;
+        i = inext;
+        s = sn;
+        e = en;
     }
 }
 
@@ -365,28 +379,28 @@ __global__ void __launch_bounds__(256) k_sym_window(const OffT* __restrict__ arm
                                                     const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
                                                     PatOut po, DevStatus* st) {
     constexpr int NW = W / 32;
-    constexpr int WB = NW + 64 + PAT_WORDS;  // words per warp: bitmap | 32 x int64 | list
+    constexpr int WB = NW + 128 + PAT_WORDS;  // words per warp: bitmap | 32 x SymRec | list
     extern __shared__ __align__(16) uint32_t sm_win[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     uint32_t* bm = sm_win + (size_t)warp * WB;
-    long long* sb = (long long*)(bm + NW);  // per A entry of the chunk: B(_C) row start
-    uint32_t* wl = (uint32_t*)(sb + 32);
+    SymRec* rec = (SymRec*)(bm + NW);
+    uint32_t* wl = (uint32_t*)(rec + 32);
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     if (r0 + blockIdx.x * warps + warp >= r1) return;
     for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
     __syncwarp();
     if (st->use_comp)
-        sym_window_rows<OffT, W, true>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm, sb, wl,
+        sym_window_rows<OffT, W, true>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm, rec, wl,
                                        po, st);
     else
-        sym_window_rows<OffT, W, false>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm, sb, wl,
-                                        po, st);
+        sym_window_rows<OffT, W, false>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm, rec,
+                                        wl, po, st);
 }
 
 template <typename OffT, int W>
 static void launch_sym_window(Launch& L, const SymArgs& a, int bin) {
-    const int warps = W <= 8192 ? 8 : 4;
-    const size_t smem = (size_t)warps * ((size_t)W / 32 + 64 + PAT_WORDS) * 4;
+    const int warps = W <= 16384 ? 8 : 4;
+    const size_t smem = (size_t)warps * ((size_t)W / 32 + 128 + PAT_WORDS) * 4;
     auto kern = k_sym_window<OffT, W>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (a.A.nrows + warps - 1) / warps;
@@ -416,8 +430,10 @@ static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stre
                                                a.k, wbits, a.cursors, a.counts, a.st);
         L.end(s);
     }
-    launch_sym_window<OffT, 65536>(L, a, SYM_WIN_BIN0 + 2);
-    launch_sym_window<OffT, 32768>(L, a, SYM_WIN_BIN0 + 1);
+    launch_sym_window<OffT, 65536>(L, a, SYM_WIN_BIN0 + 4);
+    launch_sym_window<OffT, 49152>(L, a, SYM_WIN_BIN0 + 3);
+    launch_sym_window<OffT, 32768>(L, a, SYM_WIN_BIN0 + 2);
+    launch_sym_window<OffT, 16384>(L, a, SYM_WIN_BIN0 + 1);
     launch_sym_window<OffT, 8192>(L, a, SYM_WIN_BIN0);
     launch_sym_warp<OffT, 4096>(L, a, 7);
     launch_sym_warp<OffT, 2048>(L, a, 6);

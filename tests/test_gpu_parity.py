@@ -230,3 +230,48 @@ def test_C2_full_sampled(oracle_mod):
     # properties that hold at any size: rows strictly increasing, interior row sums zero
     lens = np.diff(got[0])
     assert lens.max() == 125 and int((lens == 125).sum()) == 96 ** 3
+
+
+def _banded(m, k, per_row, band, seed, values="random"):
+    """Sorted rows with `per_row` distinct columns drawn in [i*k/m - band, i*k/m + band]."""
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for i in range(m):
+        c = int(i * k // max(m, 1))
+        lo, hi = max(0, c - band), min(k, c + band + 1)
+        n = min(per_row, hi - lo)
+        sel = np.sort(rng.choice(np.arange(lo, hi), size=n, replace=False))
+        rows.append(np.full(n, i))
+        cols.append(sel)
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    rm = np.zeros(m + 1, dtype=np.int64)
+    np.add.at(rm, rows + 1, 1)
+    rm = np.cumsum(rm)
+    vals = rng.uniform(-1, 1, size=len(cols)) if values == "random" else np.ones(len(cols))
+    return g.CSR(m, k, torch.tensor(rm), torch.tensor(cols, dtype=torch.int32), torch.tensor(vals))
+
+
+@pytest.mark.parametrize("band,per_a,per_b", [(300, 20, 30), (6000, 12, 60), (30000, 6, 40), (40, 30, 30)])
+@pytest.mark.parametrize("vt", [torch.float64, torch.float32])
+def test_window_and_pattern_paths(oracle_mod, band, per_a, per_b, vt):
+    """Banded rows: symbolic bit-vector windows of every width class, rows whose pattern is
+    kept (<= 64 words) and rows whose pattern is not (numeric falls back to the hash)."""
+    n = 3000
+    A = _banded(1500, n, per_a, band // 4, seed=band)
+    B = _banded(n, n, per_b, band, seed=band + 1)
+    for ot in (torch.int32, torch.int64):
+        got = gpu_spgemm(A, B, value_dtype=vt, offset_dtype=ot)
+        assert_parity(oracle_mod, A, B, got, value_dtype=vt)
+        got = gpu_spgemm(A, B, value_dtype=vt, offset_dtype=ot, patterns=False)
+        assert_parity(oracle_mod, A, B, got, value_dtype=vt)
+
+
+def test_pattern_pool_overflow(oracle_mod):
+    """Rows of ~60 words each overflow the 48-pairs-per-row pattern pool: the rows that do
+    not get a slot are computed by the hash kernels; the result is unchanged."""
+    n = 4000
+    A = _banded(800, n, 24, 900, seed=5)
+    B = _banded(n, n, 40, 1000, seed=6)
+    got = gpu_spgemm(A, B)
+    assert_parity(oracle_mod, A, B, got)
