@@ -527,6 +527,7 @@ kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
     na.f64 = A->value_type == KK_F64;
     na.sort = h->opts.sort_rows != 0;
     na.strict = h->stats.b_strict != 0;
+    na.wlo = (const int32_t*)h->wlo.p;
     na.pat = (const uint2*)h->pat.p;
     na.pat_off = (const long long*)h->pat_off.p;
     na.pat_len = (const int*)h->pat_len.p;

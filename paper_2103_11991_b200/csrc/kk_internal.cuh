@@ -139,6 +139,7 @@ struct NumArgs {
     int32_t* cursors;
     const DevStatus* st;
     int logG;
+    const int32_t* wlo;          // window start per row (pattern rows)
     const uint2* pat;            // row patterns (see PatOut)
     const long long* pat_off;
     const int* pat_len;

@@ -294,23 +294,32 @@ __device__ __forceinline__ uint32_t strict_find(const uint32_t* keys, uint32_t c
     return h;
 }
 
-// Per A entry of the current 32-entry chunk: its B row (entries, values, length) and a_ij,
-// read back per step with two 16-byte shared loads.
+// Per A entry of the current 32-entry chunk: its B row (start, length) and a_ij, read back
+// per step with one (O32: element offsets < 2^31) or two 16-byte shared loads.
+template <typename ValT, bool O32>
+struct StepRec;
 template <typename ValT>
-struct __align__(16) StepRec {
-    const int32_t* ent;
-    const ValT* val;
+struct __align__(16) StepRec<ValT, true> {
+    int bb;
+    int len;
     double a;
+};
+template <typename ValT>
+struct __align__(16) StepRec<ValT, false> {
+    long long bb;
     int len;
     int pad;
+    double a;
+    double pad2;
 };
+constexpr size_t REC_BYTES = 32 * 32;  // room for 32 records of either kind
 
 // Shared-memory layout of one warp: vals[S] | rec[32] | keys[S] | stage[CAP]
 template <typename ValT, int S, int CAP>
 struct StrictLayout {
     static constexpr size_t vals = 0;
     static constexpr size_t rec = ((size_t)S * sizeof(ValT) + 15) / 16 * 16;
-    static constexpr size_t keys = rec + 32 * sizeof(StepRec<ValT>);
+    static constexpr size_t keys = rec + REC_BYTES;
     static constexpr size_t stage = keys + (size_t)S * 4;
     static constexpr size_t bytes = (stage + (size_t)CAP * 4 + 15) / 16 * 16;
 };
@@ -321,11 +330,13 @@ struct StrictLayout {
 // loaded three steps ahead of the step being inserted.  insert(col, a_ij * b_jk) is
 // called by all 32 lanes for every step (col = EMPTY on idle lanes); the <= 32 columns
 // of a step are the entries of one B row segment.
-template <typename OffT, typename ValT, typename Ins>
+template <typename OffT, typename ValT, bool O32, typename Ins>
 __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT an, const int32_t* __restrict__ aent,
                                              const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                              const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
-                                             StepRec<ValT>* rec, Ins insert) {
+                                             void* rec_raw, Ins insert) {
+    using R = StepRec<ValT, O32>;
+    R* rec = (R*)rec_raw;
     const int lane = threadIdx.x & 31;
     for (int64_t c0 = s; c0 < e; c0 += 32) {
         const int na = (int)min((int64_t)32, e - c0);
@@ -340,12 +351,10 @@ __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT 
         if (lane < na) {
             const int64_t bb = ld(brm, j);
             bl = (int)(ld(brm, j + 1) - bb);
-            StepRec<ValT> sr;
-            sr.ent = bent + bb;
-            sr.val = bval + bb;
-            sr.a = (double)a;
+            R sr;
+            sr.bb = (decltype(sr.bb))bb;
             sr.len = bl;
-            sr.pad = 0;
+            sr.a = (double)a;
             rec[lane] = sr;
         }
         const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
@@ -360,11 +369,11 @@ __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT 
                 bv = (ValT)0;
                 at = (ValT)0;
                 if (t >= na) return false;
-                const StepRec<ValT> sr = rec[t++];
+                const R sr = rec[t++];
                 at = (ValT)sr.a;
                 if (lane < sr.len) {
-                    col = (uint32_t)__ldg(sr.ent + lane);
-                    bv = __ldg(sr.val + lane);
+                    col = (uint32_t)__ldg(bent + (sr.bb + lane));
+                    bv = __ldg(bval + (sr.bb + lane));
                 }
                 return true;
             };
@@ -391,14 +400,14 @@ __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT 
         } else {
             // long B rows: 32-entry segments
             for (int t = 0; t < na; ++t) {
-                const StepRec<ValT> sr = rec[t];
+                const R sr = rec[t];
                 const ValT at = (ValT)sr.a;
                 for (int q0 = 0; q0 < sr.len; q0 += 32) {
                     uint32_t col = EMPTY;
                     ValT p = (ValT)0;
                     if (q0 + lane < sr.len) {
-                        col = (uint32_t)__ldg(sr.ent + q0 + lane);
-                        p = at * __ldg(sr.val + q0 + lane);
+                        col = (uint32_t)__ldg(bent + (sr.bb + q0 + lane));
+                        p = at * __ldg(bval + (sr.bb + q0 + lane));
                     }
                     insert(col, p);
                 }
@@ -408,7 +417,7 @@ __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT 
     }
 }
 
-template <typename OffT, typename ValT, int S, int CAP, bool SORT>
+template <typename OffT, typename ValT, int S, int CAP, bool SORT, bool O32>
 __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                     const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                                     const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
@@ -422,7 +431,7 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     unsigned char* base = sm_num + (size_t)warp * LY::bytes;
     ValT* vals = (ValT*)(base + LY::vals);
-    StepRec<ValT>* rec = (StepRec<ValT>*)(base + LY::rec);
+    void* rec = base + LY::rec;
     uint32_t* keys = (uint32_t*)(base + LY::keys);
     uint32_t* stage = (uint32_t*)(base + LY::stage);
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
@@ -449,8 +458,8 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
         const int clen = (int)(ld(crm, i + 1) - cb);
         const int rn = r + stride;
         const int inext = rn < r1 ? perm[rn] : -1;
-        row_products<OffT, ValT>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
-                                 [&](uint32_t col, ValT prod) {
+        row_products<OffT, ValT, O32>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
+                                      [&](uint32_t col, ValT prod) {
                                      const bool act = col != EMPTY;
                                      const uint32_t h = strict_claim<S>(keys, col, act);
                                      if (act) vals[h] += prod;
@@ -555,51 +564,19 @@ __global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm
 // plain shared load/add/store.  Entries are written straight from the pattern and the
 // values in order: the row is sorted without a sort.
 // ------------------------------------------------------------------------------------
-constexpr int PAT_W = 64;    // max words of a kept pattern (symbolic PAT_WORDS)
-constexpr int PAT_SW = 128;  // word-table slots
+constexpr int PAT_W = 64;       // max words of a kept pattern (symbolic PAT_WORDS)
+constexpr int PAT_NWIN = 2048;  // words of the widest symbolic window (64K bits)
 
 template <typename ValT, int CAP>
 struct PatLayout {
     static constexpr size_t vals = 0;
     static constexpr size_t rec = ((size_t)CAP * sizeof(ValT) + 15) / 16 * 16;
-    static constexpr size_t winfo = rec + 32 * sizeof(StepRec<ValT>);
-    static constexpr size_t wkeys = winfo + (size_t)PAT_SW * 8;
-    static constexpr size_t bytes = (wkeys + (size_t)PAT_SW * 4 + 15) / 16 * 16;
+    static constexpr size_t winfo = rec + REC_BYTES;
+    static constexpr size_t widx = winfo + (size_t)PAT_W * 8;
+    static constexpr size_t bytes = (widx + (size_t)PAT_NWIN + 15) / 16 * 16;
 };
 
-// word table of a kept pattern: multiplicative hash, linear probing over PAT_SW slots
-__device__ __forceinline__ uint32_t wt_slot(uint32_t w) { return (w * 0x9E3779B1u) >> (32 - ilog2(PAT_SW)); }
-
-// insert distinct words (write-verify claims, as strict_claim); returns the slot
-__device__ __forceinline__ uint32_t wt_insert(uint32_t* keys, uint32_t w, bool act) {
-    uint32_t h = wt_slot(w);
-    bool need = false;
-    if (act) {
-        while (keys[h] != EMPTY) h = (h + 1) & (PAT_SW - 1);
-        need = true;
-    }
-    while (__any_sync(FULL, need)) {
-        if (need) keys[h] = w;
-        __syncwarp();
-        if (need) {
-            if (keys[h] == w) {
-                need = false;
-            } else {
-                while (keys[h] != EMPTY) h = (h + 1) & (PAT_SW - 1);
-            }
-        }
-        __syncwarp();
-    }
-    return h;
-}
-
-__device__ __forceinline__ uint32_t wt_find(const uint32_t* keys, uint32_t w) {
-    uint32_t h = wt_slot(w);
-    while (keys[h] != w) h = (h + 1) & (PAT_SW - 1);
-    return h;
-}
-
-template <typename OffT, typename ValT, int CAP>
+template <typename OffT, typename ValT, int CAP, bool O32>
 __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                      const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                                      const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
@@ -607,21 +584,20 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
                                                      ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                      const int* __restrict__ bin_start, int bin,
                                                      const uint2* __restrict__ pat, const long long* __restrict__ pat_off,
-                                                     const int* __restrict__ pat_len) {
+                                                     const int* __restrict__ pat_len, const int32_t* __restrict__ wlo) {
     using LY = PatLayout<ValT, CAP>;
     extern __shared__ __align__(16) unsigned char sm_pat[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     unsigned char* base = sm_pat + (size_t)warp * LY::bytes;
     ValT* vals = (ValT*)(base + LY::vals);
-    StepRec<ValT>* rec = (StepRec<ValT>*)(base + LY::rec);
+    void* rec = base + LY::rec;
     uint2* winfo = (uint2*)(base + LY::winfo);
-    uint32_t* wkeys = (uint32_t*)(base + LY::wkeys);
+    uint8_t* widx = (uint8_t*)(base + LY::widx);
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     const int stride = gridDim.x * warps;
     int r = r0 + blockIdx.x * warps + warp;
     if (r >= r1) return;
     for (int t = lane; t < CAP; t += 32) vals[t] = (ValT)0;
-    for (int t = lane; t < PAT_SW; t += 32) wkeys[t] = EMPTY;
     __syncwarp();
     int i = perm[r];
     int64_t s = ld(arm, i), e = ld(arm, i + 1);
@@ -636,6 +612,7 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         const int clen = (int)(ld(crm, i + 1) - cb);
         const long long po = pat_off[i];
         const int pl = pat_len[i];
+        const uint32_t wb = (uint32_t)__ldg(wlo + i) >> 5;
         const int rn = r + stride;
         const int inext = rn < r1 ? perm[rn] : -1;
         // ---- the row's pattern: word table + entries ----
@@ -653,10 +630,15 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         }
         const int tot0 = __shfl_sync(FULL, x0, 31);
         const uint32_t pre0 = (uint32_t)(x0 - c0), pre1 = (uint32_t)(tot0 + x1 - c1);
-        const uint32_t h0 = wt_insert(wkeys, p0.x, lane < pl);
-        const uint32_t h1 = wt_insert(wkeys, p1.x, lane + 32 < pl);
-        if (lane < pl) winfo[h0] = make_uint2(p0.y, pre0);
-        if (lane + 32 < pl) winfo[h1] = make_uint2(p1.y, pre1);
+        // dense word index over the row's window (entries of other rows are never read)
+        if (lane < pl) {
+            widx[p0.x - wb] = (uint8_t)lane;
+            winfo[lane] = make_uint2(p0.y, pre0);
+        }
+        if (lane + 32 < pl) {
+            widx[p1.x - wb] = (uint8_t)(lane + 32);
+            winfo[lane + 32] = make_uint2(p1.y, pre1);
+        }
         {
             uint32_t m = p0.y;
             int o = (int)pre0;
@@ -677,11 +659,10 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         }
         __syncwarp();
         // ---- products: rank lookup + dense accumulate ----
-        row_products<OffT, ValT>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
-                                 [&](uint32_t col, ValT prod) {
+        row_products<OffT, ValT, O32>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
+                                      [&](uint32_t col, ValT prod) {
                                      if (col != EMPTY) {
-                                         const uint32_t h = wt_find(wkeys, col >> 5);
-                                         const uint2 wi = winfo[h];
+                                         const uint2 wi = winfo[widx[(col >> 5) - wb]];
                                          const uint32_t rk = wi.y + __popc(wi.x & ((1u << (col & 31)) - 1u));
                                          if (rk < (uint32_t)CAP) vals[rk] += prod;
                                      }
@@ -698,8 +679,6 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
             cval[cb + t] = vals[t];
             vals[t] = (ValT)0;
         }
-        if (lane < pl) wkeys[h0] = EMPTY;
-        if (lane + 32 < pl) wkeys[h1] = EMPTY;
         if (inext >= 0 && lane < en - sn) {
             jn = __ldg(aent + sn + lane);
             an = __ldg(aval + sn + lane);
@@ -719,7 +698,7 @@ static void launch_num_pattern(Launch& L, const NumArgs& a, int bin) {
     if (rows <= 0) return;
     const int warps = 8;
     const size_t smem = (size_t)warps * PatLayout<ValT, CAP>::bytes;
-    auto kern = k_num_pattern<OffT, ValT, CAP>;
+    auto kern = a.B.nnz < INT32_MAX ? k_num_pattern<OffT, ValT, CAP, true> : k_num_pattern<OffT, ValT, CAP, false>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (rows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
@@ -727,7 +706,7 @@ static void launch_num_pattern(Launch& L, const NumArgs& a, int bin) {
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                                (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
-                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len);
+                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len, a.wlo);
     L.end(L.stream);
 }
 
@@ -739,7 +718,8 @@ static void launch_num_strict_f(Launch& L, const NumArgs& a, int bin) {
     if (rows <= 0) return;
     const int warps = CAP <= 128 ? 8 : 4;
     const size_t smem = (size_t)warps * StrictLayout<ValT, S, CAP>::bytes;
-    auto kern = k_num_strict<OffT, ValT, S, CAP, SORT>;
+    auto kern = a.B.nnz < INT32_MAX ? k_num_strict<OffT, ValT, S, CAP, SORT, true>
+                                    : k_num_strict<OffT, ValT, S, CAP, SORT, false>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (rows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);

@@ -191,20 +191,32 @@ static void launch_sym_warp(Launch& L, const SymArgs& a, int bin) {
 // ------------------------------------------------------------------------------------
 constexpr int PAT_WORDS = 64;  // max words of a stored row pattern
 
-struct __align__(16) SymRec {
-    const void* row;  // B_C pairs (uint2) or B entries (int32) of the A entry's B row
+// Per A entry of the chunk: start (element offset into B_C pairs or B entries) and length
+// of its B row; O32 when offsets fit 31 bits (cheaper 32-bit addressing).
+template <bool O32>
+struct SymRec;
+template <>
+struct __align__(8) SymRec<true> {
+    int bb;
+    int len;
+};
+template <>
+struct __align__(16) SymRec<false> {
+    long long bb;
     int len;
     int pad;
 };
 
-template <typename OffT, int W, bool COMP>
+template <typename OffT, int W, bool COMP, bool O32>
 __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                 const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
                                                 const int32_t* __restrict__ bc_len, const uint2* __restrict__ pairs,
                                                 const int32_t* __restrict__ perm, int r0, int r1,
                                                 const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
-                                                uint32_t* bm, SymRec* rec, uint32_t* wl, const PatOut& po,
+                                                uint32_t* bm, void* rec_raw, uint32_t* wl, const PatOut& po,
                                                 DevStatus* st) {
+    using SR = SymRec<O32>;
+    SR* rec = (SR*)rec_raw;
     constexpr int NW = W / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     const int stride = gridDim.x * warps;
@@ -251,22 +263,21 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
             if (lane < na) {
                 const int64_t bb = ld(brm, j);
                 bl = COMP ? __ldg(bc_len + j) : (int)(ld(brm, j + 1) - bb);
-                SymRec sr;
-                sr.row = COMP ? (const void*)(pairs + bb) : (const void*)(bent + bb);
+                SR sr;
+                sr.bb = (decltype(sr.bb))bb;
                 sr.len = bl;
-                sr.pad = 0;
                 rec[lane] = sr;
             }
             const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
             __syncwarp();
             if (maxbl == 0) continue;
-            auto load = [&](const SymRec& sr, int q, uint32_t& w, uint32_t& m) {
+            auto load = [&](const SR& sr, int q, uint32_t& w, uint32_t& m) {
                 if (COMP) {
-                    const uint2 pr = __ldg((const uint2*)sr.row + q);
+                    const uint2 pr = __ldg(pairs + (sr.bb + q));
                     w = pr.x;
                     m = pr.y;
                 } else {
-                    const int c = __ldg((const int32_t*)sr.row + q);
+                    const int c = __ldg(bent + (sr.bb + q));
                     w = (uint32_t)c >> 5;
                     m = 1u << (c & 31);
                 }
@@ -277,7 +288,7 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
                     w = 0;
                     m = 0;
                     if (t >= na) return false;
-                    const SymRec sr = rec[t++];
+                    const SR sr = rec[t++];
                     if (lane < sr.len) load(sr, lane, w, m);
                     return true;
                 };
@@ -306,7 +317,7 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
                 }
             } else {
                 for (int t = 0; t < na; ++t) {
-                    const SymRec sr = rec[t];
+                    const SR sr = rec[t];
                     for (int q0 = 0; q0 < sr.len; q0 += 32) {
                         uint32_t w = 0, m = 0;
                         if (q0 + lane < sr.len) load(sr, q0 + lane, w, m);
@@ -377,24 +388,34 @@ __global__ void __launch_bounds__(256) k_sym_window(const OffT* __restrict__ arm
                                                     const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
                                                     const int* __restrict__ bin_start, int bin,
                                                     const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
-                                                    PatOut po, DevStatus* st) {
+                                                    PatOut po, DevStatus* st, long long nnzB) {
     constexpr int NW = W / 32;
     constexpr int WB = NW + 128 + PAT_WORDS;  // words per warp: bitmap | 32 x SymRec | list
     extern __shared__ __align__(16) uint32_t sm_win[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     uint32_t* bm = sm_win + (size_t)warp * WB;
-    SymRec* rec = (SymRec*)(bm + NW);
-    uint32_t* wl = (uint32_t*)(rec + 32);
+    void* rec = (void*)(bm + NW);
+    uint32_t* wl = bm + NW + 128;
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     if (r0 + blockIdx.x * warps + warp >= r1) return;
     for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
     __syncwarp();
-    if (st->use_comp)
-        sym_window_rows<OffT, W, true>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm, rec, wl,
-                                       po, st);
-    else
-        sym_window_rows<OffT, W, false>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm, rec,
-                                        wl, po, st);
+    const bool o32 = nnzB < INT32_MAX;
+    if (st->use_comp) {
+        if (o32)
+            sym_window_rows<OffT, W, true, true>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm,
+                                                 rec, wl, po, st);
+        else
+            sym_window_rows<OffT, W, true, false>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm,
+                                                  rec, wl, po, st);
+    } else {
+        if (o32)
+            sym_window_rows<OffT, W, false, true>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts, bm,
+                                                  rec, wl, po, st);
+        else
+            sym_window_rows<OffT, W, false, false>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, wlo, counts,
+                                                   bm, rec, wl, po, st);
+    }
 }
 
 template <typename OffT, int W>
@@ -408,7 +429,7 @@ static void launch_sym_window(Launch& L, const SymArgs& a, int bin) {
     L.begin(kname("sym_window", W), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
-                                               a.counts, a.pat, (DevStatus*)a.st);
+                                               a.counts, a.pat, (DevStatus*)a.st, (long long)a.B.nnz);
     L.end(L.stream);
 }
 

@@ -13,6 +13,6 @@ fi
 timeout 600 python bench.py --kernel-table --no-e2e --no-cpu-baseline "$@" > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"
 cat $OUT/bench_$TAG.json; tail -25 $OUT/bench_$TAG.err
 if [ "$NCUK" != "none" ]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$NCUK" -s 2 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$NCUK" -s 1 -c 2 \
       -o $OUT/prof_$TAG -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline "$@" > $OUT/ncu_$TAG.log 2>&1; echo "ncu rc=$?"
 fi
