@@ -103,7 +103,7 @@ struct kk_spgemm_handle_s {
     long long launches = 0;
     // workspace
     Buf flops, fscan, binid, perm_sym, perm_num, counts, binscratch, binstart, bc_len, pairs, cursors, partial,
-        status, bfirst, blast, wlo, pat, pat_off, pat_len;
+        status, bmeta, wlo, pat, pat_off, pat_len;
     DevStatus* h_status = nullptr;  // pinned
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -294,7 +294,7 @@ kk_status_t kk_spgemm_destroy(kk_spgemm_handle_t h) {
     cudaDeviceSynchronize();
     Buf* bufs[] = {&h->flops, &h->fscan, &h->binid, &h->perm_sym, &h->perm_num, &h->counts, &h->binscratch,
                    &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status,
-                   &h->bfirst, &h->blast, &h->wlo, &h->pat, &h->pat_off, &h->pat_len};
+                   &h->bmeta, &h->wlo, &h->pat, &h->pat_off, &h->pat_len};
     for (Buf* b : bufs) release(h, *b);
     delete h->timer;
     if (h->h_status) cudaFreeHost(h->h_status);
@@ -329,7 +329,7 @@ kk_status_t kk_spgemm_compress(kk_spgemm_handle_t h, const kk_csr_t* B, int32_t*
     DevStatus* dst = (DevStatus*)h->status.p;
     kk::init_status(L, dst);
     kk::check_compress(L, B->offset_type == KK_I64, view(B), B->ncols, true, h->opts.validate != 0, len,
-                       (uint2*)pairs, nullptr, nullptr, dst);
+                       (uint2*)pairs, nullptr, dst);
     return cuda_check(h, cudaGetLastError(), "kk_spgemm_compress launch");
 }
 
@@ -354,8 +354,8 @@ kk_status_t kk_spgemm_row_flops(kk_spgemm_handle_t h, const kk_csr_t* A, const k
     kk::Launch L = make_launch(h, s);
     DevStatus* dst = (DevStatus*)h->status.p;
     kk::init_status(L, dst);
-    kk::row_flops_bin(L, off64, view(A), view(B), B->ncols, 0, h->opts.validate != 0, nullptr, nullptr, nullptr,
-                      f, (uint8_t*)h->binid.p, (int32_t*)h->counts.p, nullptr, dst);
+    kk::row_flops_bin(L, off64, view(A), view(B), B->ncols, 0, h->opts.validate != 0, nullptr, nullptr, f,
+                      (uint8_t*)h->binid.p, (int32_t*)h->counts.p, nullptr, dst);
     if (flops_scan) kk::exclusive_scan(L, true, f, true, flops_scan, m, (int64_t*)h->partial.p, nullptr, nullptr);
     if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_row_flops launch")) != KK_OK) return st;
     if (total) {
@@ -393,8 +393,7 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     if ((st = ensure(h, h->binstart, sizeof(int) * 2 * (kk::NB + 1), s)) != KK_OK) return st;
     if ((st = ensure(h, h->partial, (size_t)kk::scan_partial_len(m) * 8, s)) != KK_OK) return st;
     if ((st = ensure(h, h->cursors, (size_t)A->nnz * 4, s)) != KK_OK) return st;
-    if ((st = ensure(h, h->bfirst, (size_t)n * 4, s)) != KK_OK) return st;
-    if ((st = ensure(h, h->blast, (size_t)n * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->bmeta, (size_t)n * 16, s)) != KK_OK) return st;
     if ((st = ensure(h, h->wlo, (size_t)m * 4, s)) != KK_OK) return st;
     const bool keep_pat = h->opts.patterns != 0;
     const int64_t pat_cap = keep_pat ? 48 * m : 0;
@@ -417,10 +416,10 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     kk::init_status(L, dst);
     // a4: sortedness flags (+ B_C unless compression is off)
     kk::check_compress(L, off64, Bv, k, comp_mode != 0, h->opts.validate != 0, (int32_t*)h->bc_len.p,
-                       (uint2*)h->pairs.p, (int32_t*)h->bfirst.p, (int32_t*)h->blast.p, dst);
+                       (uint2*)h->pairs.p, (int4*)h->bmeta.p, dst);
     // a1: flops per row, symbolic bins
     kk::row_flops_bin(L, off64, Av, Bv, k, comp_mode, h->opts.validate != 0, (const int32_t*)h->bc_len.p,
-                      (const int32_t*)h->bfirst.p, (const int32_t*)h->blast.p, (int64_t*)h->flops.p,
+                      (const int4*)h->bmeta.p, (int64_t*)h->flops.p,
                       (uint8_t*)h->binid.p, (int32_t*)h->counts.p, (int32_t*)h->wlo.p, dst);
     // a2: F = exclusive scan of flops (kept in the handle for flop-balanced partitioning)
     kk::exclusive_scan(L, true, h->flops.p, true, h->fscan.p, m, (int64_t*)h->partial.p, nullptr, nullptr);
@@ -593,7 +592,7 @@ kk_status_t kk_spgemm_stats(kk_spgemm_handle_t h, kk_spgemm_stats_t* out) {
     int64_t ws = 0;
     const Buf* bufs[] = {&h->flops, &h->fscan, &h->binid, &h->perm_sym, &h->perm_num, &h->counts, &h->binscratch,
                          &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status,
-                         &h->bfirst, &h->blast, &h->wlo, &h->pat, &h->pat_off, &h->pat_len};
+                         &h->bmeta, &h->wlo, &h->pat, &h->pat_off, &h->pat_len};
     for (const Buf* b : bufs) ws += (int64_t)b->bytes;
     out->workspace_bytes = ws;
     return KK_OK;

@@ -85,13 +85,15 @@ struct Launch {
 
 // ---- host launchers (kk_kernels.cu) -------------------------------------------------
 void init_status(Launch& L, DevStatus* st);
-// bfirst/blast (may be null): first and last column of each B row (INT_MAX / -1 if empty)
+// bmeta (may be null): per B row {nnz, |B_C row|, first column, last column}
+// (first/last = INT_MAX / -1 for empty rows)
 void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_comp, bool validate,
-                    int32_t* bc_len, uint2* pairs, int32_t* bfirst, int32_t* blast, DevStatus* st);
-// wlo (may be null): word-aligned first column of the window of rows in window bins
+                    int32_t* bc_len, uint2* pairs, int4* bmeta, DevStatus* st);
+// bmeta (may be null: then the B row map is read); wlo (may be null): word-aligned first
+// column of the window of rows in window bins
 void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, int64_t k, int comp_mode,
-                   bool validate, const int32_t* bc_len, const int32_t* bfirst, const int32_t* blast,
-                   int64_t* flops, uint8_t* binid, int32_t* counts, int32_t* wlo, DevStatus* st);
+                   bool validate, const int32_t* bc_len, const int4* bmeta, int64_t* flops, uint8_t* binid,
+                   int32_t* counts, int32_t* wlo, DevStatus* st);
 // exclusive scan of in[0..m) (int32 or int64) into out[0..m] (int32 or int64);
 // *total_dst (device, may be null) receives the sum; *overflow set when out is
 // int32 and the sum exceeds INT32_MAX.  partial: >= scan_partial_len(m) int64.

@@ -37,83 +37,142 @@ void init_status(Launch& L, DevStatus* st) {
 
 // ------------------------------------------------------------------------------------
 // a4: sortedness check + compression of B into B_C
-// One warp per row of B, 32 entries per step.  Adjacent equal words are merged with a
-// segmented OR scan; a word run that crosses a 32-entry chunk is carried in registers.
+// A warp takes 32 consecutive rows of B; each lane scans its own row sequentially (B
+// rows are short on stencil and graph inputs), merging adjacent equal words.  Rows
+// longer than LANE_ROW_MAX are then walked by the whole warp, 32 entries per step, with
+// a segmented OR scan; a word run that crosses a 32-entry chunk is carried in registers.
+// Per row it also writes bmeta = {nnz, |B_C row|, first column, last column}, the
+// record a1 gathers once per A entry.
 // ------------------------------------------------------------------------------------
+constexpr int LANE_ROW_MAX = 64;
+
+struct CompressFlags {
+    bool unsorted = false, nonstrict = false, bad = false;
+    unsigned long long words = 0;
+};
+
+template <typename OffT>
+__device__ __forceinline__ void compress_row_warp(int64_t j, int64_t k, const OffT* __restrict__ brm,
+                                                  const int32_t* __restrict__ bent, bool do_comp,
+                                                  int32_t* __restrict__ bc_len, uint2* __restrict__ pairs,
+                                                  int4* __restrict__ bmeta, CompressFlags& fl) {
+    const int lane = threadIdx.x & 31;
+    const int64_t s = ld(brm, j), e = ld(brm, j + 1);
+    int prev_last = INT_MIN;
+    int cw = -1;
+    unsigned cm = 0;
+    int outn = 0;
+    for (int64_t c0 = s; c0 < e; c0 += 32) {
+        const int64_t q = c0 + lane;
+        const bool act = q < e;
+        const int nact = (int)min((int64_t)32, e - c0);
+        const int col = act ? __ldg(bent + q) : INT_MAX;
+        int prev = __shfl_up_sync(FULL, col, 1);
+        if (lane == 0) prev = prev_last;
+        if (act) {
+            fl.unsorted |= col < prev;
+            fl.nonstrict |= col <= prev;
+            fl.bad |= (col < 0) || ((int64_t)col >= k);
+        }
+        prev_last = __shfl_sync(FULL, col, nact - 1);
+        if (do_comp) {
+            const int w = act ? (col >> 5) : INT_MAX;
+            const unsigned bit = act ? (1u << (col & 31)) : 0u;
+            int pw = __shfl_up_sync(FULL, w, 1);
+            if (lane == 0) pw = cw;
+            const bool head = act && (w != pw);
+            const unsigned heads = __ballot_sync(FULL, head);
+            if (cw >= 0 && (heads & 1u)) {  // the carried run ends before this chunk
+                if (lane == 0) pairs[s + outn] = make_uint2((unsigned)cw, cm);
+                ++outn;
+                cw = -1;
+                cm = 0;
+            }
+            const unsigned le = heads & lanemask_le();
+            const int seg = le ? (31 - __clz(le)) : 0;
+            unsigned v = bit;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned t = __shfl_up_sync(FULL, v, d);
+                if (lane >= d && lane - d >= seg) v |= t;
+            }
+            if (!le) v |= cm;  // continuation of the carried run
+            const bool flush = act && lane != nact - 1 && ((heads >> (lane + 1)) & 1u);
+            const unsigned fb = __ballot_sync(FULL, flush);
+            if (flush) pairs[s + outn + __popc(fb & lanemask_lt())] = make_uint2((unsigned)w, v);
+            outn += __popc(fb);
+            cw = __shfl_sync(FULL, w, nact - 1);
+            cm = __shfl_sync(FULL, v, nact - 1);
+        }
+    }
+    if (do_comp && cw >= 0) {
+        if (lane == 0) pairs[s + outn] = make_uint2((unsigned)cw, cm);
+        ++outn;
+    }
+    if (lane == 0) {
+        if (do_comp) bc_len[j] = outn;
+        if (bmeta) bmeta[j] = make_int4((int)(e - s), do_comp ? outn : 0, s < e ? __ldg(bent + s) : INT_MAX,
+                                        s < e ? prev_last : -1);
+    }
+    if (lane == 0 && do_comp) fl.words += (unsigned long long)outn;
+}
+
 template <typename OffT>
 __global__ void __launch_bounds__(256) k_check_compress(int64_t n, int64_t k, const OffT* __restrict__ brm,
                                                         const int32_t* __restrict__ bent, int do_comp,
                                                         int validate, int32_t* __restrict__ bc_len,
-                                                        uint2* __restrict__ pairs, int32_t* __restrict__ bfirst,
-                                                        int32_t* __restrict__ blast, DevStatus* st) {
+                                                        uint2* __restrict__ pairs, int4* __restrict__ bmeta,
+                                                        DevStatus* st) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    bool unsorted = false, nonstrict = false, bad = false;
-    unsigned long long words = 0;
-    for (int64_t j = gw; j < n; j += nw) {
-        const int64_t s = ld(brm, j), e = ld(brm, j + 1);
-        int prev_last = INT_MIN;
-        if (bfirst && lane == 0) bfirst[j] = s < e ? __ldg(bent + s) : INT_MAX;
-        int cw = -1;
-        unsigned cm = 0;
-        int outn = 0;
-        for (int64_t c0 = s; c0 < e; c0 += 32) {
-            const int64_t q = c0 + lane;
-            const bool act = q < e;
-            const int nact = (int)min((int64_t)32, e - c0);
-            const int col = act ? __ldg(bent + q) : INT_MAX;
-            int prev = __shfl_up_sync(FULL, col, 1);
-            if (lane == 0) prev = prev_last;
-            if (act) {
-                unsorted |= col < prev;
-                nonstrict |= col <= prev;
-                bad |= (col < 0) || ((int64_t)col >= k);
-            }
-            prev_last = __shfl_sync(FULL, col, nact - 1);
-            if (do_comp) {
-                const int w = act ? (col >> 5) : INT_MAX;
-                const unsigned bit = act ? (1u << (col & 31)) : 0u;
-                int pw = __shfl_up_sync(FULL, w, 1);
-                if (lane == 0) pw = cw;
-                const bool head = act && (w != pw);
-                const unsigned heads = __ballot_sync(FULL, head);
-                if (cw >= 0 && (heads & 1u)) {  // the carried run ends before this chunk
-                    if (lane == 0) pairs[s + outn] = make_uint2((unsigned)cw, cm);
-                    ++outn;
-                    cw = -1;
-                    cm = 0;
+    CompressFlags fl;
+    for (int64_t j0 = gw * 32; j0 < n; j0 += nw * 32) {
+        const int64_t j = j0 + lane;
+        bool long_row = false;
+        if (j < n) {
+            const int64_t s = ld(brm, j), e = ld(brm, j + 1);
+            if (e - s > LANE_ROW_MAX) {
+                long_row = true;
+            } else {
+                int prev = INT_MIN, cw = -1, outn = 0;
+                unsigned cm = 0;
+                for (int64_t q = s; q < e; ++q) {
+                    const int col = __ldg(bent + q);
+                    fl.unsorted |= col < prev;
+                    fl.nonstrict |= col <= prev;
+                    fl.bad |= (col < 0) || ((int64_t)col >= k);
+                    prev = col;
+                    if (do_comp) {
+                        const int w = col >> 5;
+                        if (w != cw) {
+                            if (cw >= 0) pairs[s + outn++] = make_uint2((unsigned)cw, cm);
+                            cw = w;
+                            cm = 0;
+                        }
+                        cm |= 1u << (col & 31);
+                    }
                 }
-                const unsigned le = heads & lanemask_le();
-                const int seg = le ? (31 - __clz(le)) : 0;
-                unsigned v = bit;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const unsigned t = __shfl_up_sync(FULL, v, d);
-                    if (lane >= d && lane - d >= seg) v |= t;
+                if (do_comp) {
+                    if (cw >= 0) pairs[s + outn++] = make_uint2((unsigned)cw, cm);
+                    bc_len[j] = outn;
+                    fl.words += (unsigned long long)outn;
                 }
-                if (!le) v |= cm;  // continuation of the carried run
-                const bool flush = act && lane != nact - 1 && ((heads >> (lane + 1)) & 1u);
-                const unsigned fb = __ballot_sync(FULL, flush);
-                if (flush) pairs[s + outn + __popc(fb & lanemask_lt())] = make_uint2((unsigned)w, v);
-                outn += __popc(fb);
-                cw = __shfl_sync(FULL, w, nact - 1);
-                cm = __shfl_sync(FULL, v, nact - 1);
+                if (bmeta) bmeta[j] = make_int4((int)(e - s), outn, s < e ? __ldg(bent + s) : INT_MAX, s < e ? prev : -1);
             }
         }
-        if (blast && lane == 0) blast[j] = s < e ? prev_last : -1;
-        if (do_comp) {
-            if (cw >= 0) {
-                if (lane == 0) pairs[s + outn] = make_uint2((unsigned)cw, cm);
-                ++outn;
-            }
-            if (lane == 0) bc_len[j] = outn;
-            words += (unsigned long long)outn;
+        unsigned lr = __ballot_sync(FULL, long_row);
+        while (lr) {
+            const int t = __ffs(lr) - 1;
+            lr &= lr - 1;
+            compress_row_warp(j0 + t, k, brm, bent, do_comp != 0, bc_len, pairs, bmeta, fl);
         }
     }
-    if (__any_sync(FULL, unsorted) && lane == 0) atomicAnd(&st->b_sorted, 0);
-    if (__any_sync(FULL, nonstrict) && lane == 0) atomicAnd(&st->b_strict, 0);
-    if (validate && __any_sync(FULL, bad) && lane == 0) atomicOr(&st->bad_index, 1);
+    if (__any_sync(FULL, fl.unsorted) && lane == 0) atomicAnd(&st->b_sorted, 0);
+    if (__any_sync(FULL, fl.nonstrict) && lane == 0) atomicAnd(&st->b_strict, 0);
+    if (validate && __any_sync(FULL, fl.bad) && lane == 0) atomicOr(&st->bad_index, 1);
+    unsigned long long words = fl.words;
+    for (int d = 16; d > 0; d >>= 1) words += __shfl_xor_sync(FULL, words, d);
     if (do_comp && lane == 0 && words) atomicAdd(&st->total_words, words);
 }
 
@@ -126,24 +185,25 @@ static int grid_for(int64_t warps_needed, int threads, int num_sms, int per_sm =
 }
 
 void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_comp, bool validate,
-                    int32_t* bc_len, uint2* pairs, int32_t* bfirst, int32_t* blast, DevStatus* st) {
+                    int32_t* bc_len, uint2* pairs, int4* bmeta, DevStatus* st) {
     if (B.nrows == 0) return;
     const int threads = 256;
-    const int grid = grid_for(B.nrows, threads, L.num_sms, 16);
+    const int grid = grid_for((B.nrows + 31) / 32, threads, L.num_sms, 16);
     L.begin(do_comp ? "check_compress" : "check_sorted", L.stream);
     if (off64)
         k_check_compress<int64_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int64_t*)B.row_map, B.entries,
-                                                                  do_comp, validate, bc_len, pairs, bfirst, blast,
-                                                                  st);
+                                                                  do_comp, validate, bc_len, pairs, bmeta, st);
     else
         k_check_compress<int32_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int32_t*)B.row_map, B.entries,
-                                                                  do_comp, validate, bc_len, pairs, bfirst, blast,
-                                                                  st);
+                                                                  do_comp, validate, bc_len, pairs, bmeta, st);
     L.end(L.stream);
 }
 
 // ------------------------------------------------------------------------------------
 // a1: per-row flops and the symbolic work bin of each row.
+// A warp takes 32 consecutive rows of A, one per lane (long rows: the whole warp); per
+// A entry one 16-byte gather of the B row's record (bmeta from a4; without it, the B
+// row map).
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ int sym_bin_of(int64_t ub) {
     if (ub <= 0) return 0;
@@ -172,14 +232,40 @@ __device__ __forceinline__ int sym_win_bin_of(int lo, int hi, int64_t ub) {
     return SYM_WIN_BIN0 + c;
 }
 
+struct FlopAcc {
+    int64_t f = 0, fc = 0;
+    int lo = INT_MAX, hi = -1;
+    bool bad = false;
+};
+
+template <typename OffT>
+__device__ __forceinline__ void flop_entry(int j, int64_t n, bool validate, const OffT* __restrict__ brm,
+                                           const int32_t* __restrict__ bc_len, const int4* __restrict__ bmeta,
+                                           bool comp, FlopAcc& acc) {
+    if (validate && (j < 0 || (int64_t)j >= n)) {
+        acc.bad = true;
+        return;
+    }
+    if (bmeta) {
+        const int4 m = __ldg(bmeta + j);
+        acc.f += m.x;
+        acc.fc += m.y;
+        acc.lo = min(acc.lo, m.z);
+        acc.hi = max(acc.hi, m.w);
+    } else {
+        acc.f += ld(brm, (int64_t)j + 1) - ld(brm, (int64_t)j);
+        if (comp) acc.fc += __ldg(bc_len + j);
+    }
+}
+
 template <typename OffT>
 __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t k, const OffT* __restrict__ arm,
                                                    const int32_t* __restrict__ aent, const OffT* __restrict__ brm,
                                                    const int32_t* __restrict__ bc_len, int comp_mode, int64_t nnzB,
-                                                   int validate, const int32_t* __restrict__ bfirst,
-                                                   const int32_t* __restrict__ blast, int64_t* __restrict__ flops,
-                                                   uint8_t* __restrict__ binid, int32_t* __restrict__ counts,
-                                                   int32_t* __restrict__ wlo, DevStatus* st) {
+                                                   int validate, const int4* __restrict__ bmeta,
+                                                   int64_t* __restrict__ flops, uint8_t* __restrict__ binid,
+                                                   int32_t* __restrict__ counts, int32_t* __restrict__ wlo,
+                                                   DevStatus* st) {
     bool comp = false;
     if (comp_mode == 1)
         comp = true;
@@ -190,69 +276,75 @@ __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t kw = (k + 31) >> 5;
-    const bool win = wlo != nullptr && bfirst != nullptr && st->b_sorted != 0;
+    const bool win = wlo != nullptr && bmeta != nullptr && st->b_sorted != 0;
     unsigned long long tot = 0;
     bool bad = false;
-    for (int64_t i = gw; i < m; i += nw) {
-        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
-        int64_t f = 0, fc = 0;
-        int lo = INT_MAX, hi = -1;
-        for (int64_t p = s + lane; p < e; p += 32) {
-            const int j = __ldg(aent + p);
-            if (validate && (j < 0 || (int64_t)j >= n)) {
-                bad = true;
-                continue;
-            }
-            f += ld(brm, (int64_t)j + 1) - ld(brm, (int64_t)j);
-            if (comp) fc += __ldg(bc_len + j);
-            if (win) {
-                lo = min(lo, __ldg(bfirst + j));
-                hi = max(hi, __ldg(blast + j));
+    for (int64_t i0 = gw * 32; i0 < m; i0 += nw * 32) {
+        const int64_t i = i0 + lane;
+        FlopAcc acc;
+        bool long_row = false;
+        if (i < m) {
+            const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+            if (e - s > LANE_ROW_MAX) {
+                long_row = true;
+            } else {
+                for (int64_t p = s; p < e; ++p) flop_entry(__ldg(aent + p), n, validate, brm, bc_len, bmeta, comp, acc);
             }
         }
-        f = warp_sum(f);
-        if (comp) fc = warp_sum(fc);
-        if (win) {
-            lo = __reduce_min_sync(FULL, lo);
-            hi = __reduce_max_sync(FULL, hi);
+        unsigned lr = __ballot_sync(FULL, long_row);
+        while (lr) {
+            const int t = __ffs(lr) - 1;
+            lr &= lr - 1;
+            const int64_t it = i0 + t;
+            const int64_t s = ld(arm, it), e = ld(arm, it + 1);
+            FlopAcc w;
+            for (int64_t p = s + lane; p < e; p += 32) flop_entry(__ldg(aent + p), n, validate, brm, bc_len, bmeta, comp, w);
+            w.f = warp_sum(w.f);
+            w.fc = warp_sum(w.fc);
+            w.lo = __reduce_min_sync(FULL, w.lo);
+            w.hi = __reduce_max_sync(FULL, w.hi);
+            w.bad = __any_sync(FULL, w.bad);
+            if (lane == t) acc = w;
         }
-        if (lane == 0) {
-            flops[i] = f;
-            const int64_t ub = comp ? min(fc, kw) : min(f, k);
+        if (i < m) {
+            bad |= acc.bad;
+            flops[i] = acc.f;
+            const int64_t ub = comp ? min(acc.fc, kw) : min(acc.f, k);
             int b = sym_bin_of(ub);
             if (win && b > 0) {
-                const int wb = sym_win_bin_of(lo, hi, ub);
-                if (wb) {
-                    b = wb;
-                    wlo[i] = lo & ~31;
+                const int wbn = sym_win_bin_of(acc.lo, acc.hi, ub);
+                if (wbn) {
+                    b = wbn;
+                    wlo[i] = acc.lo & ~31;
                 }
             }
             binid[i] = (uint8_t)b;
             if (b == 0) counts[i] = 0;
-            tot += (unsigned long long)f;
+            tot += (unsigned long long)acc.f;
         }
     }
     if (validate && __any_sync(FULL, bad) && lane == 0) atomicOr(&st->bad_index, 1);
+    for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(FULL, tot, d);
     if (lane == 0 && tot) atomicAdd(&st->total_flops, tot);
 }
 
 void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, int64_t k, int comp_mode,
-                   bool validate, const int32_t* bc_len, const int32_t* bfirst, const int32_t* blast,
-                   int64_t* flops, uint8_t* binid, int32_t* counts, int32_t* wlo, DevStatus* st) {
+                   bool validate, const int32_t* bc_len, const int4* bmeta, int64_t* flops, uint8_t* binid,
+                   int32_t* counts, int32_t* wlo, DevStatus* st) {
     if (A.nrows == 0) return;
     const int threads = 256;
-    const int grid = grid_for(A.nrows, threads, L.num_sms, 16);
+    const int grid = grid_for((A.nrows + 31) / 32, threads, L.num_sms, 16);
     L.begin("row_flops_bin", L.stream);
     if (off64)
         k_row_flops<int64_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int64_t*)A.row_map,
                                                              A.entries, (const int64_t*)B.row_map, bc_len,
-                                                             comp_mode, B.nnz, validate, bfirst, blast, flops, binid,
-                                                             counts, wlo, st);
+                                                             comp_mode, B.nnz, validate, bmeta, flops, binid, counts,
+                                                             wlo, st);
     else
         k_row_flops<int32_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int32_t*)A.row_map,
                                                              A.entries, (const int32_t*)B.row_map, bc_len,
-                                                             comp_mode, B.nnz, validate, bfirst, blast, flops, binid,
-                                                             counts, wlo, st);
+                                                             comp_mode, B.nnz, validate, bmeta, flops, binid, counts,
+                                                             wlo, st);
     L.end(L.stream);
 }
 
@@ -425,18 +517,18 @@ void numeric_binid(Launch& L, int64_t m, const int32_t* counts, const long long*
     L.end(L.stream);
 }
 
-constexpr int BCHUNK = 2048;  // rows per warp in the binning passes
+// Stable binning in tiles of BTILE rows (one CTA of BWARPS warps, BROWS rows per warp):
+// pass 1 counts rows per bin per tile, pass 2 (one CTA) turns the counts into tile
+// offsets per bin and the bin starts, pass 3 scatters rows in row order within a bin.
+constexpr int BWARPS = 8;
+constexpr int BROWS = 256;
+constexpr int BTILE = BWARPS * BROWS;
 
-int64_t bin_scratch_len(int64_t m) { return ((m + BCHUNK - 1) / BCHUNK) * NB + NB + 1; }
+int64_t bin_scratch_len(int64_t m) { return ((m + BTILE - 1) / BTILE) * NB + NB + 1; }
 
-// pass 1: per-chunk bin histogram (warp per chunk; lane b counts bin b)
-__global__ void __launch_bounds__(256) k_bin_count(int64_t m, const uint8_t* __restrict__ binid,
-                                                   int32_t* __restrict__ chunkcnt) {
+// per-warp histogram of its BROWS rows: lane b ends with the count of bin b
+__device__ __forceinline__ int warp_bin_hist(int64_t r0, int64_t r1, const uint8_t* __restrict__ binid) {
     const int lane = threadIdx.x & 31;
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nchunks = (m + BCHUNK - 1) / BCHUNK;
-    if (c >= nchunks) return;
-    const int64_t r0 = c * BCHUNK, r1 = min(m, r0 + BCHUNK);
     int cnt = 0;
     for (int64_t base = r0; base < r1; base += 32) {
         const int64_t r = base + lane;
@@ -447,21 +539,36 @@ __global__ void __launch_bounds__(256) k_bin_count(int64_t m, const uint8_t* __r
             if (lane == t) cnt += __popc(bal);
         }
     }
-    if (lane < NB) chunkcnt[c * NB + lane] = cnt;
+    return cnt;
 }
 
-// pass 2: per bin, exclusive scan over chunks (+ bin start); one block
-__global__ void __launch_bounds__(1024) k_bin_offsets(int64_t nchunks, int32_t* __restrict__ chunkcnt,
+__global__ void __launch_bounds__(BWARPS * 32) k_bin_count(int64_t m, const uint8_t* __restrict__ binid,
+                                                           int32_t* __restrict__ tilecnt) {
+    __shared__ int wc[BWARPS][NB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * BTILE + (int64_t)warp * BROWS, r1 = min(m, r0 + BROWS);
+    const int cnt = r0 < m ? warp_bin_hist(r0, r1, binid) : 0;
+    if (lane < NB) wc[warp][lane] = cnt;
+    __syncthreads();
+    if (threadIdx.x < NB) {
+        int t = 0;
+        for (int w = 0; w < BWARPS; ++w) t += wc[w][threadIdx.x];
+        tilecnt[(int64_t)blockIdx.x * NB + threadIdx.x] = t;
+    }
+}
+
+// one CTA of 1024 threads: exclusive scan over tiles, bin by bin
+__global__ void __launch_bounds__(1024) k_bin_offsets(int64_t ntiles, int32_t* __restrict__ tilecnt,
                                                       int* __restrict__ bin_start_dst) {
     __shared__ int64_t totals[NB];
     for (int b = 0; b < NB; ++b) {
         int64_t carry = 0;
-        for (int64_t c0 = 0; c0 < nchunks; c0 += blockDim.x) {
+        for (int64_t c0 = 0; c0 < ntiles; c0 += blockDim.x) {
             const int64_t c = c0 + threadIdx.x;
-            const int64_t v = c < nchunks ? chunkcnt[c * NB + b] : 0;
+            const int64_t v = c < ntiles ? tilecnt[c * NB + b] : 0;
             int64_t ex;
             const int64_t tot = block_exclusive_scan(v, &ex);
-            if (c < nchunks) chunkcnt[c * NB + b] = (int32_t)(carry + ex);
+            if (c < ntiles) tilecnt[c * NB + b] = (int32_t)(carry + ex);
             carry += tot;
         }
         if (threadIdx.x == 0) totals[b] = carry;
@@ -477,16 +584,21 @@ __global__ void __launch_bounds__(1024) k_bin_offsets(int64_t nchunks, int32_t* 
     }
 }
 
-// pass 3: stable scatter of rows into perm
-__global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const uint8_t* __restrict__ binid,
-                                                     const int32_t* __restrict__ chunkcnt,
-                                                     const int* __restrict__ bin_start, int32_t* __restrict__ perm) {
-    const int lane = threadIdx.x & 31;
-    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nchunks = (m + BCHUNK - 1) / BCHUNK;
-    if (c >= nchunks) return;
-    const int64_t r0 = c * BCHUNK, r1 = min(m, r0 + BCHUNK);
-    int run = lane < NB ? bin_start[lane] + chunkcnt[c * NB + lane] : 0;
+__global__ void __launch_bounds__(BWARPS * 32) k_bin_scatter(int64_t m, const uint8_t* __restrict__ binid,
+                                                             const int32_t* __restrict__ tilecnt,
+                                                             const int* __restrict__ bin_start,
+                                                             int32_t* __restrict__ perm) {
+    __shared__ int wc[BWARPS][NB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * BTILE + (int64_t)warp * BROWS, r1 = min(m, r0 + BROWS);
+    const int cnt = r0 < m ? warp_bin_hist(r0, r1, binid) : 0;
+    if (lane < NB) wc[warp][lane] = cnt;
+    __syncthreads();
+    int run = 0;
+    if (lane < NB) {
+        run = bin_start[lane] + tilecnt[(int64_t)blockIdx.x * NB + lane];
+        for (int w = 0; w < warp; ++w) run += wc[w][lane];
+    }
     for (int64_t base = r0; base < r1; base += 32) {
         const int64_t r = base + lane;
         const int b = r < r1 ? (int)binid[r] : 255;
@@ -501,16 +613,15 @@ __global__ void __launch_bounds__(256) k_bin_scatter(int64_t m, const uint8_t* _
 }
 
 void bin_rows(Launch& L, int64_t m, const uint8_t* binid, int32_t* scratch, int32_t* perm, int* bin_start_dst) {
-    const int64_t nchunks = (m + BCHUNK - 1) / BCHUNK;
-    if (nchunks == 0) {
+    const int64_t ntiles = (m + BTILE - 1) / BTILE;
+    if (ntiles == 0) {
         cudaMemsetAsync(bin_start_dst, 0, sizeof(int) * (NB + 1), L.stream);
         return;
     }
-    const int grid = (int)((nchunks * 32 + 255) / 256);
     L.begin("bin_rows", L.stream);
-    k_bin_count<<<grid, 256, 0, L.stream>>>(m, binid, scratch);
-    k_bin_offsets<<<1, 1024, 0, L.stream>>>(nchunks, scratch, bin_start_dst);
-    k_bin_scatter<<<grid, 256, 0, L.stream>>>(m, binid, scratch, bin_start_dst, perm);
+    k_bin_count<<<(unsigned)ntiles, BWARPS * 32, 0, L.stream>>>(m, binid, scratch);
+    k_bin_offsets<<<1, 1024, 0, L.stream>>>(ntiles, scratch, bin_start_dst);
+    k_bin_scatter<<<(unsigned)ntiles, BWARPS * 32, 0, L.stream>>>(m, binid, scratch, bin_start_dst, perm);
     L.end(L.stream, 3);
 }
 

@@ -217,6 +217,7 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
                                                 DevStatus* st) {
     using SR = SymRec<O32>;
     SR* rec = (SR*)rec_raw;
+    SR* units = (SR*)((uint32_t*)rec_raw + 128);  // up to 128 units of <= 8 pairs
     constexpr int NW = W / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     const int stride = gridDim.x * warps;
@@ -283,14 +284,66 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
                 }
             };
             if (maxbl <= 32) {
-                int t = 0;
+                // B_C rows cut into units of SG pairs; a step takes SP = 32 / SG units, one
+                // per group of SG lanes.  Words repeat across units, so the groups update
+                // the bit vector in SP phases (a unit's own words are distinct).
+                constexpr int SG = 8, SPH = 32 / SG;
+                const int nseg = (bl + SG - 1) / SG;
+                int incl = nseg;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int y = __shfl_up_sync(FULL, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                const int U = __shfl_sync(FULL, incl, 31);
+                if (lane < na) {
+                    const SR sr = rec[lane];
+                    for (int q = 0, ex = incl - nseg; q < nseg; ++q) {
+                        SR un;
+                        un.bb = sr.bb + q * SG;
+                        un.len = min(SG, bl - q * SG);
+                        units[ex + q] = un;
+                    }
+                }
+                __syncwarp();
+                const int g = lane / SG, sl = lane % SG;
+                int u0 = 0;
                 auto fetch = [&](uint32_t& w, uint32_t& m) {
                     w = 0;
                     m = 0;
-                    if (t >= na) return false;
-                    const SR sr = rec[t++];
-                    if (lane < sr.len) load(sr, lane, w, m);
+                    if (u0 >= U) return false;
+                    const int u = u0 + g;
+                    u0 += SPH;
+                    if (u < U) {
+                        const SR un = units[u];
+                        if (sl < un.len) load(un, sl, w, m);
+                    }
                     return true;
+                };
+                auto step_or4 = [&](uint32_t w, uint32_t m) {
+                    bool fresh = false;
+                    const uint32_t x = w - wb;
+#pragma unroll
+                    for (int ph = 0; ph < SPH; ++ph) {
+                        if (g == ph && m) {
+                            uint32_t old;
+                            if (COMP) {
+                                old = bm[x];
+                                bm[x] = old | m;
+                            } else {
+                                old = atomicOr(&bm[x], m);
+                            }
+                            cnt += __popc(m & ~old);
+                            fresh = old == 0;
+                        }
+                        __syncwarp();
+                    }
+                    const unsigned fb = __ballot_sync(FULL, fresh);
+                    if (fresh) {
+                        const int pos = nt + __popc(fb & lanemask_lt());
+                        if (pos < PAT_WORDS) wl[pos] = x;
+                    }
+                    nt += __popc(fb);
                 };
                 uint32_t w0, w1, w2, w3, m0, m1, m2, m3;
                 fetch(w0, m0);
@@ -298,21 +351,17 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
                 bool h2 = fetch(w2, m2);
                 bool h3 = fetch(w3, m3);
                 while (true) {
-                    step_or(w0, m0);
+                    step_or4(w0, m0);
                     if (!h1) break;
-                    __syncwarp();
                     const bool h0 = fetch(w0, m0);
-                    step_or(w1, m1);
+                    step_or4(w1, m1);
                     if (!h2) break;
-                    __syncwarp();
                     h1 = fetch(w1, m1);
-                    step_or(w2, m2);
+                    step_or4(w2, m2);
                     if (!h3) break;
-                    __syncwarp();
                     h2 = fetch(w2, m2);
-                    step_or(w3, m3);
+                    step_or4(w3, m3);
                     if (!h0) break;
-                    __syncwarp();
                     h3 = fetch(w3, m3);
                 }
             } else {
@@ -390,12 +439,12 @@ __global__ void __launch_bounds__(256) k_sym_window(const OffT* __restrict__ arm
                                                     const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
                                                     PatOut po, DevStatus* st, long long nnzB) {
     constexpr int NW = W / 32;
-    constexpr int WB = NW + 128 + PAT_WORDS;  // words per warp: bitmap | 32 x SymRec | list
+    constexpr int WB = NW + 640 + PAT_WORDS;  // words per warp: bitmap | 32 recs | 128 units | list
     extern __shared__ __align__(16) uint32_t sm_win[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     uint32_t* bm = sm_win + (size_t)warp * WB;
     void* rec = (void*)(bm + NW);
-    uint32_t* wl = bm + NW + 128;
+    uint32_t* wl = bm + NW + 640;
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     if (r0 + blockIdx.x * warps + warp >= r1) return;
     for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
@@ -421,7 +470,7 @@ __global__ void __launch_bounds__(256) k_sym_window(const OffT* __restrict__ arm
 template <typename OffT, int W>
 static void launch_sym_window(Launch& L, const SymArgs& a, int bin) {
     const int warps = W <= 16384 ? 8 : 4;
-    const size_t smem = (size_t)warps * ((size_t)W / 32 + 128 + PAT_WORDS) * 4;
+    const size_t smem = (size_t)warps * ((size_t)W / 32 + 640 + PAT_WORDS) * 4;
     auto kern = k_sym_window<OffT, W>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (a.A.nrows + warps - 1) / warps;
