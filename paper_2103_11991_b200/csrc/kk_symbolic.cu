@@ -190,6 +190,7 @@ static void launch_sym_warp(Launch& L, const SymArgs& a, int bin) {
 // than PL words clear the whole window and keep no pattern.
 // ------------------------------------------------------------------------------------
 constexpr int PAT_WORDS = 64;  // max words of a stored row pattern
+constexpr int FLAT_WORDS = 512;  // room for the flattened pair offsets of a chunk
 
 // Per A entry of the chunk: start (element offset into B_C pairs or B entries) and length
 // of its B row; O32 when offsets fit 31 bits (cheaper 32-bit addressing).
@@ -217,7 +218,9 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
                                                 DevStatus* st) {
     using SR = SymRec<O32>;
     SR* rec = (SR*)rec_raw;
-    SR* units = (SR*)((uint32_t*)rec_raw + 128);  // up to 128 units of <= 8 pairs
+    // flattened pair offsets of a chunk (FLAT_CAP entries of SR::bb), per-lane scratch
+    decltype(SR::bb)* flat = (decltype(SR::bb)*)((uint32_t*)rec_raw + 128);
+    uint32_t* scratch = (uint32_t*)rec_raw + 128 + FLAT_WORDS;
     constexpr int NW = W / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     const int stride = gridDim.x * warps;
@@ -283,60 +286,55 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
                     m = 1u << (c & 31);
                 }
             };
-            if (maxbl <= 32) {
-                // B_C rows cut into units of SG pairs; a step takes SP = 32 / SG units, one
-                // per group of SG lanes.  Words repeat across units, so the groups update
-                // the bit vector in SP phases (a unit's own words are distinct).
-                constexpr int SG = 8, SPH = 32 / SG;
-                const int nseg = (bl + SG - 1) / SG;
-                int incl = nseg;
+            // pairs of the chunk's B_C rows, flattened: 32 consecutive pairs per step
+            int incl = bl;
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int y = __shfl_up_sync(FULL, incl, d);
-                    if (lane >= d) incl += y;
-                }
-                const int U = __shfl_sync(FULL, incl, 31);
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const int U = __shfl_sync(FULL, incl, 31);
+            constexpr int FLAT_CAP = FLAT_WORDS * 4 / (int)sizeof(SR::bb);  // else one B row per step
+            if (U <= FLAT_CAP) {
                 if (lane < na) {
                     const SR sr = rec[lane];
-                    for (int q = 0, ex = incl - nseg; q < nseg; ++q) {
-                        SR un;
-                        un.bb = sr.bb + q * SG;
-                        un.len = min(SG, bl - q * SG);
-                        units[ex + q] = un;
-                    }
+                    for (int q = 0, ex = incl - bl; q < bl; ++q) flat[ex + q] = sr.bb + q;
                 }
                 __syncwarp();
-                const int g = lane / SG, sl = lane % SG;
                 int u0 = 0;
                 auto fetch = [&](uint32_t& w, uint32_t& m) {
                     w = 0;
                     m = 0;
                     if (u0 >= U) return false;
-                    const int u = u0 + g;
-                    u0 += SPH;
-                    if (u < U) {
-                        const SR un = units[u];
-                        if (sl < un.len) load(un, sl, w, m);
+                    const int p = u0 + lane;
+                    u0 += 32;
+                    if (p < U) {
+                        SR one;
+                        one.bb = flat[p];
+                        load(one, 0, w, m);
                     }
                     return true;
                 };
-                auto step_or4 = [&](uint32_t w, uint32_t m) {
-                    bool fresh = false;
+                // equal words in a step are merged (match + OR over the group); the group
+                // leader updates the bit vector, so all updates of a step are distinct words
+                auto step_merge = [&](uint32_t w, uint32_t m) {
                     const uint32_t x = w - wb;
-#pragma unroll
-                    for (int ph = 0; ph < SPH; ++ph) {
-                        if (g == ph && m) {
-                            uint32_t old;
-                            if (COMP) {
-                                old = bm[x];
-                                bm[x] = old | m;
-                            } else {
-                                old = atomicOr(&bm[x], m);
-                            }
-                            cnt += __popc(m & ~old);
-                            fresh = old == 0;
+                    const uint32_t key = m ? x : (0x80000000u | (uint32_t)lane);
+                    const unsigned grp = __match_any_sync(FULL, key);
+                    scratch[lane] = m;
+                    __syncwarp();
+                    uint32_t mm = m;
+                    bool fresh = false;
+                    if (m && lane == __ffs(grp) - 1) {
+                        unsigned peers = grp & (grp - 1);  // the group without its leader
+                        while (peers) {
+                            mm |= scratch[__ffs(peers) - 1];
+                            peers &= peers - 1;
                         }
-                        __syncwarp();
+                        const uint32_t old = bm[x];
+                        bm[x] = old | mm;
+                        cnt += __popc(mm & ~old);
+                        fresh = old == 0;
                     }
                     const unsigned fb = __ballot_sync(FULL, fresh);
                     if (fresh) {
@@ -351,17 +349,21 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
                 bool h2 = fetch(w2, m2);
                 bool h3 = fetch(w3, m3);
                 while (true) {
-                    step_or4(w0, m0);
+                    step_merge(w0, m0);
                     if (!h1) break;
+                    __syncwarp();
                     const bool h0 = fetch(w0, m0);
-                    step_or4(w1, m1);
+                    step_merge(w1, m1);
                     if (!h2) break;
+                    __syncwarp();
                     h1 = fetch(w1, m1);
-                    step_or4(w2, m2);
+                    step_merge(w2, m2);
                     if (!h3) break;
+                    __syncwarp();
                     h2 = fetch(w2, m2);
-                    step_or4(w3, m3);
+                    step_merge(w3, m3);
                     if (!h0) break;
+                    __syncwarp();
                     h3 = fetch(w3, m3);
                 }
             } else {
@@ -439,12 +441,12 @@ __global__ void __launch_bounds__(256) k_sym_window(const OffT* __restrict__ arm
                                                     const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
                                                     PatOut po, DevStatus* st, long long nnzB) {
     constexpr int NW = W / 32;
-    constexpr int WB = NW + 640 + PAT_WORDS;  // words per warp: bitmap | 32 recs | 128 units | list
+    constexpr int WB = NW + 672 + PAT_WORDS;  // words per warp: bitmap | recs | flat | scratch | list
     extern __shared__ __align__(16) uint32_t sm_win[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     uint32_t* bm = sm_win + (size_t)warp * WB;
     void* rec = (void*)(bm + NW);
-    uint32_t* wl = bm + NW + 640;
+    uint32_t* wl = bm + NW + 672;
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     if (r0 + blockIdx.x * warps + warp >= r1) return;
     for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
@@ -470,7 +472,7 @@ __global__ void __launch_bounds__(256) k_sym_window(const OffT* __restrict__ arm
 template <typename OffT, int W>
 static void launch_sym_window(Launch& L, const SymArgs& a, int bin) {
     const int warps = W <= 16384 ? 8 : 4;
-    const size_t smem = (size_t)warps * ((size_t)W / 32 + 640 + PAT_WORDS) * 4;
+    const size_t smem = (size_t)warps * ((size_t)W / 32 + 672 + PAT_WORDS) * 4;
     auto kern = k_sym_window<OffT, W>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (a.A.nrows + warps - 1) / warps;
