@@ -51,7 +51,7 @@ WORKLOADS = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
@@ -96,60 +96,87 @@ def alg_bytes(A, B, crm, nnz, val_size):
     return sym, num
 
 
+def _clock_proc(idx, period, conn):
+    """Child process: poll NVML (SM clock, clock-event reasons) until told to stop."""
+    out = []
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        get_r = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+        conn.send(("ready", mx))
+        while not conn.poll():
+            out.append((time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), int(get_r(h))))
+            time.sleep(period)
+    except Exception as e:  # noqa: BLE001
+        conn.send(("error", str(e)))
+        return
+    conn.recv()
+    conn.send(("samples", out))
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    """SM clocks and clock-event (throttle) reasons polled through NVML every few ms by a
+    separate process (no GIL contention with the timed loop); only samples taken inside
+    the timed region [mark_start, mark_end] are kept (the B200_PROFILING.md clocks line)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
-    def __init__(self, gpu_index):
+    def __init__(self, gpu_index, period_s=0.002):
+        import multiprocessing as mp
+
+        self.ctx = mp.get_context("spawn")
         self.idx = gpu_index
+        self.period = period_s
         self.proc = None
-        self.lines = []
-        self.t = None
+        self.conn = None
+        self.max_mhz = None
+        self.err = None
+        self.t0 = self.t1 = None
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except (OSError, FileNotFoundError):
-            self.proc = None
-            return
-        self.t = threading.Thread(target=self._read, daemon=True)
-        self.t.start()
+        a, b = self.ctx.Pipe()
+        self.conn = a
+        self.proc = self.ctx.Process(target=_clock_proc, args=(self.idx, self.period, b), daemon=True)
+        self.proc.start()
+        if a.poll(60):
+            kind, v = a.recv()
+            if kind == "ready":
+                self.max_mhz = v
+            else:
+                self.err = v
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        if self.t:
-            self.t.join(timeout=2)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 9:
-                continue
-            try:
-                sm.append(float(p[1]))
-                mx.append(float(p[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        samples = []
+        if self.proc is not None and self.err is None:
+            self.conn.send("stop")
+            if self.conn.poll(30):
+                kind, v = self.conn.recv()
+                if kind == "samples":
+                    samples = v
+                else:
+                    self.err = v
+            self.proc.join(timeout=10)
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = self.t1 if self.t1 is not None else float("inf")
+        win = [(c, r) for t, c, r in samples if t0 <= t <= t1]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [self.err or "no samples"], "samples": 0}
+        mask = 0
+        for _, r in win:
+            mask |= r
+        return {"sm_mhz": statistics.median(c for c, _ in win), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(n for n, bit in self.REASONS.items() if mask & bit), "samples": len(win)}
 
 
 def load_peaks():
@@ -335,6 +362,8 @@ def run_ours(args):
             ev[2].record(stream)
         return n
 
+    clk = ClockSampler(local)
+    clk.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -344,17 +373,17 @@ def run_ours(args):
     h.timing_reset()
     launches0 = st0["kernel_launches"]
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    clk = ClockSampler(local)
-    clk.start()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk.mark_start()
     t_start.record(stream)
     for k in range(args.steps):
         step(evs[k])
     t_end.record(stream)
     torch.cuda.synchronize()
+    clk.mark_end()
     if dist is not None:
         dist.barrier()
     clocks = clk.stop()

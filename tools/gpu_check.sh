@@ -13,10 +13,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG
 tail -2 $OUT/smoke_$TAG.log
 timeout 600 python bench.py --kernel-table > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"
 cat $OUT/bench_$TAG.json; tail -30 $OUT/bench_$TAG.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_num_strict -s 3 -c 3 \
-    -o $OUT/prof_num_$TAG -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sym_warp -s 3 -c 3 \
-    -o $OUT/prof_sym_$TAG -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full_sym_$TAG.log 2>&1; echo "ncu sym rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k regex:"num_pattern<int, double, \(int\)128,|window.*49152" -s 2 -c 2 \
+    -o $OUT/prof_top_$TAG -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 ls -la $OUT
