@@ -12,7 +12,7 @@ namespace kk {
 // The compaction is followed by the fused per-row sort (a8) and a coalesced write.
 // ------------------------------------------------------------------------------------
 template <typename OffT, typename ValT, int S, bool SORT>
-__global__ void __launch_bounds__(256) k_num_warp(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+__global__ void __launch_bounds__(256, 1) k_num_warp(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                   const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                                   const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
                                                   const OffT* __restrict__ crm, int32_t* __restrict__ cent,
@@ -417,8 +417,97 @@ __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT 
     }
 }
 
+// As row_products, two B rows per warp step: insert2(col0, a*b0, col1, a*b1) gets the
+// products of B rows t (col0) and t+1 (col1).  Columns repeat between the two rows, so
+// callers must update row t's products before row t+1's.  Loads run two steps (four B
+// rows) ahead.
+template <typename OffT, typename ValT, bool O32, typename Ins2>
+__device__ __forceinline__ void row_products2(int64_t s, int64_t e, int jn, ValT an, const int32_t* __restrict__ aent,
+                                              const ValT* __restrict__ aval, const OffT* __restrict__ brm,
+                                              const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                              void* rec_raw, Ins2 insert2) {
+    using R = StepRec<ValT, O32>;
+    R* rec = (R*)rec_raw;
+    const int lane = threadIdx.x & 31;
+    for (int64_t c0 = s; c0 < e; c0 += 32) {
+        const int na = (int)min((int64_t)32, e - c0);
+        int j = jn;
+        ValT a = an;
+        if (c0 != s && lane < na) {
+            j = __ldg(aent + c0 + lane);
+            a = __ldg(aval + c0 + lane);
+        }
+        int bl = 0;
+        __syncwarp();
+        if (lane < na) {
+            const int64_t bb = ld(brm, j);
+            bl = (int)(ld(brm, j + 1) - bb);
+            R sr;
+            sr.bb = (decltype(sr.bb))bb;
+            sr.len = bl;
+            sr.a = (double)a;
+            rec[lane] = sr;
+        }
+        const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
+        __syncwarp();
+        if (maxbl == 0) continue;
+        if (maxbl <= 32) {
+            int t = 0;
+            auto fetch = [&](uint32_t& c0_, ValT& b0_, ValT& a0_, uint32_t& c1_, ValT& b1_, ValT& a1_) {
+                c0_ = c1_ = EMPTY;
+                b0_ = b1_ = a0_ = a1_ = (ValT)0;
+                if (t >= na) return false;
+                const R r0 = rec[t];
+                a0_ = (ValT)r0.a;
+                if (lane < r0.len) {
+                    c0_ = (uint32_t)__ldg(bent + (r0.bb + lane));
+                    b0_ = __ldg(bval + (r0.bb + lane));
+                }
+                if (t + 1 < na) {
+                    const R r1 = rec[t + 1];
+                    a1_ = (ValT)r1.a;
+                    if (lane < r1.len) {
+                        c1_ = (uint32_t)__ldg(bent + (r1.bb + lane));
+                        b1_ = __ldg(bval + (r1.bb + lane));
+                    }
+                }
+                t += 2;
+                return true;
+            };
+            uint32_t xc0, xc1, yc0, yc1;
+            ValT xb0, xb1, xa0, xa1, yb0, yb1, ya0, ya1;
+            fetch(xc0, xb0, xa0, xc1, xb1, xa1);
+            bool hy = fetch(yc0, yb0, ya0, yc1, yb1, ya1);
+            while (true) {
+                insert2(xc0, xa0 * xb0, xc1, xa1 * xb1);
+                if (!hy) break;
+                const bool hx = fetch(xc0, xb0, xa0, xc1, xb1, xa1);
+                insert2(yc0, ya0 * yb0, yc1, ya1 * yb1);
+                if (!hx) break;
+                hy = fetch(yc0, yb0, ya0, yc1, yb1, ya1);
+            }
+        } else {
+            // long B rows: 32-entry segments, one per step
+            for (int t = 0; t < na; ++t) {
+                const R sr = rec[t];
+                const ValT at = (ValT)sr.a;
+                for (int q0 = 0; q0 < sr.len; q0 += 32) {
+                    uint32_t col = EMPTY;
+                    ValT p = (ValT)0;
+                    if (q0 + lane < sr.len) {
+                        col = (uint32_t)__ldg(bent + (sr.bb + q0 + lane));
+                        p = at * __ldg(bval + (sr.bb + q0 + lane));
+                    }
+                    insert2(col, p, EMPTY, (ValT)0);
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 template <typename OffT, typename ValT, int S, int CAP, bool SORT, bool O32>
-__global__ void __launch_bounds__(256) k_num_strict(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+__global__ void __launch_bounds__(256, 1) k_num_strict(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                     const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                                     const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
                                                     const OffT* __restrict__ crm, int32_t* __restrict__ cent,
@@ -659,14 +748,23 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         }
         __syncwarp();
         // ---- products: rank lookup + dense accumulate ----
+        // (shared accesses go through sm_pat with 32-bit offsets: no generic addressing)
+        const uint32_t o_idx = (uint32_t)warp * (uint32_t)LY::bytes + (uint32_t)LY::widx - wb;
+        const uint32_t o_inf = (uint32_t)warp * (uint32_t)LY::bytes + (uint32_t)LY::winfo;
+        const uint32_t o_val = (uint32_t)warp * (uint32_t)LY::bytes + (uint32_t)LY::vals;
+        auto rank = [&](uint32_t col) {
+            const uint32_t wi = sm_pat[o_idx + (col >> 5)];
+            const uint2 mp = *(const uint2*)(sm_pat + o_inf + wi * 8u);
+            return mp.y + __popc(mp.x & ((1u << (col & 31)) - 1u));
+        };
         row_products<OffT, ValT, O32>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
                                       [&](uint32_t col, ValT prod) {
-                                     if (col != EMPTY) {
-                                         const uint2 wi = winfo[widx[(col >> 5) - wb]];
-                                         const uint32_t rk = wi.y + __popc(wi.x & ((1u << (col & 31)) - 1u));
-                                         if (rk < (uint32_t)CAP) vals[rk] += prod;
-                                     }
-                                 });
+                                          if (col != EMPTY) {
+                                              const uint32_t rk = rank(col);
+                                              if (rk < (uint32_t)CAP) *(ValT*)(sm_pat + o_val + rk * sizeof(ValT)) += prod;
+                                          }
+                                          __syncwarp();
+                                      });
         int64_t sn = 0, en = 0;
         if (inext >= 0) {
             sn = ld(arm, inext);

@@ -433,7 +433,7 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
 }
 
 template <typename OffT, int W>
-__global__ void __launch_bounds__(256) k_sym_window(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+__global__ void __launch_bounds__(256, 1) k_sym_window(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                     const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
                                                     const int32_t* __restrict__ bc_len,
                                                     const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
