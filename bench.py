@@ -43,6 +43,7 @@ UNIT = "GFLOP/s"
 WORKLOADS = {
     "C1": "A*A 2D 5-point Laplacian 32x32 (1,024 rows)",
     "C2": "A*A 3D 27-point Laplacian 100^3 (1,000,000 rows)",
+    "C3": "Galerkin R*(A*P): 3D 7-point Laplacian 128^3, 3x3x3 aggregation P, R = P^T (two products)",
     "C4": "A*A RMAT scale 20, edge factor 16, directed (1,048,576 rows)",
     "C5": "A*A 3D 27-point block stencil, 3 dof/node, 160^3 (12,288,000 rows)",
 }
@@ -76,10 +77,10 @@ def offset_dtype_for(cfg):
 
 
 def make_workload(cfg, size, values, device):
+    """(A, B) for the A*B configs; (A, P, R) for C3."""
     from workloads import generators as g
 
-    A, B = g.config(cfg, size=size, values=values, device=device)
-    return A, B
+    return g.config(cfg, size=size, values=values, device=device)
 
 
 def nbytes(t):
@@ -259,7 +260,8 @@ def run_reference(args):
     oracle.build()
     cores = len(os.sched_getaffinity(0))
     oracle.set_num_threads(cores)
-    A, B = make_workload(args.config, args.size, args.values, "cpu")
+    mats = make_workload(args.config, args.size, args.values, "cpu")
+    A, B = mats[0], mats[1]  # C3: the first product T = A*P
     rows = args.cpu_rows or max(1, A.nrows // 8)
     As, r0 = oracle_sample(A, rows)
     Bh = B.to(value_dtype=torch.float64)
@@ -309,18 +311,20 @@ def run_ours(args):
 
     # ---- workload (generated on the device: inputs resident in HBM) ----
     t_bcast = None
+    def conv(M):
+        return CsrMatrix(M.nrows, M.ncols, M.row_map.to(odt), M.entries, M.values.to(vdt))
+
     if world == 1:
-        A0, B0 = make_workload(args.config, args.size, args.values, dev)
-        A = CsrMatrix(A0.nrows, A0.ncols, A0.row_map.to(odt), A0.entries, A0.values.to(vdt))
-        B = CsrMatrix(B0.nrows, B0.ncols, B0.row_map.to(odt), B0.entries, B0.values.to(vdt))
-        del A0, B0
+        mats = [conv(M) for M in make_workload(args.config, args.size, args.values, dev)]
+        A, B = mats[0], mats[1]
         r0, r1 = 0, A.nrows
     else:
+        if args.config == "C3":
+            raise SystemExit("C3 (two chained products) is benchmarked on one GPU")
         from paper_2103_11991_b200.parallel import broadcast_csr, flop_balanced_cuts, slice_rows
 
         if rank == 0:
-            _, B0 = make_workload(args.config, args.size, args.values, dev)
-            B0 = CsrMatrix(B0.nrows, B0.ncols, B0.row_map.to(odt), B0.entries, B0.values.to(vdt))
+            B0 = conv(make_workload(args.config, args.size, args.values, dev)[1])
         else:
             B0 = None
         torch.cuda.synchronize()
@@ -339,40 +343,58 @@ def run_ours(args):
         cuts = flop_balanced_cuts(F.cpu().numpy(), world)
         r0, r1 = cuts[rank], cuts[rank + 1]
         A = slice_rows(B, r0, r1)
+        mats = [A, B]
 
-    h = SpGEMM(device=dev, timing=True)
     stream = torch.cuda.current_stream(dev)
-    crm = torch.empty(A.nrows + 1, dtype=odt, device=dev)
-    _, nnz = h.symbolic(A, B, c_row_map=crm)
-    cent = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
-    cval = torch.empty(max(nnz, 1), dtype=vdt, device=dev)
+
+    class Product:
+        """One C = X*Y of the step: its handle, row map and preallocated C arrays."""
+
+        def __init__(self, X, Y):
+            self.X, self.Y = X, Y
+            self.h = SpGEMM(device=dev, timing=True)
+            self.crm = torch.empty(X.nrows + 1, dtype=odt, device=dev)
+            _, n = self.h.symbolic(X, Y, c_row_map=self.crm)
+            self.cent = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            self.cval = torch.empty(max(n, 1), dtype=vdt, device=dev)
+            self.nnz = n
+
+        def C(self):
+            return CsrMatrix(self.X.nrows, self.Y.ncols, self.crm, self.cent[:self.nnz], self.cval[:self.nnz])
+
+    # the step's products: A*B, or for C3 T = A*P then Ac = R*T (T stays in HBM)
+    prods = [Product(A, B)]
+    if args.config == "C3":
+        prods.append(Product(mats[2], prods[0].C()))
     nnz_all = torch.zeros(world, dtype=torch.int64, device=dev)
 
     def step(ev=None):
+        for k, pr in enumerate(prods):
+            if ev is not None:
+                ev[2 * k].record(stream)
+            _, n = pr.h.symbolic(pr.X, pr.Y, c_row_map=pr.crm)
+            if world > 1:
+                mine = torch.tensor([n], dtype=torch.int64, device=dev)
+                dist.all_gather_into_tensor(nnz_all, mine)
+            if ev is not None:
+                ev[2 * k + 1].record(stream)
+            pr.h.numeric(pr.X, pr.Y, pr.crm, nnz=n, c_entries=pr.cent[:n], c_values=pr.cval[:n])
         if ev is not None:
-            ev[0].record(stream)
-        _, n = h.symbolic(A, B, c_row_map=crm)
-        if world > 1:
-            mine = torch.tensor([n], dtype=torch.int64, device=dev)
-            dist.all_gather_into_tensor(nnz_all, mine)
-        if ev is not None:
-            ev[1].record(stream)
-        h.numeric(A, B, crm, nnz=n, c_entries=cent[:n], c_values=cval[:n])
-        if ev is not None:
-            ev[2].record(stream)
-        return n
+            ev[2 * len(prods)].record(stream)
 
     clk = ClockSampler(local)
     clk.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    st0 = h.stats()
-    muladds = st0["muladds"]
-    nnz = st0["nnz_c"]
-    h.timing_reset()
-    launches0 = st0["kernel_launches"]
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sts = [pr.h.stats() for pr in prods]
+    muladds = sum(st["muladds"] for st in sts)
+    nnz = sts[-1]["nnz_c"]
+    for pr in prods:
+        pr.h.timing_reset()
+    launches0 = sum(st["kernel_launches"] for st in sts)
+    ne = 2 * len(prods) + 1
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(ne)] for _ in range(args.steps)]
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -387,11 +409,19 @@ def run_ours(args):
     if dist is not None:
         dist.barrier()
     clocks = clk.stop()
-    launches = h.stats()["kernel_launches"] - launches0
-    ktimes = h.kernel_times()
+    launches = sum(pr.h.stats()["kernel_launches"] for pr in prods) - launches0
+    ktimes = {}
+    for pr in prods:
+        for name, n_, tot, mx in pr.h.kernel_times():
+            a_ = ktimes.setdefault(name, [name, 0, 0.0, 0.0])
+            a_[1] += n_
+            a_[2] += tot
+            a_[3] = max(a_[3], mx)
+    ktimes = [tuple(v) for v in ktimes.values()]
     ms_total = t_start.elapsed_time(t_end)
-    sym_ms = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
-    num_ms = statistics.median(e[1].elapsed_time(e[2]) for e in evs)
+    sym_ms = statistics.median(sum(e[2 * k].elapsed_time(e[2 * k + 1]) for k in range(len(prods))) for e in evs)
+    num_ms = statistics.median(sum(e[2 * k + 1].elapsed_time(e[2 * k + 2]) for k in range(len(prods)))
+                               for e in evs)
 
     # max over ranks (device-timed); aggregate work = sum over ranks
     if dist is not None:
@@ -408,7 +438,11 @@ def run_ours(args):
     gflops = 2.0 * muladds_all / (ms_step * 1e-3) / 1e9
 
     val_size = 8 if vdt == torch.float64 else 4
-    sym_b, num_b = alg_bytes(A, B, crm, nnz, val_size)
+    sym_b = num_b = 0
+    for pr, st in zip(prods, sts):
+        sb, nb = alg_bytes(pr.X, pr.Y, pr.crm, st["nnz_c"], val_size)
+        sym_b += sb
+        num_b += nb
     if dist is not None:
         w = torch.tensor([sym_b, num_b], dtype=torch.int64, device=dev)
         dist.all_reduce(w)
@@ -426,7 +460,7 @@ def run_ours(args):
     # numeric phase = the dominant unit on every config here (~85% of bytes);
     # its algorithmic bytes per step are the numeric bytes.
     roof_achieved = num_b / (num_launch_ms * 1e-3) / 1e9 if num_launch_ms > 0 else None
-    traffic = ncu_traffic()
+    traffic = ncu_traffic() if args.config == "C2" and args.size is None else None
     roofline = {"bound": "hbm", "achieved": round(roof_achieved, 1) if roof_achieved else None,
                 "peak": peak, "unit": "GB/s", "frac": round(roof_achieved / peak, 4) if roof_achieved else None,
                 "traffic": (traffic or {}).get("dram_bytes_per_step"),
@@ -443,14 +477,32 @@ def run_ours(args):
 
     # ---- e2e through the public API from pinned host buffers (N=1; per rank for N>1) ----
     e2e = None
-    if not args.no_e2e:
-        Ah = CsrMatrix(A.nrows, A.ncols, A.row_map.cpu().pin_memory(), A.entries.cpu().pin_memory(),
-                       A.values.cpu().pin_memory())
-        Bh = CsrMatrix(B.nrows, B.ncols, B.row_map.cpu().pin_memory(), B.entries.cpu().pin_memory(),
-                       B.values.cpu().pin_memory())
-        he = SpGEMM(device=dev)
+    host_bytes = sum(nbytes(x) for M in mats for x in (M.row_map, M.entries, M.values)) + \
+        nnz * (4 + val_size) + (prods[-1].X.nrows + 1) * 8
+    if args.no_e2e:
+        e2e = None
+    elif host_bytes > 48e9:
+        e2e = {"value": None, "unit": UNIT, "skipped": f"inputs + C = {host_bytes / 1e9:.0f} GB of pinned host memory"}
+    else:
+        def host(M):
+            return CsrMatrix(M.nrows, M.ncols, M.row_map.cpu().pin_memory(), M.entries.cpu().pin_memory(),
+                             M.values.cpu().pin_memory())
+
+        hmats = [host(M) for M in mats]
+        hes = [SpGEMM(device=dev) for _ in prods]
+
+        def e2e_step():
+            # the user-level host path: C = A*B, or T = A*P then Ac = R*T, each call copying
+            # its operands in and its result out
+            C = hes[0].multiply_host(hmats[0], hmats[1])
+            ins = [hmats[0], hmats[1]]
+            if len(prods) > 1:
+                ins += [hmats[2], C]
+                C = hes[1].multiply_host(hmats[2], C)
+            return ins, C
+
         for _ in range(2):
-            he.multiply_host(Ah, Bh)
+            e2e_step()
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
@@ -458,7 +510,7 @@ def run_ours(args):
         e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_s.record(stream)
         for _ in range(reps):
-            Ch = he.multiply_host(Ah, Bh)
+            ins, Ch = e2e_step()
         e_e.record(stream)
         torch.cuda.synchronize()
         e_ms = e_s.elapsed_time(e_e) / reps
@@ -466,21 +518,28 @@ def run_ours(args):
             t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = t.item()
-        h2d = sum(nbytes(x) for x in (Ah.row_map, Ah.entries, Ah.values, Bh.row_map, Bh.entries, Bh.values))
+        h2d = sum(nbytes(x) for M in ins for x in (M.row_map, M.entries, M.values))
         d2h = sum(nbytes(x) for x in (Ch.row_map, Ch.entries, Ch.values))
+        if len(prods) > 1:
+            d2h += sum(nbytes(x) for x in (ins[3].row_map, ins[3].entries, ins[3].values))
         if dist is not None:
             w = torch.tensor([h2d, d2h], dtype=torch.int64, device=dev)
             dist.all_reduce(w)
             h2d, d2h = w.tolist()
         e2e = {"value": round(2.0 * muladds_all / (e_ms * 1e-3) / 1e9, 3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3)}
-        he.close()
-        del Ah, Bh
+        for he in hes:
+            he.close()
+        del hmats
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rows = args.cpu_rows or max(1, A.nrows // 4)
+        # a quarter of the rows, fewer when the product is big (bounded oracle memory/time)
+        frac = min(0.25, 2e8 / max(sts[0]["muladds"], 1))
+        rows = args.cpu_rows or max(1, int(A.nrows * frac))
         cpu = cpu_baseline(A, B, args.cpu_seconds, rows)
+        if args.config == "C3":
+            cpu["sample"] = "first product T = A*P only: " + cpu["sample"]
 
     if rank == 0:
         out = {"metric": METRIC, "value": round(gflops, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -499,7 +558,8 @@ def run_ours(args):
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clocks}
         print(json.dumps(out), flush=True)
-    h.close()
+    for pr in prods:
+        pr.h.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

@@ -1,0 +1,117 @@
+"""Full-size configurations of BASELINE.json (C3, C4, C5) on the GPU, checked against the
+oracle on sampled rows (the oracle computes those rows one by one; it is not run on the
+whole product) plus properties that hold at any size.
+
+Opt-in (minutes, up to ~120 GB of device memory): KK_FULLSIZE=1 pytest -m gpu tests/test_gpu_fullsize.py
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from workloads import generators as g
+
+from .helpers import assert_parity
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("KK_FULLSIZE") != "1", reason="set KK_FULLSIZE=1")]
+
+
+def _dev(M, ot, vt=torch.float64):
+    from paper_2103_11991_b200 import CsrMatrix
+
+    return CsrMatrix(M.nrows, M.ncols, M.row_map.to(ot), M.entries, M.values.to(vt))
+
+
+def _host(M):
+    return g.CSR(M.nrows, M.ncols, M.row_map.to(torch.int64).cpu(), M.entries.cpu(), M.values.cpu().double())
+
+
+def _rows_sample(m, k, seed):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([rng.integers(0, m, size=k), [0, m - 1, m // 2]]))
+
+
+def _check_rows(oracle_mod, A, B, rm, ent, val, rows):
+    from .helpers import sample_rows
+
+    As = sample_rows(A, rows)
+    orm, oent, oval, obnd = oracle_mod.spgemm(As, B)
+    for r in rows:
+        g0, g1 = int(rm[r]), int(rm[r + 1])
+        o0, o1 = int(orm[r]), int(orm[r + 1])
+        assert g1 - g0 == o1 - o0, f"row {r}: nnz {g1 - g0} vs {o1 - o0}"
+        ge = ent[g0:g1].cpu().numpy()
+        gv = val[g0:g1].cpu().double().numpy()
+        assert np.array_equal(ge, oent[o0:o1]), f"row {r}: columns differ"
+        assert np.array_equal(gv, oval[o0:o1]), f"row {r}: values differ (integer-valued config)"
+
+
+def test_C4_rmat_full(oracle_mod):
+    """RMAT scale 20 (directed, unit values): nnz(C) = 9,703,269,060 needs int64 offsets;
+    hub rows (483,882 entries) run through the CTA-owned dense tiers."""
+    from paper_2103_11991_b200 import SpGEMM
+
+    A, B = g.config("C4", device="cuda")
+    Ad, Bd = _dev(A, torch.int64), _dev(B, torch.int64)
+    h = SpGEMM()
+    rm, nnz = h.symbolic(Ad, Bd)
+    st = h.stats()
+    assert st["muladds"] == 20927401865 and nnz == 9703269060
+    ent, val = h.numeric(Ad, Bd, rm, nnz=nnz)
+    torch.cuda.synchronize()
+    # rows: random + the heaviest rows
+    lens = (rm[1:] - rm[:-1]).cpu().numpy()
+    heavy = np.argsort(lens)[-8:]
+    rows = np.unique(np.concatenate([_rows_sample(A.nrows, 200, 3), heavy]))
+    _check_rows(oracle_mod, _host(A), _host(B), rm.cpu(), ent, val, rows)
+    # row sums identity (unit values): sum_j C(i,j) = sum_{k in A(i,:)} outdeg(k)
+    rs = torch.zeros(A.nrows, dtype=torch.float64, device="cuda")
+    rows_of = torch.repeat_interleave(torch.arange(A.nrows, device="cuda"), torch.diff(rm))
+    rs.index_add_(0, rows_of, val)
+    outdeg = torch.diff(Bd.row_map).double()
+    ar = torch.repeat_interleave(torch.arange(A.nrows, device="cuda"), torch.diff(Ad.row_map))
+    want = torch.zeros_like(rs).index_add_(0, ar, outdeg[Ad.entries.long()])
+    assert torch.equal(rs, want)
+    h.close()
+
+
+def test_C5_block_stencil_full(oracle_mod):
+    """27-point block stencil, 3 dof/node, 160^3: nnz(C) = 9(5n-6)^3, multiply-adds 27(9n-10)^3."""
+    from paper_2103_11991_b200 import SpGEMM
+
+    n = 160
+    A, B = g.config("C5", device="cuda")
+    Ad, Bd = _dev(A, torch.int64), _dev(B, torch.int64)
+    h = SpGEMM()
+    rm, nnz = h.symbolic(Ad, Bd)
+    st = h.stats()
+    assert nnz == 9 * (5 * n - 6) ** 3 and st["muladds"] == 27 * (9 * n - 10) ** 3
+    ent, val = h.numeric(Ad, Bd, rm, nnz=nnz)
+    torch.cuda.synchronize()
+    rows = _rows_sample(A.nrows, 300, 5)
+    _check_rows(oracle_mod, _host(A), _host(B), rm.cpu(), ent, val, rows)
+    h.close()
+
+
+def test_C3_galerkin_full(oracle_mod):
+    """T = A*P and Ac = R*T at 128^3: structural nnz(T) = 6,225,920 (cancelled zeros kept),
+    nnz(Ac) = 545,455; the whole product checked against the oracle."""
+    from paper_2103_11991_b200 import SpGEMM
+
+    A, P, R = g.config("C3")
+    Ad, Pd, Rd = (_dev(M.to(device="cuda"), torch.int32) for M in (A, P, R))
+    h1, h2 = SpGEMM(), SpGEMM()
+    T = h1(Ad, Pd)
+    Ac = h2(Rd, T)
+    torch.cuda.synchronize()
+    assert T.nnz == 6225920 and Ac.nnz == 545455
+    got_T = (T.row_map.cpu().numpy().astype(np.int64), T.entries.cpu().numpy(), T.values.cpu().numpy())
+    assert_parity(oracle_mod, A, P, got_T, exact=True)
+    orm, oent, oval, _ = oracle_mod.spgemm(A, P)
+    To = g.CSR(A.nrows, P.ncols, torch.tensor(orm), torch.tensor(oent), torch.tensor(oval))
+    got = (Ac.row_map.cpu().numpy().astype(np.int64), Ac.entries.cpu().numpy(), Ac.values.cpu().numpy())
+    assert_parity(oracle_mod, R, To, got, exact=True)
+    h1.close()
+    h2.close()
