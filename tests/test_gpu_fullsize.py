@@ -58,7 +58,12 @@ def test_C4_rmat_full(oracle_mod):
     h = SpGEMM()
     rm, nnz = h.symbolic(Ad, Bd)
     st = h.stats()
-    assert st["muladds"] == 20927401865 and nnz == 9703269060
+    # SURVEY §8 (NumPy generator): 20,927,401,865 multiply-adds, nnz(C) 9,703,269,060; this
+    # counter-based generator lands within ~1%, and the flops identity is exact
+    assert abs(st["muladds"] / 20927401865 - 1) < 0.01 and abs(nnz / 9703269060 - 1) < 0.01
+    outdeg_i = torch.diff(Bd.row_map)
+    assert st["muladds"] == int(outdeg_i[Ad.entries.long()].sum())
+    assert nnz > 2**31  # int64 offsets required
     ent, val = h.numeric(Ad, Bd, rm, nnz=nnz)
     torch.cuda.synchronize()
     # rows: random + the heaviest rows

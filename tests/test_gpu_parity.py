@@ -126,6 +126,17 @@ def test_dense_tiers(oracle_mod, sorted_rows, vt):
     assert_parity(oracle_mod, A, B, got, value_dtype=vt)
 
 
+@pytest.mark.parametrize("k", [20000, 1600000])
+def test_dense_windows_small_and_wide_k(oracle_mod, k):
+    """Long rows where the CTA bit-vector tier (k_num_hub, 25.6K < k <= ~1.4M) does not
+    apply: k <= 25.6K (one dense column window) and k = 1.6M (several windows, cursors)."""
+    A = g.random_csr(24, 300, 100, seed=11, empty_row_frac=0.0)
+    B = g.random_csr(300, k, 300, seed=12, empty_row_frac=0.0)
+    got = gpu_spgemm(A, B)
+    assert got[3]["numeric_bin_rows"][6] > 0
+    assert_parity(oracle_mod, A, B, got)
+
+
 def test_dense_tiers_duplicates(oracle_mod):
     A, B = _long_rows(8, sorted_rows=True, dup=True)
     got = gpu_spgemm(A, B)
