@@ -180,4 +180,76 @@ inline const char* kname(const char* base, int S) {
     return it->second.c_str();
 }
 
+// ------------------------------------------------------------------------------------
+// warp-owned linear-probing tables with atomic-free claims (numeric strict, symbolic hash)
+// ------------------------------------------------------------------------------------
+// Probe position L in [0,S) (L = bank*R + row, R = S/32) -> slot row*32 + ((bank + 7*row) & 31).
+// A key starts at bank = col & 31, row = hash(col >> 5): consecutive columns of one
+// 32-column word sit in consecutive banks, and the 7*row rotation spreads keys of the
+// same bank (e.g. stencil planes 32k columns apart) over different physical banks.
+template <int S>
+__device__ __forceinline__ uint32_t bm_slot(uint32_t L) {
+    constexpr int R = S / 32, LOGR = ilog2(R);
+    const uint32_t row = L & (R - 1);
+    return row * 32u + (((L >> LOGR) + 7u * row) & 31u);
+}
+
+template <int S>
+__device__ __forceinline__ uint32_t bm_start(uint32_t col) {
+    constexpr int R = S / 32, LOGR = ilog2(R);
+    return (col & 31u) * R + (((col >> 5) * 0x9E3779B1u) >> (32 - LOGR));
+}
+
+// Lane-local probe from position *L: stops at `col` or at an EMPTY slot; returns the key seen.
+template <int S>
+__device__ __forceinline__ uint32_t probe_local(const uint32_t* keys, uint32_t col, uint32_t& L, uint32_t& h) {
+    uint32_t k = keys[h];
+    while (k != col && k != EMPTY) {
+        L = (L + 1) & (S - 1);
+        h = bm_slot<S>(L);
+        k = keys[h];
+    }
+    return k;
+}
+
+// Find or claim `col` for the lanes with act; returns the slot.  Keys of the active
+// lanes may repeat (equal keys walk the same probe sequence and agree on the slot).
+// Lanes probe on their own; lanes that reach an EMPTY slot write their key, the warp
+// syncs, the lanes re-read, and a lane whose write lost probes on (rare).
+template <int S>
+__device__ __forceinline__ uint32_t strict_claim(uint32_t* keys, uint32_t col, bool act) {
+    uint32_t L = bm_start<S>(col);
+    uint32_t h = bm_slot<S>(L);
+    bool need = false;
+    if (act) need = probe_local<S>(keys, col, L, h) == EMPTY;
+    if (need) keys[h] = col;
+    __syncwarp();
+    bool lost = false;
+    if (need) lost = keys[h] != col;
+    while (__any_sync(FULL, lost)) {
+        __syncwarp();
+        bool again = false;
+        if (lost) {
+            L = (L + 1) & (S - 1);
+            h = bm_slot<S>(L);
+            again = probe_local<S>(keys, col, L, h) == EMPTY;
+            if (again) keys[h] = col;
+        }
+        __syncwarp();
+        lost = again && keys[h] != col;
+    }
+    return h;
+}
+
+template <int S>
+__device__ __forceinline__ uint32_t strict_find(const uint32_t* keys, uint32_t col) {
+    uint32_t L = bm_start<S>(col);
+    uint32_t h = bm_slot<S>(L);
+    while (keys[h] != col) {
+        L = (L + 1) & (S - 1);
+        h = bm_slot<S>(L);
+    }
+    return h;
+}
+
 }  // namespace kk

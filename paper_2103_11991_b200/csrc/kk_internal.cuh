@@ -27,8 +27,12 @@ constexpr int NUM_WARP_BINS = 5;
 constexpr int NUM_DENSE_BIN = 6;
 //   7..11: rows with a pattern kept by symbolic (nnz <= 32 << (b - 7)): word-table rank
 //   lookup into a dense per-row value array (no claims, no sort)
+//   12..15: the same for patterns whose words span > 2048 words (hashed word lookup;
+//   nnz <= 64 << (b - 12))
 constexpr int NUM_PAT_BIN0 = 7;
-constexpr int NUM_NBINS = 12;
+constexpr int NUM_PATH_BIN0 = 12;
+constexpr int PAT_DENSE_WORDS = 2048;  // widest word span of a pattern with a dense word index
+constexpr int NUM_NBINS = 16;
 
 // Device-side status block.  Written by the kernels, copied to pinned host memory
 // once at the end of the symbolic phase (the phase's only device->host sync).
@@ -102,8 +106,8 @@ void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out,
                     unsigned long long* total_dst, int* overflow);
 // pat_off (may be null): rows with a stored pattern (and strictly sorted B) go to the
 // pattern bins NUM_PAT_BIN0 + (b - 1)
-void numeric_binid(Launch& L, int64_t m, const int32_t* counts, const long long* pat_off, uint8_t* binid,
-                   const DevStatus* st);
+void numeric_binid(Launch& L, int64_t m, const int32_t* counts, const long long* pat_off, const int* pat_len,
+                   const uint2* pat, uint8_t* binid, const DevStatus* st);
 // stable binning of rows by binid: perm lists rows of bin 0, then bin 1, ...
 // (each bin in increasing row order); bin_start_dst (device int[NB+1]).
 int64_t bin_scratch_len(int64_t m);

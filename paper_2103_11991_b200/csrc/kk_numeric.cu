@@ -225,75 +225,6 @@ __global__ void __launch_bounds__(256) k_num_dense(const OffT* __restrict__ arm,
 // sort of those 32-bit words in registers, coalesced writes, and the table is reset at
 // exactly the slots that were used.
 // ------------------------------------------------------------------------------------
-// Probe position L in [0,S) (L = bank*R + row, R = S/32) -> slot row*32 + ((bank + 7*row) & 31).
-// A key starts at bank = col & 31, row = hash(col >> 5): consecutive columns of one
-// 32-column word sit in consecutive banks, and the 7*row rotation spreads keys of the
-// same bank (e.g. stencil planes 32k columns apart) over different physical banks.
-template <int S>
-__device__ __forceinline__ uint32_t bm_slot(uint32_t L) {
-    constexpr int R = S / 32, LOGR = ilog2(R);
-    const uint32_t row = L & (R - 1);
-    return row * 32u + (((L >> LOGR) + 7u * row) & 31u);
-}
-
-template <int S>
-__device__ __forceinline__ uint32_t bm_start(uint32_t col) {
-    constexpr int R = S / 32, LOGR = ilog2(R);
-    return (col & 31u) * R + (((col >> 5) * 0x9E3779B1u) >> (32 - LOGR));
-}
-
-// Lane-local probe from position *L: stops at `col` or at an EMPTY slot; returns the key seen.
-template <int S>
-__device__ __forceinline__ uint32_t probe_local(const uint32_t* keys, uint32_t col, uint32_t& L, uint32_t& h) {
-    uint32_t k = keys[h];
-    while (k != col && k != EMPTY) {
-        L = (L + 1) & (S - 1);
-        h = bm_slot<S>(L);
-        k = keys[h];
-    }
-    return k;
-}
-
-// Find or claim `col` for the lanes with act; returns the slot.  Keys of the active
-// lanes may repeat (equal keys walk the same probe sequence and agree on the slot).
-// Lanes probe on their own; lanes that reach an EMPTY slot write their key, the warp
-// syncs, the lanes re-read, and a lane whose write lost probes on (rare).
-template <int S>
-__device__ __forceinline__ uint32_t strict_claim(uint32_t* keys, uint32_t col, bool act) {
-    uint32_t L = bm_start<S>(col);
-    uint32_t h = bm_slot<S>(L);
-    bool need = false;
-    if (act) need = probe_local<S>(keys, col, L, h) == EMPTY;
-    if (need) keys[h] = col;
-    __syncwarp();
-    bool lost = false;
-    if (need) lost = keys[h] != col;
-    while (__any_sync(FULL, lost)) {
-        __syncwarp();
-        bool again = false;
-        if (lost) {
-            L = (L + 1) & (S - 1);
-            h = bm_slot<S>(L);
-            again = probe_local<S>(keys, col, L, h) == EMPTY;
-            if (again) keys[h] = col;
-        }
-        __syncwarp();
-        lost = again && keys[h] != col;
-    }
-    return h;
-}
-
-template <int S>
-__device__ __forceinline__ uint32_t strict_find(const uint32_t* keys, uint32_t col) {
-    uint32_t L = bm_start<S>(col);
-    uint32_t h = bm_slot<S>(L);
-    while (keys[h] != col) {
-        L = (L + 1) & (S - 1);
-        h = bm_slot<S>(L);
-    }
-    return h;
-}
-
 // Per A entry of the current 32-entry chunk: its B row (start, length) and a_ij, read back
 // per step with one (O32: element offsets < 2^31) or two 16-byte shared loads.
 template <typename ValT, bool O32>
@@ -360,48 +291,70 @@ __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT 
         const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
         __syncwarp();
         if (maxbl == 0) continue;
-        // steps: (A entry t, 32-entry segment q0 of its B row), in order; loads run three
-        // steps ahead; the product is formed at insert time so no load is waited on early
-        int t = 0, q0 = 0;
-        while (t < na && rec[t].len == 0) ++t;
-        auto fetch = [&](uint32_t& col, ValT& bv, ValT& at) {
-            col = EMPTY;
-            bv = (ValT)0;
-            at = (ValT)0;
-            if (t >= na) return false;
-            const R sr = rec[t];
-            at = (ValT)sr.a;
-            if (q0 + lane < sr.len) {
-                col = (uint32_t)__ldg(bent + (sr.bb + q0 + lane));
-                bv = __ldg(bval + (sr.bb + q0 + lane));
+        // steps in A-entry order; loads run three steps ahead; the product is formed at
+        // insert time so no load is waited on early.  `step` fills one step's (col, b)
+        // and returns false after the last step.
+        auto ring = [&](auto&& step) {
+            uint32_t k0, k1, k2, k3;
+            ValT b0, b1, b2, b3, a0, a1, a2, a3;
+            step(k0, b0, a0);
+            bool h1 = step(k1, b1, a1);
+            bool h2 = step(k2, b2, a2);
+            bool h3 = step(k3, b3, a3);
+            while (true) {
+                insert(k0, a0 * b0);
+                if (!h1) break;
+                const bool h0 = step(k0, b0, a0);
+                insert(k1, a1 * b1);
+                if (!h2) break;
+                h1 = step(k1, b1, a1);
+                insert(k2, a2 * b2);
+                if (!h3) break;
+                h2 = step(k2, b2, a2);
+                insert(k3, a3 * b3);
+                if (!h0) break;
+                h3 = step(k3, b3, a3);
             }
-            q0 += 32;
-            if (q0 >= sr.len) {
-                q0 = 0;
-                ++t;
-                while (t < na && rec[t].len == 0) ++t;
-            }
-            return true;
         };
-        uint32_t k0, k1, k2, k3;
-        ValT b0, b1, b2, b3, a0, a1, a2, a3;
-        fetch(k0, b0, a0);
-        bool h1 = fetch(k1, b1, a1);
-        bool h2 = fetch(k2, b2, a2);
-        bool h3 = fetch(k3, b3, a3);
-        while (true) {
-            insert(k0, a0 * b0);
-            if (!h1) break;
-            const bool h0 = fetch(k0, b0, a0);
-            insert(k1, a1 * b1);
-            if (!h2) break;
-            h1 = fetch(k1, b1, a1);
-            insert(k2, a2 * b2);
-            if (!h3) break;
-            h2 = fetch(k2, b2, a2);
-            insert(k3, a3 * b3);
-            if (!h0) break;
-            h3 = fetch(k3, b3, a3);
+        int t = 0;
+        if (maxbl <= 32) {
+            // one step per A entry (empty B rows give idle steps)
+            ring([&](uint32_t& col, ValT& bv, ValT& at) {
+                col = EMPTY;
+                bv = (ValT)0;
+                at = (ValT)0;
+                if (t >= na) return false;
+                const R sr = rec[t++];
+                at = (ValT)sr.a;
+                if (lane < sr.len) {
+                    col = (uint32_t)__ldg(bent + (sr.bb + lane));
+                    bv = __ldg(bval + (sr.bb + lane));
+                }
+                return true;
+            });
+        } else {
+            // long B rows: steps are (A entry t, 32-entry segment q0 of its B row)
+            int q0 = 0;
+            while (t < na && rec[t].len == 0) ++t;
+            ring([&](uint32_t& col, ValT& bv, ValT& at) {
+                col = EMPTY;
+                bv = (ValT)0;
+                at = (ValT)0;
+                if (t >= na) return false;
+                const R sr = rec[t];
+                at = (ValT)sr.a;
+                if (q0 + lane < sr.len) {
+                    col = (uint32_t)__ldg(bent + (sr.bb + q0 + lane));
+                    bv = __ldg(bval + (sr.bb + q0 + lane));
+                }
+                q0 += 32;
+                if (q0 >= sr.len) {
+                    q0 = 0;
+                    ++t;
+                    while (t < na && rec[t].len == 0) ++t;
+                }
+                return true;
+            });
         }
         __syncwarp();
     }
@@ -646,37 +599,67 @@ __global__ void __launch_bounds__(256, 1) k_num_strict(const OffT* __restrict__ 
 constexpr int PAT_W = 64;       // max words of a kept pattern (symbolic PAT_WORDS)
 constexpr int PAT_NWIN = 2048;  // words of the widest symbolic window (64K bits)
 
+constexpr int PAT_SW = 128;  // word-table slots (patterns whose words span > PAT_NWIN)
+
 template <typename ValT, int CAP>
 struct PatLayout {
     static constexpr size_t vals = 0;
     static constexpr size_t rec = ((size_t)CAP * sizeof(ValT) + 15) / 16 * 16;
     static constexpr size_t winfo = rec + REC_BYTES;
-    static constexpr size_t widx = winfo + (size_t)PAT_W * 8;
+    static constexpr size_t wkeys = winfo + (size_t)PAT_SW * 8;
+    static constexpr size_t widx = wkeys + (size_t)PAT_SW * 4;
     static constexpr size_t bytes = (widx + (size_t)PAT_NWIN + 15) / 16 * 16;
 };
 
-template <typename OffT, typename ValT, int CAP, bool O32>
-__global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+// word table of a pattern whose words are spread out: multiplicative hash, linear probing
+__device__ __forceinline__ uint32_t wt_slot(uint32_t w) { return (w * 0x9E3779B1u) >> (32 - ilog2(PAT_SW)); }
+
+// insert distinct words (write-then-verify claims); returns the slot
+__device__ __forceinline__ uint32_t wt_insert(uint32_t* keys, uint32_t w, bool act) {
+    uint32_t h = wt_slot(w);
+    bool need = false;
+    if (act) {
+        while (keys[h] != EMPTY) h = (h + 1) & (PAT_SW - 1);
+        need = true;
+    }
+    while (__any_sync(FULL, need)) {
+        if (need) keys[h] = w;
+        __syncwarp();
+        if (need) {
+            if (keys[h] == w) {
+                need = false;
+            } else {
+                while (keys[h] != EMPTY) h = (h + 1) & (PAT_SW - 1);
+            }
+        }
+        __syncwarp();
+    }
+    return h;
+}
+
+template <typename OffT, typename ValT, int CAP, bool O32, int MINB, bool DENSE>
+__global__ void __launch_bounds__(256, MINB) k_num_pattern(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                      const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                                      const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
                                                      const OffT* __restrict__ crm, int32_t* __restrict__ cent,
                                                      ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                      const int* __restrict__ bin_start, int bin,
                                                      const uint2* __restrict__ pat, const long long* __restrict__ pat_off,
-                                                     const int* __restrict__ pat_len, const int32_t* __restrict__ wlo) {
+                                                     const int* __restrict__ pat_len) {
     using LY = PatLayout<ValT, CAP>;
     extern __shared__ __align__(16) unsigned char sm_pat[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     unsigned char* base = sm_pat + (size_t)warp * LY::bytes;
     ValT* vals = (ValT*)(base + LY::vals);
     void* rec = base + LY::rec;
-    uint2* winfo = (uint2*)(base + LY::winfo);
-    uint8_t* widx = (uint8_t*)(base + LY::widx);
+    uint32_t* wkeys = (uint32_t*)(base + LY::wkeys);
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     const int stride = gridDim.x * warps;
     int r = r0 + blockIdx.x * warps + warp;
     if (r >= r1) return;
     for (int t = lane; t < CAP; t += 32) vals[t] = (ValT)0;
+    if (!DENSE)
+        for (int t = lane; t < PAT_SW; t += 32) wkeys[t] = EMPTY;
     __syncwarp();
     int i = perm[r];
     int64_t s = ld(arm, i), e = ld(arm, i + 1);
@@ -691,7 +674,6 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         const int clen = (int)(ld(crm, i + 1) - cb);
         const long long po = pat_off[i];
         const int pl = pat_len[i];
-        const uint32_t wb = (uint32_t)__ldg(wlo + i) >> 5;
         const int rn = r + stride;
         const int inext = rn < r1 ? perm[rn] : -1;
         // ---- the row's pattern: word table + entries ----
@@ -709,14 +691,28 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         }
         const int tot0 = __shfl_sync(FULL, x0, 31);
         const uint32_t pre0 = (uint32_t)(x0 - c0), pre1 = (uint32_t)(tot0 + x1 - c1);
-        // dense word index over the row's window (entries of other rows are never read)
-        if (lane < pl) {
-            widx[p0.x - wb] = (uint8_t)lane;
-            winfo[lane] = make_uint2(p0.y, pre0);
-        }
-        if (lane + 32 < pl) {
-            widx[p1.x - wb] = (uint8_t)(lane + 32);
-            winfo[lane + 32] = make_uint2(p1.y, pre1);
+        // word lookup: a dense index over the pattern's word span when it is narrow
+        // (entries of other rows are never read), else a small hash table
+        const uint32_t wb = __shfl_sync(FULL, p0.x, 0);
+        const uint32_t wl_ = pl > 32 ? __shfl_sync(FULL, p1.x, (pl - 33) & 31) : __shfl_sync(FULL, p0.x, (pl - 1) & 31);
+        (void)wl_;
+        constexpr bool dense = DENSE;  // binning put the row here by its word span
+        const uint32_t o_sw = (uint32_t)warp * (uint32_t)LY::bytes;
+        uint32_t h0 = 0, h1 = 0;
+        if constexpr (DENSE) {
+            if (lane < pl) {
+                sm_pat[o_sw + LY::widx + (p0.x - wb)] = (uint8_t)lane;
+                *(uint2*)(sm_pat + o_sw + LY::winfo + lane * 8u) = make_uint2(p0.y, pre0);
+            }
+            if (lane + 32 < pl) {
+                sm_pat[o_sw + LY::widx + (p1.x - wb)] = (uint8_t)(lane + 32);
+                *(uint2*)(sm_pat + o_sw + LY::winfo + (lane + 32) * 8u) = make_uint2(p1.y, pre1);
+            }
+        } else {
+            h0 = wt_insert(wkeys, p0.x, lane < pl);
+            h1 = wt_insert(wkeys, p1.x, lane + 32 < pl);
+            if (lane < pl) *(uint2*)(sm_pat + o_sw + LY::winfo + h0 * 8u) = make_uint2(p0.y, pre0);
+            if (lane + 32 < pl) *(uint2*)(sm_pat + o_sw + LY::winfo + h1 * 8u) = make_uint2(p1.y, pre1);
         }
         {
             uint32_t m = p0.y;
@@ -739,22 +735,34 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         __syncwarp();
         // ---- products: rank lookup + dense accumulate ----
         // (shared accesses go through sm_pat with 32-bit offsets: no generic addressing)
-        const uint32_t o_idx = (uint32_t)warp * (uint32_t)LY::bytes + (uint32_t)LY::widx - wb;
-        const uint32_t o_inf = (uint32_t)warp * (uint32_t)LY::bytes + (uint32_t)LY::winfo;
-        const uint32_t o_val = (uint32_t)warp * (uint32_t)LY::bytes + (uint32_t)LY::vals;
-        auto rank = [&](uint32_t col) {
-            const uint32_t wi = sm_pat[o_idx + (col >> 5)];
+        const uint32_t o_idx = o_sw + (uint32_t)LY::widx - wb;
+        const uint32_t o_inf = o_sw + (uint32_t)LY::winfo;
+        const uint32_t o_val = o_sw + (uint32_t)LY::vals;
+        auto mp_rank = [&](uint32_t wi, uint32_t col) {
             const uint2 mp = *(const uint2*)(sm_pat + o_inf + wi * 8u);
             return mp.y + __popc(mp.x & ((1u << (col & 31)) - 1u));
         };
-        row_products<OffT, ValT, O32>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
-                                      [&](uint32_t col, ValT prod) {
-                                          if (col != EMPTY) {
-                                              const uint32_t rk = rank(col);
-                                              if (rk < (uint32_t)CAP) *(ValT*)(sm_pat + o_val + rk * sizeof(ValT)) += prod;
-                                          }
-                                          __syncwarp();
-                                      });
+        auto acc = [&](uint32_t rk, ValT prod) {
+            if (rk < (uint32_t)CAP) *(ValT*)(sm_pat + o_val + rk * sizeof(ValT)) += prod;
+        };
+        if constexpr (DENSE) {
+            row_products<OffT, ValT, O32>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
+                                          [&](uint32_t col, ValT prod) {
+                                              if (col != EMPTY) acc(mp_rank(sm_pat[o_idx + (col >> 5)], col), prod);
+                                              __syncwarp();
+                                          });
+        } else {
+            row_products<OffT, ValT, O32>(s, e, jn, an, aent, aval, brm, bent, bval, rec,
+                                          [&](uint32_t col, ValT prod) {
+                                              if (col != EMPTY) {
+                                                  const uint32_t w = col >> 5;
+                                                  uint32_t wi = wt_slot(w);
+                                                  while (wkeys[wi] != w) wi = (wi + 1) & (PAT_SW - 1);
+                                                  acc(mp_rank(wi, col), prod);
+                                              }
+                                              __syncwarp();
+                                          });
+        }
         int64_t sn = 0, en = 0;
         if (inext >= 0) {
             sn = ld(arm, inext);
@@ -766,6 +774,10 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
         for (int t = lane; t < nn; t += 32) {
             cval[cb + t] = vals[t];
             vals[t] = (ValT)0;
+        }
+        if constexpr (!DENSE) {
+            if (lane < pl) wkeys[h0] = EMPTY;
+            if (lane + 32 < pl) wkeys[h1] = EMPTY;
         }
         if (inext >= 0 && lane < en - sn) {
             jn = __ldg(aent + sn + lane);
@@ -780,21 +792,31 @@ __global__ void __launch_bounds__(256) k_num_pattern(const OffT* __restrict__ ar
     }
 }
 
-template <typename OffT, typename ValT, int CAP>
+template <typename OffT, typename ValT, int CAP, bool DENSE>
 static void launch_num_pattern(Launch& L, const NumArgs& a, int bin) {
     const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
     if (rows <= 0) return;
     const int warps = 8;
     const size_t smem = (size_t)warps * PatLayout<ValT, CAP>::bytes;
-    auto kern = a.B.nnz < INT32_MAX ? k_num_pattern<OffT, ValT, CAP, true> : k_num_pattern<OffT, ValT, CAP, false>;
+    // resident CTAs per SM the register budget targets: 4 (60 registers, no spills) measured
+    // fastest on C2; KK_PAT_MINB=5|6 for experiments
+    static const int minb = [] {
+        const char* v = getenv("KK_PAT_MINB");
+        const int x = v ? atoi(v) : 4;
+        return (x == 5 || x == 6) ? x : 4;
+    }();
+    auto kern = a.B.nnz >= INT32_MAX ? k_num_pattern<OffT, ValT, CAP, false, 4, DENSE>
+              : minb == 5            ? k_num_pattern<OffT, ValT, CAP, true, 5, DENSE>
+              : minb == 6            ? k_num_pattern<OffT, ValT, CAP, true, 6, DENSE>
+                                     : k_num_pattern<OffT, ValT, CAP, true, 4, DENSE>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (rows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
-    L.begin(kname("num_pattern", CAP), L.stream);
+    L.begin(kname(DENSE ? "num_pattern" : "num_pattern_hash", CAP), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                                (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
-                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len, a.wlo);
+                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len);
     L.end(L.stream);
 }
 
@@ -998,13 +1020,17 @@ static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_strea
         L.end(s);
     }
     if (a.pat) {
-        launch_num_pattern<OffT, ValT, 512>(L, a, NUM_PAT_BIN0 + 4);
-        launch_num_pattern<OffT, ValT, 256>(L, a, NUM_PAT_BIN0 + 3);
-        launch_num_pattern<OffT, ValT, 128>(L, a, NUM_PAT_BIN0 + 2);
-        launch_num_pattern<OffT, ValT, 64>(L, a, NUM_PAT_BIN0 + 1);
-        launch_num_pattern<OffT, ValT, 32>(L, a, NUM_PAT_BIN0);
+        launch_num_pattern<OffT, ValT, 512, true>(L, a, NUM_PAT_BIN0 + 4);
+        launch_num_pattern<OffT, ValT, 256, true>(L, a, NUM_PAT_BIN0 + 3);
+        launch_num_pattern<OffT, ValT, 128, true>(L, a, NUM_PAT_BIN0 + 2);
+        launch_num_pattern<OffT, ValT, 64, true>(L, a, NUM_PAT_BIN0 + 1);
+        launch_num_pattern<OffT, ValT, 32, true>(L, a, NUM_PAT_BIN0);
+        launch_num_pattern<OffT, ValT, 512, false>(L, a, NUM_PATH_BIN0 + 3);
+        launch_num_pattern<OffT, ValT, 256, false>(L, a, NUM_PATH_BIN0 + 2);
+        launch_num_pattern<OffT, ValT, 128, false>(L, a, NUM_PATH_BIN0 + 1);
+        launch_num_pattern<OffT, ValT, 64, false>(L, a, NUM_PATH_BIN0);
     }
-    if (a.strict && a.logG == 5) {
+    if (a.strict && a.logG >= 4) {
         launch_num_strict<OffT, ValT, 512, SORT>(L, a, 5);
         launch_num_strict<OffT, ValT, 256, SORT>(L, a, 4);
         launch_num_strict<OffT, ValT, 128, SORT>(L, a, 3);

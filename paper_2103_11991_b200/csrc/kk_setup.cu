@@ -499,21 +499,29 @@ __device__ __forceinline__ int num_bin_of(int64_t nnz) {
 
 __global__ void __launch_bounds__(256) k_numeric_binid(int64_t m, const int32_t* __restrict__ counts,
                                                        const long long* __restrict__ pat_off,
+                                                       const int* __restrict__ pat_len, const uint2* __restrict__ pat,
                                                        uint8_t* __restrict__ binid, const DevStatus* st) {
-    const bool pat = pat_off != nullptr && st->b_strict != 0;
+    const bool use_pat = pat_off != nullptr && st->b_strict != 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         int b = num_bin_of(counts[i]);
-        if (pat && b >= 1 && b <= NUM_WARP_BINS && pat_off[i] >= 0) b = NUM_PAT_BIN0 + b - 1;
+        if (use_pat && b >= 1 && b <= NUM_WARP_BINS) {
+            const long long o = pat_off[i];
+            if (o >= 0) {
+                const int l = pat_len[i];
+                const uint32_t span = l > 0 ? pat[o + l - 1].x - pat[o].x : 0u;
+                b = span < (uint32_t)PAT_DENSE_WORDS ? NUM_PAT_BIN0 + b - 1 : NUM_PATH_BIN0 + max(b, 2) - 2;
+            }
+        }
         binid[i] = (uint8_t)b;
     }
 }
 
-void numeric_binid(Launch& L, int64_t m, const int32_t* counts, const long long* pat_off, uint8_t* binid,
-                   const DevStatus* st) {
+void numeric_binid(Launch& L, int64_t m, const int32_t* counts, const long long* pat_off, const int* pat_len,
+                   const uint2* pat, uint8_t* binid, const DevStatus* st) {
     if (m == 0) return;
     int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)L.num_sms * 16);
     L.begin("numeric_binid", L.stream);
-    k_numeric_binid<<<grid, 256, 0, L.stream>>>(m, counts, pat_off, binid, st);
+    k_numeric_binid<<<grid, 256, 0, L.stream>>>(m, counts, pat_off, pat_len, pat, binid, st);
     L.end(L.stream);
 }
 

@@ -432,6 +432,266 @@ __device__ __forceinline__ void sym_window_rows(const OffT* __restrict__ arm, co
     }
 }
 
+// a5 on a warp-owned hash table of B_C words (keys[S] | masks[S]) -- the structure of
+// sym_window_rows (flattened pairs, match-merged duplicate words, touched-word list,
+// kept patterns) for rows whose columns do not fit a bit-vector window.  Leaders claim
+// new words with write-then-verify (strict_claim); the list holds slots.
+template <typename OffT, int S, bool COMP, bool O32>
+__device__ __forceinline__ void sym_hash_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                                const int32_t* __restrict__ bc_len, const uint2* __restrict__ pairs,
+                                                const int32_t* __restrict__ perm, int r0, int r1,
+                                                int32_t* __restrict__ counts,
+                                                uint32_t* keys, uint32_t* masks, void* rec_raw, uint32_t* wl,
+                                                const PatOut& po, DevStatus* st) {
+    using SR = SymRec<O32>;
+    SR* rec = (SR*)rec_raw;
+    // flattened pair offsets of a chunk (FLAT_CAP entries of SR::bb), per-lane scratch
+    decltype(SR::bb)* flat = (decltype(SR::bb)*)((uint32_t*)rec_raw + 128);
+    uint32_t* scratch = (uint32_t*)rec_raw + 128 + FLAT_WORDS;
+    constexpr int LOGS = ilog2(S);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    const int stride = gridDim.x * warps;
+    int r = r0 + blockIdx.x * warps + warp;
+    // software pipeline over rows: the next row's bounds and first 32 A entries are
+    // loaded while the current row finishes
+    int i = perm[r];
+    int64_t s = ld(arm, i), e = ld(arm, i + 1);
+    int jn = lane < e - s ? __ldg(aent + s + lane) : 0;
+    while (true) {
+        const int rn = r + stride;
+        const int inext = rn < r1 ? perm[rn] : -1;
+        int cnt = 0;
+        int nt = 0;  // words touched (warp-uniform)
+        auto step_or = [&](uint32_t w, uint32_t m) {
+            // one B row segment: words distinct (COMP); raw columns may repeat a word, so
+            // they are merged first exactly like the flattened path
+            const uint32_t key = m ? w : (0x80000000u | (uint32_t)lane);
+            const unsigned grp = COMP ? (1u << lane) : __match_any_sync(FULL, key);
+            scratch[lane] = m;
+            __syncwarp();
+            uint32_t mm = m;
+            const bool lead = m && lane == __ffs(grp) - 1;
+            if (lead) {
+                unsigned peers = grp & (grp - 1);
+                while (peers) {
+                    mm |= scratch[__ffs(peers) - 1];
+                    peers &= peers - 1;
+                }
+            }
+            const uint32_t hs = strict_claim<S>(keys, w, lead);
+            bool fresh = false;
+            if (lead) {
+                const uint32_t old = masks[hs];
+                masks[hs] = old | mm;
+                cnt += __popc(mm & ~old);
+                fresh = old == 0;
+            }
+            const unsigned fb = __ballot_sync(FULL, fresh);
+            if (fresh) {
+                const int pos = nt + __popc(fb & lanemask_lt());
+                if (pos < PAT_WORDS) wl[pos] = hs;
+            }
+            nt += __popc(fb);
+        };
+        for (int64_t c0 = s; c0 < e; c0 += 32) {
+            const int na = (int)min((int64_t)32, e - c0);
+            int j = jn;
+            if (c0 != s && lane < na) j = __ldg(aent + c0 + lane);
+            int bl = 0;
+            __syncwarp();
+            if (lane < na) {
+                const int64_t bb = ld(brm, j);
+                bl = COMP ? __ldg(bc_len + j) : (int)(ld(brm, j + 1) - bb);
+                SR sr;
+                sr.bb = (decltype(sr.bb))bb;
+                sr.len = bl;
+                rec[lane] = sr;
+            }
+            const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
+            __syncwarp();
+            if (maxbl == 0) continue;
+            auto load = [&](const SR& sr, int q, uint32_t& w, uint32_t& m) {
+                if (COMP) {
+                    const uint2 pr = __ldg(pairs + (sr.bb + q));
+                    w = pr.x;
+                    m = pr.y;
+                } else {
+                    const int c = __ldg(bent + (sr.bb + q));
+                    w = (uint32_t)c >> 5;
+                    m = 1u << (c & 31);
+                }
+            };
+            // pairs of the chunk's B_C rows, flattened: 32 consecutive pairs per step
+            int incl = bl;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, d);
+                if (lane >= d) incl += y;
+            }
+            const int U = __shfl_sync(FULL, incl, 31);
+            constexpr int FLAT_CAP = FLAT_WORDS * 4 / (int)sizeof(SR::bb);  // else one B row per step
+            if (U <= FLAT_CAP) {
+                if (lane < na) {
+                    const SR sr = rec[lane];
+                    for (int q = 0, ex = incl - bl; q < bl; ++q) flat[ex + q] = sr.bb + q;
+                }
+                __syncwarp();
+                int u0 = 0;
+                auto fetch = [&](uint32_t& w, uint32_t& m) {
+                    w = 0;
+                    m = 0;
+                    if (u0 >= U) return false;
+                    const int p = u0 + lane;
+                    u0 += 32;
+                    if (p < U) {
+                        SR one;
+                        one.bb = flat[p];
+                        load(one, 0, w, m);
+                    }
+                    return true;
+                };
+                // equal words in a step are merged (match + OR over the group); the group
+                // leader updates the bit vector, so all updates of a step are distinct words
+                auto step_merge = [&](uint32_t w, uint32_t m) {
+                    const uint32_t key = m ? w : (0x80000000u | (uint32_t)lane);
+                    const unsigned grp = __match_any_sync(FULL, key);
+                    scratch[lane] = m;
+                    __syncwarp();
+                    uint32_t mm = m;
+                    const bool lead = m && lane == __ffs(grp) - 1;
+                    if (lead) {
+                        unsigned peers = grp & (grp - 1);
+                        while (peers) {
+                            mm |= scratch[__ffs(peers) - 1];
+                            peers &= peers - 1;
+                        }
+                    }
+                    const uint32_t hs = strict_claim<S>(keys, w, lead);
+                    bool fresh = false;
+                    if (lead) {
+                        const uint32_t old = masks[hs];
+                        masks[hs] = old | mm;
+                        cnt += __popc(mm & ~old);
+                        fresh = old == 0;
+                    }
+                    const unsigned fb = __ballot_sync(FULL, fresh);
+                    if (fresh) {
+                        const int pos = nt + __popc(fb & lanemask_lt());
+                        if (pos < PAT_WORDS) wl[pos] = hs;
+                    }
+                    nt += __popc(fb);
+                };
+                uint32_t w0, w1, w2, w3, m0, m1, m2, m3;
+                fetch(w0, m0);
+                bool h1 = fetch(w1, m1);
+                bool h2 = fetch(w2, m2);
+                bool h3 = fetch(w3, m3);
+                while (true) {
+                    step_merge(w0, m0);
+                    if (!h1) break;
+                    __syncwarp();
+                    const bool h0 = fetch(w0, m0);
+                    step_merge(w1, m1);
+                    if (!h2) break;
+                    __syncwarp();
+                    h1 = fetch(w1, m1);
+                    step_merge(w2, m2);
+                    if (!h3) break;
+                    __syncwarp();
+                    h2 = fetch(w2, m2);
+                    step_merge(w3, m3);
+                    if (!h0) break;
+                    __syncwarp();
+                    h3 = fetch(w3, m3);
+                }
+            } else {
+                for (int t = 0; t < na; ++t) {
+                    const SR sr = rec[t];
+                    for (int q0 = 0; q0 < sr.len; q0 += 32) {
+                        uint32_t w = 0, m = 0;
+                        if (q0 + lane < sr.len) load(sr, q0 + lane, w, m);
+                        step_or(w, m);
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        int64_t sn = 0, en = 0;
+        if (inext >= 0) {
+            sn = ld(arm, inext);
+            en = ld(arm, inext + 1);
+        }
+        cnt = warp_sum(cnt);
+        if (lane == 0) counts[i] = cnt;
+        __syncwarp();
+        if (nt <= PAT_WORDS) {
+            // sort the touched words as (word - min) << log2 S | slot, keep the pattern,
+            // clear the slots
+            constexpr int E = PAT_WORDS / 32;
+            uint32_t hsl[E], wd[E];
+            uint32_t mn = 0xffffffffu, mx = 0u;
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int idx = lane * E + q;
+                hsl[q] = idx < nt ? wl[idx] : 0u;
+                wd[q] = idx < nt ? keys[hsl[q]] : 0u;
+                if (idx < nt) {
+                    mn = min(mn, wd[q]);
+                    mx = max(mx, wd[q]);
+                }
+            }
+            mn = __reduce_min_sync(FULL, mn);
+            mx = __reduce_max_sync(FULL, mx);
+            const bool packed = nt == 0 || (mx - mn) < ((1u << (32 - LOGS)) - 1u);
+            uint32_t v[E];
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int idx = lane * E + q;
+                v[q] = idx < nt ? (((wd[q] - mn) << LOGS) | hsl[q]) : 0xffffffffu;
+            }
+            if (packed) warp_bitonic_sort<E>(v);
+            long long off = -1;
+            if (po.pat && packed) {
+                if (lane == 0) {
+                    const unsigned long long o = atomicAdd(&st->pat_used, (unsigned long long)nt);
+                    off = (o + (unsigned long long)nt <= (unsigned long long)po.cap) ? (long long)o : -1;
+                }
+                off = __shfl_sync(FULL, off, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int idx = lane * E + q;
+                if (idx < nt) {
+                    const uint32_t hs = v[q] & (S - 1);
+                    const uint32_t m = masks[hs];
+                    const uint32_t w = keys[hs];
+                    keys[hs] = EMPTY;
+                    masks[hs] = 0;
+                    if (off >= 0) po.pat[off + idx] = make_uint2(w, m);
+                }
+            }
+            if (po.pat && lane == 0) {
+                po.off[i] = off;
+                po.len[i] = nt;
+            }
+        } else {
+            for (int t = lane; t < S; t += 32) {
+                keys[t] = EMPTY;
+                masks[t] = 0;
+            }
+        }
+        if (inext >= 0) jn = lane < en - sn ? __ldg(aent + sn + lane) : 0;
+        __syncwarp();
+        if (inext < 0) break;
+        r = rn;
+        i = inext;
+        s = sn;
+        e = en;
+    }
+}
+
 template <typename OffT, int W>
 __global__ void __launch_bounds__(256, 1) k_sym_window(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                     const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
@@ -484,6 +744,61 @@ static void launch_sym_window(Launch& L, const SymArgs& a, int bin) {
     L.end(L.stream);
 }
 
+template <typename OffT, int S>
+__global__ void __launch_bounds__(256, 1) k_sym_hash(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                     const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                                     const int32_t* __restrict__ bc_len, const uint2* __restrict__ pairs,
+                                                     const int32_t* __restrict__ perm, const int* __restrict__ bin_start,
+                                                     int bin, int32_t* __restrict__ counts, PatOut po, DevStatus* st,
+                                                     long long nnzB) {
+    constexpr int WB = 2 * S + 672 + PAT_WORDS;  // words per warp: keys | masks | recs | flat | scratch | list
+    extern __shared__ __align__(16) uint32_t sm_hs[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    uint32_t* keys = sm_hs + (size_t)warp * WB;
+    uint32_t* masks = keys + S;
+    void* rec = (void*)(masks + S);
+    uint32_t* wl = masks + S + 672;
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    if (r0 + blockIdx.x * warps + warp >= r1) return;
+    for (int t = lane; t < S; t += 32) {
+        keys[t] = EMPTY;
+        masks[t] = 0;
+    }
+    __syncwarp();
+    const bool o32 = nnzB < INT32_MAX;
+    if (st->use_comp) {
+        if (o32)
+            sym_hash_rows<OffT, S, true, true>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, counts, keys, masks,
+                                               rec, wl, po, st);
+        else
+            sym_hash_rows<OffT, S, true, false>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, counts, keys, masks,
+                                                rec, wl, po, st);
+    } else {
+        if (o32)
+            sym_hash_rows<OffT, S, false, true>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, counts, keys, masks,
+                                                rec, wl, po, st);
+        else
+            sym_hash_rows<OffT, S, false, false>(arm, aent, brm, bent, bc_len, pairs, perm, r0, r1, counts, keys,
+                                                 masks, rec, wl, po, st);
+    }
+}
+
+// hash bins: rows with ub <= cap = 64 << (bin - 1) words; table S = 2 * cap
+template <typename OffT, int S>
+static void launch_sym_hash(Launch& L, const SymArgs& a, int bin) {
+    const int warps = S <= 1024 ? 8 : (S <= 4096 ? 4 : 2);
+    const size_t smem = (size_t)warps * (2 * S + 672 + PAT_WORDS) * 4;
+    auto kern = k_sym_hash<OffT, S>;
+    KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    int64_t need = (a.A.nrows + warps - 1) / warps;
+    int grid = (int)std::min<int64_t>(need, c.grid_cap);
+    L.begin(kname("sym_hash", S), L.stream);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+                                               a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.counts,
+                                               a.pat, (DevStatus*)a.st, (long long)a.B.nnz);
+    L.end(L.stream);
+}
+
 template <typename OffT>
 static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stream) {
     // dense rows first (heaviest), on their own stream when given
@@ -507,13 +822,25 @@ static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stre
     launch_sym_window<OffT, 32768>(L, a, SYM_WIN_BIN0 + 2);
     launch_sym_window<OffT, 16384>(L, a, SYM_WIN_BIN0 + 1);
     launch_sym_window<OffT, 8192>(L, a, SYM_WIN_BIN0);
-    launch_sym_warp<OffT, 4096>(L, a, 7);
-    launch_sym_warp<OffT, 2048>(L, a, 6);
-    launch_sym_warp<OffT, 1024>(L, a, 5);
-    launch_sym_warp<OffT, 512>(L, a, 4);
-    launch_sym_warp<OffT, 256>(L, a, 3);
-    launch_sym_warp<OffT, 128>(L, a, 2);
-    launch_sym_warp<OffT, 64>(L, a, 1);
+    if (a.logG >= 3) {
+        // B rows of >= ~5 words on average: flattened-pair hash kernels (keep patterns)
+        launch_sym_hash<OffT, 8192>(L, a, 7);
+        launch_sym_hash<OffT, 4096>(L, a, 6);
+        launch_sym_hash<OffT, 2048>(L, a, 5);
+        launch_sym_hash<OffT, 1024>(L, a, 4);
+        launch_sym_hash<OffT, 512>(L, a, 3);
+        launch_sym_hash<OffT, 256>(L, a, 2);
+        launch_sym_hash<OffT, 128>(L, a, 1);
+    } else {
+        // very short B rows (e.g. a prolongator): sub-warp groups, several B rows per step
+        launch_sym_warp<OffT, 4096>(L, a, 7);
+        launch_sym_warp<OffT, 2048>(L, a, 6);
+        launch_sym_warp<OffT, 1024>(L, a, 5);
+        launch_sym_warp<OffT, 512>(L, a, 4);
+        launch_sym_warp<OffT, 256>(L, a, 3);
+        launch_sym_warp<OffT, 128>(L, a, 2);
+        launch_sym_warp<OffT, 64>(L, a, 1);
+    }
 }
 
 void symbolic_bins(Launch& L, const SymArgs& a, cudaStream_t dense_stream) {
