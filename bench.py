@@ -64,6 +64,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU oracle time budget (cpu_baseline)")
     ap.add_argument("--cpu-rows", type=int, default=None, help="rows of A in the oracle sample")
     ap.add_argument("--kernel-table", action="store_true", help="print the per-kernel timing table to stderr")
+    ap.add_argument("--streams", type=int, default=2, help="library internal streams (1 = serialise the bins)")
     return ap.parse_args()
 
 
@@ -352,7 +353,7 @@ def run_ours(args):
 
         def __init__(self, X, Y):
             self.X, self.Y = X, Y
-            self.h = SpGEMM(device=dev, timing=True)
+            self.h = SpGEMM(device=dev, timing=True, num_streams=args.streams)
             self.crm = torch.empty(X.nrows + 1, dtype=odt, device=dev)
             _, n = self.h.symbolic(X, Y, c_row_map=self.crm)
             self.cent = torch.empty(max(n, 1), dtype=torch.int32, device=dev)

@@ -875,10 +875,14 @@ constexpr int HUB_THREADS = 512;
 constexpr int HUB_WARPS = HUB_THREADS / 32;
 
 __host__ __device__ constexpr int64_t hub_words(int64_t k) { return ((k + 127) / 128) * 4; }  // multiple of 4
-// shared layout: bm[NW] | gp[NW/4] (padded to 8 bytes) | wtot[HUB_WARPS] (int64)
+constexpr int HUB_LONG = 256;     // B rows longer than this are walked by the whole CTA
+constexpr int HUB_LIST = 1024;    // capacity of the per-row list of such A entries
+
+// shared layout: bm[NW] | gp[NW/4] (padded to 8 bytes) | wtot[HUB_WARPS] (int64) |
+//                list[HUB_LIST] (int32) | nlist
 __host__ __device__ constexpr int64_t hub_gp_words(int64_t k) { return (hub_words(k) / 4 + 1) & ~1ll; }
 __host__ __device__ constexpr size_t hub_smem(int64_t k) {
-    return (size_t)(hub_words(k) + hub_gp_words(k)) * 4 + (size_t)HUB_WARPS * 8;
+    return (size_t)(hub_words(k) + hub_gp_words(k)) * 4 + (size_t)HUB_WARPS * 8 + (size_t)HUB_LIST * 4 + 16;
 }
 
 template <typename OffT, typename ValT>
@@ -893,6 +897,8 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
     uint32_t* bm = sm_hub;
     uint32_t* gp = bm + NW;
     long long* wtot = (long long*)(gp + hub_gp_words(k));
+    int* list = (int*)(wtot + HUB_WARPS);
+    int* nlist = list + HUB_LIST;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     if (r0 + (int)blockIdx.x >= r1) return;
@@ -903,12 +909,34 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
         const int64_t cb = ld(crm, i);
         const int64_t clen = ld(crm, i + 1) - cb;
         for (int64_t t = threadIdx.x; t < NW / 4; t += HUB_THREADS) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
+        if (threadIdx.x == 0) *nlist = 0;
         __syncthreads();
-        // (1) pattern
+        // (1) pattern.  Warps take the A entries whose B rows are short; longer B rows are
+        // listed and then walked by the whole CTA, one at a time (a hub B row must not
+        // leave one warp working while the others wait at the barrier).
         for (int64_t p = s + warp; p < e; p += HUB_WARPS) {
             const int j = __ldg(aent + p);
             const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+            if (be - bs > HUB_LONG) {
+                int slot = 0;
+                if (lane == 0) slot = atomicAdd(nlist, 1);
+                slot = __shfl_sync(FULL, slot, 0);
+                if (slot < HUB_LIST) {
+                    if (lane == 0) list[slot] = (int)(p - s);
+                    continue;
+                }
+            }
             for (int64_t q = bs + lane; q < be; q += 32) {
+                const int c = __ldg(bent + q);
+                atomicOr(&bm[c >> 5], 1u << (c & 31));
+            }
+        }
+        __syncthreads();
+        const int nl = min(*nlist, HUB_LIST);
+        for (int l = 0; l < nl; ++l) {
+            const int j = __ldg(aent + s + list[l]);
+            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+            for (int64_t q = bs + threadIdx.x; q < be; q += HUB_THREADS) {
                 const int c = __ldg(bent + q);
                 atomicOr(&bm[c >> 5], 1u << (c & 31));
             }
@@ -946,22 +974,35 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
         }
         for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) cval[cb + t] = (ValT)0;
         __syncthreads();
-        // (3) values: rank lookup, reduction into C(i, rank)
+        // (3) values: rank lookup, reduction into C(i, rank) (same split of the work)
+        auto add = [&](int c, ValT prod) {
+            const int w = c >> 5;
+            uint32_t rk = gp[w >> 2];
+            const int g0 = w & ~3;
+            if (g0 + 0 < w) rk += __popc(bm[g0 + 0]);
+            if (g0 + 1 < w) rk += __popc(bm[g0 + 1]);
+            if (g0 + 2 < w) rk += __popc(bm[g0 + 2]);
+            rk += __popc(bm[w] & ((1u << (c & 31)) - 1u));
+            if ((int64_t)rk < clen) atomicAdd(&cval[cb + rk], prod);
+        };
         for (int64_t p = s + warp; p < e; p += HUB_WARPS) {
+            const int j = __ldg(aent + p);
+            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+            if (be - bs > HUB_LONG && nl > 0) {
+                // listed above (unless the list overflowed: then it is not in the list)
+                bool listed = false;
+                for (int l = lane; l < nl; l += 32) listed |= list[l] == (int)(p - s);
+                if (__any_sync(FULL, listed)) continue;
+            }
+            const ValT a = __ldg(aval + p);
+            for (int64_t q = bs + lane; q < be; q += 32) add(__ldg(bent + q), a * __ldg(bval + q));
+        }
+        for (int l = 0; l < nl; ++l) {
+            const int64_t p = s + list[l];
             const int j = __ldg(aent + p);
             const ValT a = __ldg(aval + p);
             const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
-            for (int64_t q = bs + lane; q < be; q += 32) {
-                const int c = __ldg(bent + q);
-                const int w = c >> 5;
-                uint32_t rk = gp[w >> 2];
-                const int g0 = w & ~3;
-                if (g0 + 0 < w) rk += __popc(bm[g0 + 0]);
-                if (g0 + 1 < w) rk += __popc(bm[g0 + 1]);
-                if (g0 + 2 < w) rk += __popc(bm[g0 + 2]);
-                rk += __popc(bm[w] & ((1u << (c & 31)) - 1u));
-                if ((int64_t)rk < clen) atomicAdd(&cval[cb + rk], a * __ldg(bval + q));
-            }
+            for (int64_t q = bs + threadIdx.x; q < be; q += HUB_THREADS) add(__ldg(bent + q), a * __ldg(bval + q));
         }
         __syncthreads();
     }
