@@ -87,6 +87,11 @@ __global__ void __launch_bounds__(512) k_sym_dense(const OffT* __restrict__ arm,
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     if (r0 + (int)blockIdx.x >= r1) return;
     const int64_t maxw = wbits >> 5;
+    // single-window rows: A entries whose B(_C) row is long are listed and walked by the
+    // whole CTA afterwards, so one hub B row does not hold the other warps at the barrier
+    constexpr int LONG = 256, LIST = 1024;
+    int* list = (int*)(bmp + maxw);
+    int* nlist = list + LIST;
     for (int64_t t = threadIdx.x; t < maxw; t += blockDim.x) bmp[t] = 0;
     __syncthreads();
     const bool comp = st->use_comp != 0;
@@ -99,9 +104,23 @@ __global__ void __launch_bounds__(512) k_sym_dense(const OffT* __restrict__ arm,
             const int64_t hi = min(k, lo + wbits);
             const bool single = (lo == 0 && hi == k);
             const int64_t low = lo >> 5, hiw = (hi + 31) >> 5;
+            if (threadIdx.x == 0) *nlist = 0;
+            __syncthreads();
             for (int64_t p = s + warp; p < e; p += warps) {
                 const int j = __ldg(aent + p);
                 const int64_t bs = ld(brm, j);
+                if (single) {
+                    const int64_t len = comp ? __ldg(bc_len + j) : ld(brm, j + 1) - bs;
+                    if (len > LONG) {
+                        int slot = 0;
+                        if (lane == 0) slot = atomicAdd(nlist, 1);
+                        slot = __shfl_sync(FULL, slot, 0);
+                        if (slot < LIST) {
+                            if (lane == 0) list[slot] = (int)(p - s);
+                            continue;
+                        }
+                    }
+                }
                 if (comp) {
                     const int64_t be = bs + __ldg(bc_len + j);
                     if (single) {
@@ -143,6 +162,27 @@ __global__ void __launch_bounds__(512) k_sym_dense(const OffT* __restrict__ arm,
                 }
             }
             __syncthreads();
+            if (single) {
+                const int nl = min(*nlist, LIST);
+                for (int l = 0; l < nl; ++l) {
+                    const int j = __ldg(aent + s + list[l]);
+                    const int64_t bs = ld(brm, j);
+                    if (comp) {
+                        const int64_t be = bs + __ldg(bc_len + j);
+                        for (int64_t q = bs + threadIdx.x; q < be; q += blockDim.x) {
+                            const uint2 pr = __ldg(pairs + q);
+                            atomicOr(&bmp[pr.x], pr.y);
+                        }
+                    } else {
+                        const int64_t be = ld(brm, j + 1);
+                        for (int64_t q = bs + threadIdx.x; q < be; q += blockDim.x) {
+                            const int c = __ldg(bent + q);
+                            atomicOr(&bmp[c >> 5], 1u << (c & 31));
+                        }
+                    }
+                }
+                __syncthreads();
+            }
             const int64_t nw = hiw - low;
             for (int64_t t = threadIdx.x; t < nw; t += blockDim.x) {
                 const uint32_t v = bmp[t];
@@ -807,7 +847,7 @@ static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stre
         int64_t wbits = 200 * 1024 * 8;  // 200 KB bit vector
         const int64_t k32 = ((a.k + 31) / 32) * 32;
         if (k32 < wbits) wbits = k32 > 0 ? k32 : 32;
-        const size_t smem = (size_t)(wbits / 8);
+        const size_t smem = (size_t)(wbits / 8) + 1025 * 4;  // + the long-entry list
         auto kern = k_sym_dense<OffT>;
         KCfg c = kernel_cfg(kern, threads, smem, L.num_sms);
         cudaStream_t s = dense_stream ? dense_stream : L.stream;
