@@ -792,8 +792,227 @@ __global__ void __launch_bounds__(256, MINB) k_num_pattern(const OffT* __restric
     }
 }
 
+// ------------------------------------------------------------------------------------
+// a7 for pattern rows with a dense word index, lean form (k_num_rank).  The method is
+// k_num_pattern's -- rank(c) = prefix(word(c)) + popc(mask & bits below c) from the
+// pattern kept by symbolic, accum = + into a dense per-row value array (PAPER.md:178,
+// Eq. 1) -- with the instruction stream cut down:
+//   * each 32-entry A chunk is compacted to its non-empty B rows; one B row per warp step
+//     (B rows of <= 32 entries; longer ones take a plain segment loop);
+//   * steps are branch-free: lanes past the B row's end load a valid entry of it and
+//     accumulate into a dump slot vals[CAP], so no divergent region per step;
+//   * two steps per iteration, loads two steps ahead, and both steps' rank lookups are
+//     issued before either read-modify-write (the lookups only read the pattern tables);
+//   * the prologue writes each rank's column into shared memory once (one popcount scan
+//     of two 16-bit halves), and the epilogue writes entries and values coalesced.
+// Needs B.nnz < 2^31 (32-bit element offsets) and strictly increasing B rows.
+// ------------------------------------------------------------------------------------
+template <typename ValT, int CAP>
+struct RankLayout {
+    static constexpr size_t vals = 0;  // CAP + 1 values (slot CAP: idle lanes)
+    static constexpr size_t cols = ((size_t)(CAP + 1) * sizeof(ValT) + 15) / 16 * 16;  // CAP int32
+    static constexpr size_t rec = cols + (size_t)CAP * 4;                                // 32 x {bb, len, a}
+    static constexpr size_t winfo = rec + 32 * 16;                                       // PAT_W x (mask, prefix)
+    static constexpr size_t widx = winfo + (size_t)PAT_W * 8;                            // PAT_NWIN x u8
+    static constexpr size_t bytes = (widx + (size_t)PAT_NWIN + 15) / 16 * 16;
+};
+
+template <typename OffT, typename ValT, int CAP, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                        const ValT* __restrict__ aval, const OffT* __restrict__ brm,
+                                                        const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                                        const OffT* __restrict__ crm, int32_t* __restrict__ cent,
+                                                        ValT* __restrict__ cval, const int32_t* __restrict__ perm,
+                                                        const int* __restrict__ bin_start, int bin,
+                                                        const uint2* __restrict__ pat, const long long* __restrict__ pat_off,
+                                                        const int* __restrict__ pat_len) {
+    using LY = RankLayout<ValT, CAP>;
+    extern __shared__ __align__(16) unsigned char sm_rank[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    // all shared accesses as sm_rank + 32-bit offset (shared addressing, no generic)
+    const uint32_t o_w = (uint32_t)warp * (uint32_t)LY::bytes;
+    const uint32_t o_val = o_w + (uint32_t)LY::vals, o_col = o_w + (uint32_t)LY::cols;
+    const uint32_t o_rec = o_w + (uint32_t)LY::rec, o_inf = o_w + (uint32_t)LY::winfo;
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    const int stride = gridDim.x * warps;
+    int r = r0 + blockIdx.x * warps + warp;
+    if (r >= r1) return;
+    for (int t = lane; t < CAP; t += 32) *(ValT*)(sm_rank + o_val + t * (uint32_t)sizeof(ValT)) = (ValT)0;
+    int i = perm[r];
+    while (true) {
+        const int rn = r + stride;
+        const int inext = rn < r1 ? __ldg(perm + rn) : -1;
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        const int64_t cb = ld(crm, i);
+        const int clen = (int)(ld(crm, i + 1) - cb);
+        const long long po = __ldg(pat_off + i);
+        const int pl = __ldg(pat_len + i);
+        // ---- the row's pattern: (mask, prefix) per word, word index, column of each rank ----
+        const uint2 p0 = lane < pl ? __ldg(pat + po + lane) : make_uint2(0u, 0u);
+        uint2 p1 = make_uint2(0u, 0u);
+        if (pl > 32 && lane + 32 < pl) p1 = __ldg(pat + po + 32 + lane);
+        const int c0 = __popc(p0.y), c1 = __popc(p1.y);
+        int x = c0 | (c1 << 16);  // both halves' counts at once (each total <= 2048)
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(FULL, x, d);
+            if (lane >= d) x += y;
+        }
+        const int tot = __shfl_sync(FULL, x, 31);
+        const int pre0 = (x & 0xffff) - c0;
+        const int pre1 = (tot & 0xffff) + (x >> 16) - c1;
+        const uint32_t wb = __shfl_sync(FULL, p0.x, 0);
+        const uint32_t o_idx = o_w + (uint32_t)LY::widx - wb;
+        __syncwarp();
+        if (lane < pl) {
+            sm_rank[o_idx + p0.x] = (uint8_t)lane;
+            *(uint2*)(sm_rank + o_inf + lane * 8u) = make_uint2(p0.y, (uint32_t)pre0);
+            uint32_t m = p0.y;
+            uint32_t o = o_col + (uint32_t)pre0 * 4u;
+            while (m) {
+                *(int32_t*)(sm_rank + o) = (int32_t)(p0.x * 32u + (uint32_t)(__ffs(m) - 1));
+                m &= m - 1;
+                o += 4;
+            }
+        }
+        if (lane + 32 < pl) {
+            sm_rank[o_idx + p1.x] = (uint8_t)(lane + 32);
+            *(uint2*)(sm_rank + o_inf + (lane + 32) * 8u) = make_uint2(p1.y, (uint32_t)pre1);
+            uint32_t m = p1.y;
+            uint32_t o = o_col + (uint32_t)pre1 * 4u;
+            while (m) {
+                *(int32_t*)(sm_rank + o) = (int32_t)(p1.x * 32u + (uint32_t)(__ffs(m) - 1));
+                m &= m - 1;
+                o += 4;
+            }
+        }
+        __syncwarp();
+        auto rank = [&](int col, bool valid) -> uint32_t {
+            const uint32_t wi = sm_rank[o_idx + ((uint32_t)col >> 5)];
+            const uint2 mp = *(const uint2*)(sm_rank + o_inf + wi * 8u);
+            const uint32_t rk = mp.y + __popc(mp.x & ~(0xffffffffu << (col & 31)));
+            return valid ? rk : (uint32_t)CAP;
+        };
+        auto acc = [&](uint32_t rk, ValT prod) {
+            ValT* p = (ValT*)(sm_rank + o_val + rk * (uint32_t)sizeof(ValT));
+            *p += prod;
+        };
+        // ---- products, one 32-entry A chunk at a time ----
+        for (int64_t a0 = s; a0 < e; a0 += 32) {
+            const int na = (int)min((int64_t)32, e - a0);
+            int bb = 0, bl = 0;
+            double av = 0.0;
+            if (lane < na) {
+                const int j = __ldg(aent + a0 + lane);
+                av = (double)__ldg(aval + a0 + lane);
+                bb = (int)ld(brm, j);
+                bl = (int)(ld(brm, j + 1) - bb);
+            }
+            const unsigned ne = __ballot_sync(FULL, bl > 0);
+            const int nt = __popc(ne);
+            const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
+            __syncwarp();
+            if (bl > 0)
+                *(int4*)(sm_rank + o_rec + __popc(ne & lanemask_lt()) * 16u) =
+                    make_int4(bb, bl, __double2loint(av), __double2hiint(av));
+            __syncwarp();
+            if (nt == 0) continue;
+            if (maxbl <= 32) {
+                auto load = [&](int t, int& col, ValT& bv, ValT& a, bool& valid) {
+                    const int4 rr = *(const int4*)(sm_rank + o_rec + (uint32_t)min(t, nt - 1) * 16u);
+                    valid = t < nt && lane < rr.y;
+                    const int q = rr.x + min(lane, rr.y - 1);
+                    col = __ldg(bent + q);
+                    bv = __ldg(bval + q);
+                    a = (ValT)__hiloint2double(rr.w, rr.z);
+                };
+                int colA, colB;
+                ValT bA, bB, aA, aB;
+                bool vA, vB;
+                load(0, colA, bA, aA, vA);
+                load(1, colB, bB, aB, vB);
+                for (int t = 0; t < nt; t += 2) {
+                    const uint32_t rA = rank(colA, vA), rB = rank(colB, vB);
+                    const ValT pA = aA * bA, pB = aB * bB;
+                    if (t + 2 < nt) {
+                        load(t + 2, colA, bA, aA, vA);
+                        load(t + 3, colB, bB, aB, vB);
+                    }
+                    acc(rA, pA);
+                    __syncwarp();
+                    acc(rB, pB);
+                    __syncwarp();
+                }
+            } else {
+                for (int t = 0; t < nt; ++t) {
+                    const int4 rr = *(const int4*)(sm_rank + o_rec + (uint32_t)t * 16u);
+                    const ValT a = (ValT)__hiloint2double(rr.w, rr.z);
+                    for (int q0 = 0; q0 < rr.y; q0 += 32) {
+                        const bool valid = q0 + lane < rr.y;
+                        const int q = rr.x + min(q0 + lane, rr.y - 1);
+                        const int col = __ldg(bent + q);
+                        const ValT bv = __ldg(bval + q);
+                        acc(rank(col, valid), a * bv);
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        // ---- entries and values, coalesced; reset ----
+        for (int t = lane; t < clen; t += 32) {
+            cent[cb + t] = *(const int32_t*)(sm_rank + o_col + (uint32_t)t * 4u);
+            ValT* p = (ValT*)(sm_rank + o_val + (uint32_t)t * (uint32_t)sizeof(ValT));
+            cval[cb + t] = *p;
+            *p = (ValT)0;
+        }
+        __syncwarp();
+        if (inext < 0) break;
+        r = rn;
+        i = inext;
+    }
+}
+
+// KK_NUM_RANK=0 selects k_num_pattern for the dense-index pattern bins (experiments)
+static bool use_num_rank() {
+    static const bool v = [] {
+        const char* s = getenv("KK_NUM_RANK");
+        return !(s && s[0] == '0');
+    }();
+    return v;
+}
+
+template <typename OffT, typename ValT, int CAP>
+static void launch_num_rank(Launch& L, const NumArgs& a, int bin) {
+    const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
+    if (rows <= 0) return;
+    const int warps = 8;
+    const size_t smem = (size_t)warps * RankLayout<ValT, CAP>::bytes;
+    static const int minb = [] {
+        const char* v = getenv("KK_RANK_MINB");
+        const int x = v ? atoi(v) : 4;
+        return (x == 5 || x == 6) ? x : 4;
+    }();
+    auto kern = minb == 5 ? k_num_rank<OffT, ValT, CAP, 5>
+              : minb == 6 ? k_num_rank<OffT, ValT, CAP, 6>
+                          : k_num_rank<OffT, ValT, CAP, 4>;
+    KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    int64_t need = (rows + warps - 1) / warps;
+    int grid = (int)std::min<int64_t>(need, c.grid_cap);
+    L.begin(kname("num_rank", CAP), L.stream);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
+                                               (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
+                                               (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
+                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len);
+    L.end(L.stream);
+}
+
 template <typename OffT, typename ValT, int CAP, bool DENSE>
 static void launch_num_pattern(Launch& L, const NumArgs& a, int bin) {
+    if (DENSE && a.B.nnz < INT32_MAX && use_num_rank()) {
+        launch_num_rank<OffT, ValT, CAP>(L, a, bin);
+        return;
+    }
     const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
     if (rows <= 0) return;
     const int warps = 8;

@@ -769,8 +769,219 @@ __global__ void __launch_bounds__(256, 1) k_sym_window(const OffT* __restrict__ 
     }
 }
 
+// ------------------------------------------------------------------------------------
+// a5 for window rows, lean form (k_sym_rows): the same bit-vector accumulator (accum = OR,
+// PAPER.md:171, 180) and kept pattern as sym_window_rows, without the flattened pairs and
+// their duplicate-word merging.  Each B_C row has distinct words, so a B_C row per group of
+// lanes needs no merging: with B_C rows of <= 16 pairs two rows run per warp step (lanes
+// 0-15 and 16-31), their bit-vector updates in two rounds; longer rows take the whole warp.
+// Pairs are loaded one step ahead.  The touched-word list is sorted with one key per lane
+// when it holds <= 32 words.  Pattern space is taken from the pool in warp-private blocks
+// (one pool atomic per block of pblk pairs, not per row; pblk = the pool share of one
+// warp, clamped to [PAT_WORDS, 2048]).  Needs B.nnz < 2^31; without B_C the bit-vector
+// OR is atomic.
+// ------------------------------------------------------------------------------------
+
+template <typename OffT, int W>
+__global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                  const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                                  const int32_t* __restrict__ bc_len,
+                                                  const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
+                                                  const int* __restrict__ bin_start, int bin,
+                                                  const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
+                                                  PatOut po, DevStatus* st, int pblk) {
+    constexpr int NW = W / 32;
+    constexpr int WB = NW + 64 + PAT_WORDS;  // words per warp: bitmap | rec[32] (int2) | list
+    extern __shared__ __align__(16) uint32_t sm_rows[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+    uint32_t* bm = sm_rows + (size_t)warp * WB;
+    int2* rec = (int2*)(bm + NW);
+    uint32_t* wl = bm + NW + 64;
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    const int stride = gridDim.x * warps;
+    int r = r0 + blockIdx.x * warps + warp;
+    if (r >= r1) return;
+    for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
+    const int half = lane >> 4, hl = lane & 15;
+    long long pcur = 0, pend = 0;  // this warp's block of the pattern pool
+    // without B_C, words repeat inside a B row: the OR is atomic (plain B entries)
+    const bool comp = st->use_comp != 0;
+    int i = perm[r];
+    __syncwarp();
+    while (true) {
+        const int rn = r + stride;
+        const int inext = rn < r1 ? __ldg(perm + rn) : -1;
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        const uint32_t wb = (uint32_t)__ldg(wlo + i) >> 5;
+        int cnt = 0, nt = 0;
+        // OR (w, m) into the bit vector; count new bits; list words turning non-zero
+        auto upd = [&](uint32_t w, uint32_t m, bool act) -> bool {
+            bool fresh = false;
+            if (act) {
+                const uint32_t x = w - wb;
+                uint32_t old;
+                if (comp) {
+                    old = bm[x];
+                    bm[x] = old | m;
+                } else {
+                    old = atomicOr(&bm[x], m);
+                }
+                cnt += __popc(m & ~old);
+                fresh = old == 0;
+            }
+            return fresh;
+        };
+        auto list = [&](bool fresh, uint32_t w) {
+            const unsigned fb = __ballot_sync(FULL, fresh);
+            if (fresh) {
+                const int pos = nt + __popc(fb & lanemask_lt());
+                if (pos < PAT_WORDS) wl[pos] = w - wb;
+            }
+            nt += __popc(fb);
+        };
+        for (int64_t a0 = s; a0 < e; a0 += 32) {
+            const int na = (int)min((int64_t)32, e - a0);
+            int bb = 0, bl = 0;
+            if (lane < na) {
+                const int j = __ldg(aent + a0 + lane);
+                bb = (int)ld(brm, j);
+                bl = comp ? __ldg(bc_len + j) : (int)(ld(brm, j + 1) - bb);
+            }
+            const unsigned ne = __ballot_sync(FULL, bl > 0);
+            const int ntr = __popc(ne);
+            const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
+            __syncwarp();
+            if (bl > 0) rec[__popc(ne & lanemask_lt())] = make_int2(bb, bl);
+            __syncwarp();
+            if (ntr == 0) continue;
+            auto pair_at = [&](int q) -> uint2 {
+                if (comp) return __ldg(pairs + q);
+                const int c = __ldg(bent + q);
+                return make_uint2((uint32_t)c >> 5, 1u << (c & 31));
+            };
+            if (maxbl <= 16) {
+                // two B_C rows per step: row t + half on lanes [16 half, 16 half + 16)
+                auto fetch = [&](int t, uint2& p, bool& act) {
+                    const int tt = t + half;
+                    const int2 rr = rec[min(tt, ntr - 1)];
+                    act = tt < ntr && hl < rr.y;
+                    p = pair_at(rr.x + min(hl, rr.y - 1));
+                };
+                uint2 p;
+                bool act;
+                fetch(0, p, act);
+                for (int t = 0; t < ntr; t += 2) {
+                    uint2 pn = p;
+                    bool actn = false;
+                    if (t + 2 < ntr) fetch(t + 2, pn, actn);
+                    bool fresh = upd(p.x, p.y, act && half == 0);
+                    __syncwarp();
+                    fresh |= upd(p.x, p.y, act && half == 1);
+                    list(fresh, p.x);
+                    p = pn;
+                    act = actn;
+                }
+            } else {
+                for (int t = 0; t < ntr; ++t) {
+                    const int2 rr = rec[t];
+                    for (int q0 = 0; q0 < rr.y; q0 += 32) {
+                        const bool act = q0 + lane < rr.y;
+                        const uint2 pq = pair_at(rr.x + min(q0 + lane, rr.y - 1));
+                        list(upd(pq.x, pq.y, act), pq.x);
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        cnt = warp_sum(cnt);
+        if (lane == 0) counts[i] = cnt;
+        __syncwarp();
+        if (nt <= PAT_WORDS) {
+            // sorted pattern into the pool, clear the listed words
+            long long off = -1;
+            if (po.pat) {
+                if (pcur + nt > pend) {
+                    long long o = 0;
+                    if (lane == 0) o = (long long)atomicAdd(&st->pat_used, (unsigned long long)pblk);
+                    o = __shfl_sync(FULL, o, 0);
+                    pcur = o;
+                    pend = min(o + pblk, (long long)po.cap);
+                }
+                if (pcur + nt <= pend) {
+                    off = pcur;
+                    pcur += nt;
+                }
+            }
+            if (nt <= 32) {
+                uint32_t v[1] = {lane < nt ? wl[lane] : 0xffffffffu};
+                warp_bitonic_sort<1>(v);
+                if (lane < nt) {
+                    const uint32_t m = bm[v[0]];
+                    bm[v[0]] = 0;
+                    if (off >= 0) po.pat[off + lane] = make_uint2(v[0] + wb, m);
+                }
+            } else {
+                uint32_t v[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) v[q] = lane * 2 + q < nt ? wl[lane * 2 + q] : 0xffffffffu;
+                warp_bitonic_sort<2>(v);
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int idx = lane * 2 + q;
+                    if (idx < nt) {
+                        const uint32_t m = bm[v[q]];
+                        bm[v[q]] = 0;
+                        if (off >= 0) po.pat[off + idx] = make_uint2(v[q] + wb, m);
+                    }
+                }
+            }
+            if (po.pat && lane == 0) {
+                po.off[i] = off;
+                po.len[i] = nt;
+            }
+        } else {
+            for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
+        }
+        __syncwarp();
+        if (inext < 0) break;
+        r = rn;
+        i = inext;
+    }
+}
+
+// KK_SYM_ROWS=0 selects k_sym_window for the window bins (experiments)
+static bool use_sym_rows() {
+    static const bool v = [] {
+        const char* s = getenv("KK_SYM_ROWS");
+        return !(s && s[0] == '0');
+    }();
+    return v;
+}
+
+template <typename OffT, int W>
+static void launch_sym_rows(Launch& L, const SymArgs& a, int bin) {
+    const int warps = 8;
+    const size_t smem = (size_t)warps * ((size_t)W / 32 + 64 + PAT_WORDS) * 4;
+    auto kern = k_sym_rows<OffT, W>;
+    KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    int64_t need = (a.A.nrows + warps - 1) / warps;
+    int grid = (int)std::min<int64_t>(need, c.grid_cap);
+    const int64_t share = a.pat.cap / ((int64_t)grid * warps);
+    const int pblk = (int)std::max<int64_t>(PAT_WORDS, std::min<int64_t>(2048, share));
+    L.begin(kname("sym_rows", W), L.stream);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+                                               a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
+                                               a.counts, a.pat, (DevStatus*)a.st, pblk);
+    L.end(L.stream);
+}
+
 template <typename OffT, int W>
 static void launch_sym_window(Launch& L, const SymArgs& a, int bin) {
+    if (a.B.nnz < INT32_MAX && use_sym_rows()) {
+        launch_sym_rows<OffT, W>(L, a, bin);
+        return;
+    }
     const int warps = W <= 16384 ? 8 : 4;
     const size_t smem = (size_t)warps * ((size_t)W / 32 + 672 + PAT_WORDS) * 4;
     auto kern = k_sym_window<OffT, W>;
