@@ -444,6 +444,7 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     sa.pat.off = keep_pat ? (long long*)h->pat_off.p : nullptr;
     sa.pat.len = keep_pat ? (int*)h->pat_len.p : nullptr;
     sa.st = dst;
+    sa.comp_mode = comp_mode;
     sa.logG = pick_logG(n > 0 ? (double)B->nnz / (double)n / (comp_mode != 0 ? 2.0 : 1.0) : 1.0);
     cudaStream_t side = nullptr;
     if (h->side) {

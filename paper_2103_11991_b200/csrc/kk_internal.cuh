@@ -128,6 +128,7 @@ struct SymArgs {
     int32_t* cursors;       // nnz(A) scratch for windowed rows
     const DevStatus* st;
     int logG;
+    int comp_mode;          // opts.compression: 1 on, 0 off, -1 decided on the device (a1)
 };
 void symbolic_bins(Launch& L, const SymArgs& a, cudaStream_t dense_stream);
 

@@ -772,17 +772,19 @@ __global__ void __launch_bounds__(256, 1) k_sym_window(const OffT* __restrict__ 
 // ------------------------------------------------------------------------------------
 // a5 for window rows, lean form (k_sym_rows): the same bit-vector accumulator (accum = OR,
 // PAPER.md:171, 180) and kept pattern as sym_window_rows, without the flattened pairs and
-// their duplicate-word merging.  Each B_C row has distinct words, so a B_C row per group of
-// lanes needs no merging: with B_C rows of <= 16 pairs two rows run per warp step (lanes
-// 0-15 and 16-31), their bit-vector updates in two rounds; longer rows take the whole warp.
-// Pairs are loaded one step ahead.  The touched-word list is sorted with one key per lane
-// when it holds <= 32 words.  Pattern space is taken from the pool in warp-private blocks
-// (one pool atomic per block of pblk pairs, not per row; pblk = the pool share of one
-// warp, clamped to [PAT_WORDS, 2048]).  Needs B.nnz < 2^31; without B_C the bit-vector
-// OR is atomic.
+// their duplicate-word merging.  A B_C row has distinct words, so a B_C row per group of
+// lanes needs no merging: with B_C rows of <= G pairs, R = 32 / G rows run per warp step
+// (G = 8, 10, 16, 32), their bit-vector read-OR-writes in R rounds (rows of a step may share
+// words), the counting of new bits and the touched-word list once per step.  Longer rows
+// take the whole warp per 32-pair segment.  Pairs are loaded one step ahead.  The
+// touched-word list is sorted with one key per lane when it holds <= 32 words.  Pattern
+// space is taken from the pool in warp-private blocks (one pool atomic per block of pblk
+// pairs, not per row; pblk = the pool share of one warp, clamped to [PAT_WORDS, 2048]).
+// Needs B.nnz < 2^31; without B_C (COMP = false, words repeat inside a B row) the OR is a
+// shared atomic.
 // ------------------------------------------------------------------------------------
 
-template <typename OffT, int W>
+template <typename OffT, int W, bool COMP>
 __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                   const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
                                                   const int32_t* __restrict__ bc_len,
@@ -801,37 +803,26 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
     const int stride = gridDim.x * warps;
     int r = r0 + blockIdx.x * warps + warp;
     if (r >= r1) return;
+    if (COMP != (st->use_comp != 0)) return;  // launched for the other mode
     for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
-    const int half = lane >> 4, hl = lane & 15;
     long long pcur = 0, pend = 0;  // this warp's block of the pattern pool
-    // without B_C, words repeat inside a B row: the OR is atomic (plain B entries)
-    const bool comp = st->use_comp != 0;
     int i = perm[r];
     __syncwarp();
+    auto pair_at = [&](int q) -> uint2 {
+        if (COMP) return __ldg(pairs + q);
+        const int c = __ldg(bent + q);
+        return make_uint2((uint32_t)c >> 5, 1u << (c & 31));
+    };
     while (true) {
         const int rn = r + stride;
         const int inext = rn < r1 ? __ldg(perm + rn) : -1;
         const int64_t s = ld(arm, i), e = ld(arm, i + 1);
         const uint32_t wb = (uint32_t)__ldg(wlo + i) >> 5;
         int cnt = 0, nt = 0;
-        // OR (w, m) into the bit vector; count new bits; list words turning non-zero
-        auto upd = [&](uint32_t w, uint32_t m, bool act) -> bool {
-            bool fresh = false;
-            if (act) {
-                const uint32_t x = w - wb;
-                uint32_t old;
-                if (comp) {
-                    old = bm[x];
-                    bm[x] = old | m;
-                } else {
-                    old = atomicOr(&bm[x], m);
-                }
-                cnt += __popc(m & ~old);
-                fresh = old == 0;
-            }
-            return fresh;
-        };
-        auto list = [&](bool fresh, uint32_t w) {
+        // count the bits a lane added and list the words it turned non-zero
+        auto post = [&](uint32_t w, uint32_t m, uint32_t old, bool act) {
+            const bool fresh = act && old == 0;
+            if (act) cnt += __popc(m & ~old);
             const unsigned fb = __ballot_sync(FULL, fresh);
             if (fresh) {
                 const int pos = nt + __popc(fb & lanemask_lt());
@@ -839,13 +830,22 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
             }
             nt += __popc(fb);
         };
+        auto rmw = [&](uint32_t w, uint32_t m) -> uint32_t {
+            const uint32_t x = w - wb;
+            if (COMP) {
+                const uint32_t old = bm[x];
+                bm[x] = old | m;
+                return old;
+            }
+            return atomicOr(&bm[x], m);
+        };
         for (int64_t a0 = s; a0 < e; a0 += 32) {
             const int na = (int)min((int64_t)32, e - a0);
             int bb = 0, bl = 0;
             if (lane < na) {
                 const int j = __ldg(aent + a0 + lane);
                 bb = (int)ld(brm, j);
-                bl = comp ? __ldg(bc_len + j) : (int)(ld(brm, j + 1) - bb);
+                bl = COMP ? __ldg(bc_len + j) : (int)(ld(brm, j + 1) - bb);
             }
             const unsigned ne = __ballot_sync(FULL, bl > 0);
             const int ntr = __popc(ne);
@@ -854,30 +854,35 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
             if (bl > 0) rec[__popc(ne & lanemask_lt())] = make_int2(bb, bl);
             __syncwarp();
             if (ntr == 0) continue;
-            auto pair_at = [&](int q) -> uint2 {
-                if (comp) return __ldg(pairs + q);
-                const int c = __ldg(bent + q);
-                return make_uint2((uint32_t)c >> 5, 1u << (c & 31));
-            };
-            if (maxbl <= 16) {
-                // two B_C rows per step: row t + half on lanes [16 half, 16 half + 16)
+            if (maxbl <= 32) {
+                // R rows per step, G lanes per row; lanes >= R*G idle
+                const int R = maxbl <= 8 ? 4 : maxbl <= 10 ? 3 : maxbl <= 16 ? 2 : 1;
+                const int G = 32 / R;
+                const int grp = lane / G, gl = lane - grp * G;
                 auto fetch = [&](int t, uint2& p, bool& act) {
-                    const int tt = t + half;
+                    const int tt = t + grp;
                     const int2 rr = rec[min(tt, ntr - 1)];
-                    act = tt < ntr && hl < rr.y;
-                    p = pair_at(rr.x + min(hl, rr.y - 1));
+                    act = grp < R && tt < ntr && gl < rr.y;
+                    p = pair_at(rr.x + min(gl, rr.y - 1));
                 };
                 uint2 p;
                 bool act;
                 fetch(0, p, act);
-                for (int t = 0; t < ntr; t += 2) {
+                for (int t = 0; t < ntr; t += R) {
                     uint2 pn = p;
                     bool actn = false;
-                    if (t + 2 < ntr) fetch(t + 2, pn, actn);
-                    bool fresh = upd(p.x, p.y, act && half == 0);
-                    __syncwarp();
-                    fresh |= upd(p.x, p.y, act && half == 1);
-                    list(fresh, p.x);
+                    if (t + R < ntr) fetch(t + R, pn, actn);
+                    uint32_t old = 0;
+                    if (COMP) {
+                        // rows of a step may share words: one row per round
+                        for (int k = 0; k < R; ++k) {
+                            if (act && grp == k) old = rmw(p.x, p.y);
+                            __syncwarp();
+                        }
+                    } else if (act) {
+                        old = rmw(p.x, p.y);
+                    }
+                    post(p.x, p.y, old, act);
                     p = pn;
                     act = actn;
                 }
@@ -887,7 +892,8 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
                     for (int q0 = 0; q0 < rr.y; q0 += 32) {
                         const bool act = q0 + lane < rr.y;
                         const uint2 pq = pair_at(rr.x + min(q0 + lane, rr.y - 1));
-                        list(upd(pq.x, pq.y, act), pq.x);
+                        const uint32_t old = act ? rmw(pq.x, pq.y) : 0u;
+                        post(pq.x, pq.y, old, act);
                         __syncwarp();
                     }
                 }
@@ -963,17 +969,26 @@ template <typename OffT, int W>
 static void launch_sym_rows(Launch& L, const SymArgs& a, int bin) {
     const int warps = 8;
     const size_t smem = (size_t)warps * ((size_t)W / 32 + 64 + PAT_WORDS) * 4;
-    auto kern = k_sym_rows<OffT, W>;
+    // compression may be decided on the device (a1, comp_mode -1): then both kernels are
+    // launched and the one that does not match the device flag exits
+    auto kern = k_sym_rows<OffT, W, true>;
+    auto kern0 = k_sym_rows<OffT, W, false>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    kernel_cfg(kern0, warps * 32, smem, L.num_sms);
     int64_t need = (a.A.nrows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
     const int64_t share = a.pat.cap / ((int64_t)grid * warps);
     const int pblk = (int)std::max<int64_t>(PAT_WORDS, std::min<int64_t>(2048, share));
     L.begin(kname("sym_rows", W), L.stream);
-    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
-                                               a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
-                                               a.counts, a.pat, (DevStatus*)a.st, pblk);
-    L.end(L.stream);
+    int nl = 0;
+    for (auto k : {kern, kern0}) {
+        if ((k == kern && a.comp_mode == 0) || (k == kern0 && a.comp_mode == 1)) continue;
+        k<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
+                                                a.counts, a.pat, (DevStatus*)a.st, pblk);
+        ++nl;
+    }
+    L.end(L.stream, nl);
 }
 
 template <typename OffT, int W>
