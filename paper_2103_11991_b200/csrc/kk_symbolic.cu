@@ -4,6 +4,8 @@
 //   k_sym_dense     CTA-owned dense bit vector over column windows
 #include "kk_device.cuh"
 
+#include <type_traits>
+
 namespace kk {
 // ------------------------------------------------------------------------------------
 // a5: symbolic, warp-owned shared hash ("HashmapAccumulator"; accum = OR
@@ -854,10 +856,11 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
             if (bl > 0) rec[__popc(ne & lanemask_lt())] = make_int2(bb, bl);
             __syncwarp();
             if (ntr == 0) continue;
-            if (maxbl <= 32) {
-                // R rows per step, G lanes per row; lanes >= R*G idle
-                const int R = maxbl <= 8 ? 4 : maxbl <= 10 ? 3 : maxbl <= 16 ? 2 : 1;
-                const int G = 32 / R;
+            // R rows per step, G = 32 / R lanes per row (lanes >= R*G idle); loads of the
+            // next step are unconditional (indices clamped into the chunk's last row)
+            auto run = [&](auto RC) {
+                constexpr int R = decltype(RC)::value;
+                constexpr int G = 32 / R;
                 const int grp = lane / G, gl = lane - grp * G;
                 auto fetch = [&](int t, uint2& p, bool& act) {
                     const int tt = t + grp;
@@ -869,24 +872,35 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
                 bool act;
                 fetch(0, p, act);
                 for (int t = 0; t < ntr; t += R) {
-                    uint2 pn = p;
-                    bool actn = false;
-                    if (t + R < ntr) fetch(t + R, pn, actn);
+                    uint2 pn;
+                    bool actn;
+                    fetch(t + R, pn, actn);
                     uint32_t old = 0;
                     if (COMP) {
                         // rows of a step may share words: one row per round
+#pragma unroll
                         for (int k = 0; k < R; ++k) {
                             if (act && grp == k) old = rmw(p.x, p.y);
                             __syncwarp();
                         }
-                    } else if (act) {
-                        old = rmw(p.x, p.y);
+                    } else {
+                        if (act) old = rmw(p.x, p.y);
+                        __syncwarp();
                     }
                     post(p.x, p.y, old, act);
                     p = pn;
                     act = actn;
                 }
-            } else {
+            };
+            if (maxbl <= 8)
+                run(std::integral_constant<int, 4>{});
+            else if (maxbl <= 10)
+                run(std::integral_constant<int, 3>{});
+            else if (maxbl <= 16)
+                run(std::integral_constant<int, 2>{});
+            else if (maxbl <= 32)
+                run(std::integral_constant<int, 1>{});
+            else {
                 for (int t = 0; t < ntr; ++t) {
                     const int2 rr = rec[t];
                     for (int q0 = 0; q0 < rr.y; q0 += 32) {
