@@ -808,18 +808,28 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
     if (COMP != (st->use_comp != 0)) return;  // launched for the other mode
     for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
     long long pcur = 0, pend = 0;  // this warp's block of the pattern pool
-    int i = perm[r];
-    __syncwarp();
     auto pair_at = [&](int q) -> uint2 {
         if (COMP) return __ldg(pairs + q);
         const int c = __ldg(bent + q);
         return make_uint2((uint32_t)c >> 5, 1u << (c & 31));
     };
+    // rows are software-pipelined: the next row's bounds and window are loaded when a row
+    // starts, its first 32 A entries when the row's products are done
+    int i = perm[r];
+    int64_t s = ld(arm, i), e = ld(arm, i + 1);
+    uint32_t wb = (uint32_t)__ldg(wlo + i) >> 5;
+    int jfirst = lane < e - s ? __ldg(aent + s + lane) : 0;
+    int inext = r + stride < r1 ? __ldg(perm + r + stride) : -1;
+    __syncwarp();
     while (true) {
-        const int rn = r + stride;
-        const int inext = rn < r1 ? __ldg(perm + rn) : -1;
-        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
-        const uint32_t wb = (uint32_t)__ldg(wlo + i) >> 5;
+        int64_t sn = 0, en = 0;
+        uint32_t wbn = 0;
+        if (inext >= 0) {
+            sn = ld(arm, inext);
+            en = ld(arm, inext + 1);
+            wbn = (uint32_t)__ldg(wlo + inext) >> 5;
+        }
+        const int inext2 = r + 2 * stride < r1 ? __ldg(perm + r + 2 * stride) : -1;
         int cnt = 0, nt = 0;
         // count the bits a lane added and list the words it turned non-zero
         auto post = [&](uint32_t w, uint32_t m, uint32_t old, bool act) {
@@ -845,7 +855,7 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
             const int na = (int)min((int64_t)32, e - a0);
             int bb = 0, bl = 0;
             if (lane < na) {
-                const int j = __ldg(aent + a0 + lane);
+                const int j = a0 == s ? jfirst : __ldg(aent + a0 + lane);
                 bb = (int)ld(brm, j);
                 bl = COMP ? __ldg(bc_len + j) : (int)(ld(brm, j + 1) - bb);
             }
@@ -914,6 +924,7 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
             }
             __syncwarp();
         }
+        jfirst = inext >= 0 && lane < en - sn ? __ldg(aent + sn + lane) : 0;
         cnt = warp_sum(cnt);
         if (lane == 0) counts[i] = cnt;
         __syncwarp();
@@ -965,8 +976,12 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
         }
         __syncwarp();
         if (inext < 0) break;
-        r = rn;
+        r += stride;
         i = inext;
+        s = sn;
+        e = en;
+        wb = wbn;
+        inext = inext2;
     }
 }
 
