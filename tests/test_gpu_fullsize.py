@@ -71,10 +71,18 @@ def test_C4_rmat_full(oracle_mod):
     heavy = np.argsort(lens)[-8:]
     rows = np.unique(np.concatenate([_rows_sample(A.nrows, 200, 3), heavy]))
     _check_rows(oracle_mod, _host(A), _host(B), rm.cpu(), ent, val, rows)
-    # row sums identity (unit values): sum_j C(i,j) = sum_{k in A(i,:)} outdeg(k)
+    # row sums identity (unit values): sum_j C(i,j) = sum_{k in A(i,:)} outdeg(k); C's values
+    # (78 GB) are reduced in row blocks of <= 2^28 entries so no 9.7e9-long index is formed
     rs = torch.zeros(A.nrows, dtype=torch.float64, device="cuda")
-    rows_of = torch.repeat_interleave(torch.arange(A.nrows, device="cuda"), torch.diff(rm))
-    rs.index_add_(0, rows_of, val)
+    rmc = rm.cpu()
+    r0 = 0
+    while r0 < A.nrows:
+        r1 = int(torch.searchsorted(rmc, rmc[r0] + 2**28, right=True)) - 1
+        r1 = min(max(r1, r0 + 1), A.nrows)
+        lo, hi = int(rmc[r0]), int(rmc[r1])
+        rows_of = torch.repeat_interleave(torch.arange(r0, r1, device="cuda"), torch.diff(rm[r0:r1 + 1]))
+        rs.index_add_(0, rows_of, val[lo:hi])
+        r0 = r1
     outdeg = torch.diff(Bd.row_map).double()
     ar = torch.repeat_interleave(torch.arange(A.nrows, device="cuda"), torch.diff(Ad.row_map))
     want = torch.zeros_like(rs).index_add_(0, ar, outdeg[Ad.entries.long()])
