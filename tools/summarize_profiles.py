@@ -117,6 +117,11 @@ RAW = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
 
 def summarize_ncu(tag):
     rep = os.path.join(OUT, f"prof_top_{tag}.ncu-rep")
+    if not os.path.exists(rep) and os.path.exists(rep + ".gz"):
+        import gzip
+        import shutil
+        with gzip.open(rep + ".gz", "rb") as fi, open(rep, "wb") as fo:
+            shutil.copyfileobj(fi, fo)
     if not os.path.exists(rep):
         return None
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
