@@ -54,6 +54,12 @@ def _load():
             lib.kko_numeric.restype = ctypes.c_int
             lib.kko_numeric.argtypes = [ctypes.c_int64] * 3 + [_i64p, _i32p, _f64p, _i64p, _i32p, _f64p, _i64p,
                                                                _i32p, _f64p, _f64p]
+            lib.kko_jacobi_counts.restype = ctypes.c_int
+            lib.kko_jacobi_counts.argtypes = [ctypes.c_int64] * 2 + [_i64p, _i32p, _i64p, _i32p, _i64p]
+            lib.kko_jacobi_fill.restype = ctypes.c_int
+            lib.kko_jacobi_fill.argtypes = [ctypes.c_int64] * 2 + [_i64p, _i32p, _f64p, _i64p, _i32p, _f64p,
+                                                                   ctypes.c_double, _f64p, _i64p, _i32p, _f64p,
+                                                                   _f64p]
             lib.kko_num_threads.restype = ctypes.c_int
             lib.kko_set_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
@@ -146,3 +152,34 @@ def spgemm(A, B):
     rm = symbolic(A, B)
     ent, val, bnd = numeric(A, B, rm)
     return rm, ent, val, bnd
+
+
+def jacobi(omega, dinv, A, B):
+    """Jacobi-fused SpGEMM reference C = (I - omega D^-1 A) B (Sec. 2.2.2),
+    written as the paper's three-kernel composition E = AB, F = D^-1 E, C = B - omega F
+    (MSAK), row by row.  A is m x m, B is m x k, dinv has m entries.
+    Returns (row_map[int64], entries[int32], values[f64], bound[f64]) with
+    bound = |b| + |omega| |dinv_i| sum |a||b|; C's pattern = pattern(B) U pattern(E)."""
+    lib = _load()
+    m, n, arm, aent, aval = _csr(A)
+    nb, k, brm, bent, bval = _csr(B)
+    if n != m or nb != m:
+        raise ValueError("Jacobi SpGEMM needs A m x m and B m x k")
+    d = _np(dinv, np.float64)
+    if len(d) != m:
+        raise ValueError("dinv must have m entries")
+    counts = np.zeros(max(m, 1), dtype=np.int64)
+    if lib.kko_jacobi_counts(m, k, _p(arm, _i64p), _p(aent, _i32p), _p(brm, _i64p), _p(bent, _i32p),
+                             _p(counts, _i64p)) != 0:
+        raise ValueError("oracle jacobi: bad input")
+    rm = np.zeros(m + 1, dtype=np.int64)
+    rm[1:] = np.cumsum(counts[:m])
+    nnz = int(rm[-1])
+    ent = np.zeros(max(nnz, 1), dtype=np.int32)
+    val = np.zeros(max(nnz, 1), dtype=np.float64)
+    bnd = np.zeros(max(nnz, 1), dtype=np.float64)
+    if lib.kko_jacobi_fill(m, k, _p(arm, _i64p), _p(aent, _i32p), _p(aval, _f64p), _p(brm, _i64p),
+                           _p(bent, _i32p), _p(bval, _f64p), float(omega), _p(d, _f64p), _p(rm, _i64p),
+                           _p(ent, _i32p), _p(val, _f64p), _p(bnd, _f64p)) != 0:
+        raise ValueError("oracle jacobi: bad input")
+    return rm, ent[:nnz], val[:nnz], bnd[:nnz]

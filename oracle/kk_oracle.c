@@ -226,3 +226,112 @@ int kko_numeric(int64_t m, int64_t n, int64_t k, const int64_t* a_row_map, const
     }
     return bad ? -1 : 0;
 }
+
+/*
+ * Jacobi-fused SpGEMM reference, PAPER.md:188-217 (Sec. 2.2.2): C = (I - omega D^-1 A) B
+ * with A square (m x m), B m x k, dinv[i] = D^-1(i) given.  Written as the paper's
+ * three-kernel composition (MSAK), applied row by row (rows are
+ * independent):
+ *   1. E(i,:) = sum_{j in A(i,:)} A(i,j) B(j,:)          (Eq. 1, usual SpGEMM)
+ *   2. F(i,:) = D^-1(i) E(i,:)                             (scaling)
+ *   3. C(i,:) = B(i,:) - omega F(i,:)                      (matrix addition)
+ * The pattern of C(i,:) is the union of the patterns of B(i,:) and E(i,:) (structural,
+ * R1); with a stored diagonal in A it equals E's pattern.  Values:
+ * c = b - omega * (dinv_i * e) on the union (b = 0 or e = 0 where a side is absent).
+ * bound = |b| + |omega| |dinv_i| sum |a||b| (R5 tolerance reference).
+ * kko_jacobi_counts fills counts[m] (|C(i,:)|); kko_jacobi_fill fills the rows given
+ * the exclusive scan c_row_map.  Return 0, or -1 on bad input.
+ */
+static int jacobi_rows(int64_t m, int64_t k, const int64_t* a_row_map, const int32_t* a_entries,
+                       const double* a_values, const int64_t* b_row_map, const int32_t* b_entries,
+                       const double* b_values, double omega, const double* dinv, int64_t* counts,
+                       const int64_t* c_row_map, int32_t* c_entries, double* c_values, double* c_bound) {
+    if (m < 0 || k < 0) return -1;
+    int bad = 0;
+#pragma omp parallel reduction(| : bad)
+    {
+        int64_t* marker = (int64_t*)malloc((size_t)(k > 0 ? k : 1) * sizeof(int64_t));
+        double* e = (double*)malloc((size_t)(k > 0 ? k : 1) * sizeof(double));
+        double* eb = (double*)malloc((size_t)(k > 0 ? k : 1) * sizeof(double));
+        double* bv = (double*)malloc((size_t)(k > 0 ? k : 1) * sizeof(double));
+        int32_t* cols = (int32_t*)malloc((size_t)(k > 0 ? k : 1) * sizeof(int32_t));
+        if (!marker || !e || !eb || !bv || !cols) bad = 1;
+        if (marker)
+            for (int64_t c = 0; c < k; ++c) marker[c] = -1;
+#pragma omp for schedule(dynamic, 256)
+        for (int64_t i = 0; i < m; ++i) {
+            if (!marker || !e || !eb || !bv || !cols) continue;
+            int64_t len = 0;
+            /* step 1: E(i,:) */
+            for (int64_t p = a_row_map[i]; p < a_row_map[i + 1]; ++p) {
+                int32_t j = a_entries[p];
+                if (j < 0 || j >= m) { bad = 1; continue; }
+                double a = a_values ? a_values[p] : 0.0;
+                for (int64_t q = b_row_map[j]; q < b_row_map[j + 1]; ++q) {
+                    int32_t c = b_entries[q];
+                    if (c < 0 || c >= k) { bad = 1; continue; }
+                    if (marker[c] != i) {
+                        marker[c] = i;
+                        e[c] = 0.0;
+                        eb[c] = 0.0;
+                        bv[c] = 0.0;
+                        cols[len++] = c;
+                    }
+                    if (a_values) {
+                        double b = b_values[q];
+                        double prod = a * b;
+                        e[c] = e[c] + prod;
+                        eb[c] = eb[c] + fabs(a) * fabs(b);
+                    }
+                }
+            }
+            /* B(i,:) joins the pattern (step 3's addition) */
+            for (int64_t q = b_row_map[i]; q < b_row_map[i + 1]; ++q) {
+                int32_t c = b_entries[q];
+                if (c < 0 || c >= k) { bad = 1; continue; }
+                if (marker[c] != i) {
+                    marker[c] = i;
+                    e[c] = 0.0;
+                    eb[c] = 0.0;
+                    bv[c] = 0.0;
+                    cols[len++] = c;
+                }
+                if (b_values) bv[c] = bv[c] + b_values[q];
+            }
+            if (counts) {
+                counts[i] = len;
+                continue;
+            }
+            int64_t base = c_row_map[i];
+            if (len != c_row_map[i + 1] - base) { bad = 1; continue; }
+            qsort(cols, (size_t)len, sizeof(int32_t), cmp_i32);
+            for (int64_t t = 0; t < len; ++t) {
+                int32_t c = cols[t];
+                double f = dinv[i] * e[c];          /* step 2 */
+                c_entries[base + t] = c;
+                c_values[base + t] = bv[c] - omega * f; /* step 3 */
+                if (c_bound) c_bound[base + t] = fabs(bv[c]) + fabs(omega) * fabs(dinv[i]) * eb[c];
+            }
+        }
+        free(marker);
+        free(e);
+        free(eb);
+        free(bv);
+        free(cols);
+    }
+    return bad ? -1 : 0;
+}
+
+int kko_jacobi_counts(int64_t m, int64_t k, const int64_t* a_row_map, const int32_t* a_entries,
+                      const int64_t* b_row_map, const int32_t* b_entries, int64_t* counts) {
+    return jacobi_rows(m, k, a_row_map, a_entries, NULL, b_row_map, b_entries, NULL, 0.0, NULL, counts, NULL,
+                       NULL, NULL, NULL);
+}
+
+int kko_jacobi_fill(int64_t m, int64_t k, const int64_t* a_row_map, const int32_t* a_entries,
+                    const double* a_values, const int64_t* b_row_map, const int32_t* b_entries,
+                    const double* b_values, double omega, const double* dinv, const int64_t* c_row_map,
+                    int32_t* c_entries, double* c_values, double* c_bound) {
+    return jacobi_rows(m, k, a_row_map, a_entries, a_values, b_row_map, b_entries, b_values, omega, dinv, NULL,
+                       c_row_map, c_entries, c_values, c_bound);
+}

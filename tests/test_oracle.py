@@ -270,3 +270,74 @@ def test_compress_roundtrip(oracle_mod):
                 if (int(mm) >> b) & 1:
                     rec.add(int(ww) * 32 + b)
         assert rec == cols
+
+
+# ---- Jacobi-fused SpGEMM reference (Sec. 2.2.2) ----------------------
+
+def _square_with_diag(m, maxr, seed, diag=True):
+    A = g.random_csr(m, m, maxr, seed=seed)
+    D = A.to_dense().numpy()
+    if diag:
+        rng = np.random.default_rng(seed + 7)
+        for i in range(m):
+            D[i, i] = rng.uniform(1.0, 3.0) * (1 if rng.random() < 0.5 else -1)
+    return dense_to_csr(D)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("diag", [True, False])
+def test_jacobi_oracle_vs_dense(oracle_mod, seed, diag):
+    """C = (I - w D^-1 A) B against a dense evaluation of the formula; pattern = the
+    Boolean union of B's and A*B's patterns (pattern(C) = pattern(E) when A's diagonal is
+    stored, PAPER.md:209)."""
+    m, k = 30, 17
+    A = _square_with_diag(m, 6, seed, diag)
+    B = g.random_csr(m, k, 5, seed=seed + 50)
+    rng = np.random.default_rng(seed)
+    dinv = rng.uniform(-2, 2, size=m)
+    w = 0.7
+    rm, ent, val, bnd = oracle_mod.jacobi(w, dinv, A, B)
+    Ad, Bd = A.to_dense().numpy(), B.to_dense().numpy()
+    want = Bd - w * np.diag(dinv) @ (Ad @ Bd)
+    pa = (Ad != 0).astype(float)
+    pb = (Bd != 0).astype(float)
+    pat = ((pa @ pb) + pb) > 0
+    assert np.array_equal(np.diff(rm), pat.sum(1))
+    if diag:
+        rmE, entE, _, _ = oracle_mod.spgemm(A, B)
+        assert np.array_equal(rm, rmE) and np.array_equal(ent, entE)
+    got = csr_to_dense_np(m, k, rm, ent, val)
+    bound = np.abs(Bd) + abs(w) * np.abs(dinv)[:, None] * (np.abs(Ad) @ np.abs(Bd))
+    assert np.all(np.abs(got - want) <= 1e-12 * bound + 1e-300)
+    assert np.allclose(csr_to_dense_np(m, k, rm, ent, bnd), bound, rtol=1e-13, atol=0)
+
+
+def test_jacobi_oracle_special_cases(oracle_mod):
+    """omega = 0 gives B on E's pattern (E-only entries are explicit zeros); A = D with
+    dinv = 1/diag gives (1 - omega) B exactly."""
+    m, k = 12, 9
+    A = _square_with_diag(m, 4, 11)
+    B = g.random_csr(m, k, 4, seed=12)
+    rm, ent, val, _ = oracle_mod.jacobi(0.0, np.ones(m), A, B)
+    got = csr_to_dense_np(m, k, rm, ent, val)
+    assert np.array_equal(got, B.to_dense().numpy())
+    assert len(val) > B.nnz and np.count_nonzero(val) == np.count_nonzero(B.to_dense().numpy())
+    Dg = np.diag([2.0, 4.0, 0.5, 8.0] * 3)
+    rm, ent, val, _ = oracle_mod.jacobi(0.5, 1.0 / np.diag(Dg), dense_to_csr(Dg), B)
+    assert np.array_equal(csr_to_dense_np(m, k, rm, ent, val), 0.5 * B.to_dense().numpy())
+
+
+def test_jacobi_oracle_smoothed_aggregation_1d(oracle_mod):
+    """Textbook smoothed aggregation in 1D: A = tridiag(-1, 2, -1), aggregates of 3 nodes,
+    omega = 2/3, D^-1 = 1/2: each column of (I - w D^-1 A) P is the hat (1/3, 2/3, 1, 2/3, 1/3)
+    around its aggregate (interior aggregates)."""
+    n, na = 30, 10
+    A = np.diag(2.0 * np.ones(n)) - np.diag(np.ones(n - 1), 1) - np.diag(np.ones(n - 1), -1)
+    P = np.zeros((n, na))
+    P[np.arange(n), np.arange(n) // 3] = 1.0
+    rm, ent, val, _ = oracle_mod.jacobi(2.0 / 3.0, np.full(n, 0.5), dense_to_csr(A), dense_to_csr(P))
+    S = csr_to_dense_np(n, na, rm, ent, val)
+    for c in range(1, na - 1):
+        col = S[3 * c - 1: 3 * c + 4, c]
+        assert np.allclose(col, [1 / 3, 2 / 3, 1.0, 2 / 3, 1 / 3], rtol=0, atol=1e-15)
+        assert np.count_nonzero(S[:, c]) == 5
