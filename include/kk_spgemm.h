@@ -149,6 +149,24 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t handle, const kk_csr_t* A, con
 kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t handle, const kk_csr_t* A, const kk_csr_t* B,
                               const void* c_row_map, int32_t* c_entries, void* c_values, void* stream);
 
+/* Jacobi-fused numeric phase (Sec. 2.2.2; Eq. (2) at PAPER.md:209-211):
+ * C = (I - omega D^-1 A) B, i.e. C(i,:) = B(i,:) - omega * dinv[i] * E(i,:) with
+ * E(i,:) = sum_{j in A(i,:)} A(i,j) B(j,:).  Runs after kk_spgemm_symbolic(A, B) -- the
+ * usual symbolic, as in the paper (pattern(C) = pattern(E) because A(i,i) is stored) --
+ * and writes c_entries / c_values exactly like kk_spgemm_numeric.
+ *   omega: the scalar (host); dinv: device, A.nrows values of A.value_type, the entries
+ *   of D^-1 (caller-owned, read only).
+ * Preconditions: A square (A.nrows == A.ncols == B.nrows, else KK_ERR_DIM_MISMATCH);
+ * every row of A stores its diagonal entry -- checked only when
+ * opts.validate = 1 (KK_ERR_INVALID_ARG); without it, entries of B(i,:) outside E(i,:)'s
+ * pattern are dropped.  Rows with nnz(C_i) > 512 (the dense tiers) are not supported yet:
+ * KK_ERR_UNSUPPORTED_TYPE.  Per row the kernel forms -omega * dinv[i] once, scales E(i,:)
+ * by it and inserts B(i,:) into the accumulator (the paper's fusion).
+ * Asynchronous on `stream` (the validate check synchronises it). */
+kk_status_t kk_spgemm_jacobi_numeric(kk_spgemm_handle_t handle, double omega, const void* dinv, const kk_csr_t* A,
+                                     const kk_csr_t* B, const void* c_row_map, int32_t* c_entries, void* c_values,
+                                     void* stream);
+
 /* Per-kernel device times (opts.timing = 1).  One record per kernel (or fixed group of
  * launches, e.g. the three launches of a scan), accumulated since the last
  * kk_spgemm_timing_reset: number of launches, total and maximum duration in ms, from

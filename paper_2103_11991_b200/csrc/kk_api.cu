@@ -103,7 +103,7 @@ struct kk_spgemm_handle_s {
     long long launches = 0;
     // workspace
     Buf flops, fscan, binid, perm_sym, perm_num, counts, binscratch, binstart, bc_len, pairs, cursors, partial,
-        status, bmeta, wlo, pat, pat_off, pat_len;
+        status, bmeta, wlo, pat, pat_off, pat_len, diagchk;
     DevStatus* h_status = nullptr;  // pinned
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -510,8 +510,8 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     return KK_OK;
 }
 
-kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, const void* c_row_map,
-                              int32_t* c_entries, void* c_values, void* stream) {
+static kk_status_t numeric_impl(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, const void* c_row_map,
+                                int32_t* c_entries, void* c_values, void* stream, const void* dinv, double omega) {
     if (!h) return KK_ERR_INVALID_ARG;
     kk_status_t st;
     if ((st = check_pair(h, A, B, true)) != KK_OK) return st;
@@ -545,8 +545,26 @@ kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
     na.cursors = (int32_t*)h->cursors.p;
     na.st = (const DevStatus*)h->status.p;
     na.logG = pick_logG(B->nrows > 0 ? (double)B->nnz / (double)B->nrows : 1.0);
+    na.dinv = dinv;
+    na.omega = omega;
     cudaStream_t side = nullptr;
     const bool dense = h->host_num_bin_start[kk::NUM_DENSE_BIN + 1] > h->host_num_bin_start[kk::NUM_DENSE_BIN];
+    if (dinv) {
+        if (dense)
+            return fail(h, KK_ERR_UNSUPPORTED_TYPE,
+                        "jacobi numeric: %d rows with nnz(C_i) > 512 need the dense tiers, which have no Jacobi form yet",
+                        h->host_num_bin_start[kk::NUM_DENSE_BIN + 1] - h->host_num_bin_start[kk::NUM_DENSE_BIN]);
+        if (h->opts.validate) {
+            int missing = 0;
+            if ((st = ensure(h, h->diagchk, sizeof(int), s)) != KK_OK) return st;
+            if (!kk::check_diagonal(L, A->offset_type == KK_I64, A->nrows, A->row_map, A->entries, (int*)h->diagchk.p,
+                                    &missing))
+                return fail(h, KK_ERR_CUDA, "jacobi numeric: diagonal check failed");
+            if (missing)
+                return fail(h, KK_ERR_INVALID_ARG, "jacobi numeric: A(i,i) is not stored in %d rows (PAPER.md:194)",
+                            missing);
+        }
+    }
     if (h->side && dense) {
         cudaEventRecord(h->ev_fork, s);
         cudaStreamWaitEvent(h->side, h->ev_fork, 0);
@@ -558,6 +576,23 @@ kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
         cudaStreamWaitEvent(s, h->ev_join, 0);
     }
     return cuda_check(h, cudaGetLastError(), "kk_spgemm_numeric launch");
+}
+
+kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, const void* c_row_map,
+                              int32_t* c_entries, void* c_values, void* stream) {
+    return numeric_impl(h, A, B, c_row_map, c_entries, c_values, stream, nullptr, 0.0);
+}
+
+kk_status_t kk_spgemm_jacobi_numeric(kk_spgemm_handle_t h, double omega, const void* dinv, const kk_csr_t* A,
+                                     const kk_csr_t* B, const void* c_row_map, int32_t* c_entries, void* c_values,
+                                     void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    if (!A || !B) return fail(h, KK_ERR_INVALID_ARG, "A or B is NULL");
+    if (A->nrows != A->ncols || B->nrows != A->nrows)
+        return fail(h, KK_ERR_DIM_MISMATCH, "jacobi numeric: A must be m x m and B m x k (A %lld x %lld, B %lld rows)",
+                    (long long)A->nrows, (long long)A->ncols, (long long)B->nrows);
+    if (!dinv && A->nrows > 0) return fail(h, KK_ERR_INVALID_ARG, "jacobi numeric: dinv is NULL");
+    return numeric_impl(h, A, B, c_row_map, c_entries, c_values, stream, dinv ? dinv : (const void*)h, omega);
 }
 
 kk_status_t kk_spgemm_kernel_times(kk_spgemm_handle_t h, kk_kernel_time_t* out, int* count_inout) {

@@ -150,7 +150,14 @@ struct NumArgs {
     const uint2* pat;            // row patterns (see PatOut)
     const long long* pat_off;
     const int* pat_len;
+    // Jacobi-fused numeric: C = (I - omega D^-1 A) B when dinv != null
+    const void* dinv = nullptr;  // device, A.nrows values of the value type
+    double omega = 0.0;
 };
 void numeric_bins(Launch& L, const NumArgs& a, cudaStream_t dense_stream);
+// validate for the Jacobi-fused numeric: *missing (host) = rows of the square A without a
+// stored diagonal entry; scratch: one device int.  Synchronises L.stream.  false on a CUDA error.
+bool check_diagonal(Launch& L, bool off64, int64_t m, const void* row_map, const int32_t* entries, int* scratch,
+                    int* missing);
 
 }  // namespace kk

@@ -18,7 +18,8 @@ __global__ void __launch_bounds__(256, 1) k_num_warp(const OffT* __restrict__ ar
                                                   const OffT* __restrict__ crm, int32_t* __restrict__ cent,
                                                   ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                   const int* __restrict__ bin_start, int bin, int logG,
-                                                  const DevStatus* __restrict__ st) {
+                                                  const DevStatus* __restrict__ st, const ValT* __restrict__ dinv,
+                                                  double omega) {
     extern __shared__ __align__(16) unsigned char sm_num[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     constexpr size_t WB = (size_t)S * sizeof(ValT) + (size_t)S * 4 + (size_t)S * 2;
@@ -59,6 +60,19 @@ __global__ void __launch_bounds__(256, 1) k_num_warp(const OffT* __restrict__ ar
             if (plain) __syncwarp();
         }
         __syncwarp();
+        if (dinv) {
+            // Jacobi-fused row: C(i,:) = B(i,:) - omega D^-1(i) E(i,:)
+            const ValT sc = (ValT)(-omega * (double)__ldg(dinv + i));
+            for (int t = lane; t < S; t += 32) vals[t] *= sc;
+            __syncwarp();
+            const int64_t bs = ld(brm, i), be = ld(brm, i + 1);
+            for (int64_t q = bs + lane; q < be; q += 32) {
+                bool fresh;
+                const uint32_t h = probe_claim<S>(keys, (uint32_t)__ldg(bent + q), &fresh);
+                atomicAdd(&vals[h], __ldg(bval + q));
+            }
+            __syncwarp();
+        }
         // compaction (slot order) into stage: keys when sorting, slots otherwise
         int n = 0;
 #pragma unroll 4
@@ -455,7 +469,8 @@ __global__ void __launch_bounds__(256, 1) k_num_strict(const OffT* __restrict__ 
                                                     const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
                                                     const OffT* __restrict__ crm, int32_t* __restrict__ cent,
                                                     ValT* __restrict__ cval, const int32_t* __restrict__ perm,
-                                                    const int* __restrict__ bin_start, int bin) {
+                                                    const int* __restrict__ bin_start, int bin,
+                                                    const ValT* __restrict__ dinv, double omega) {
     using LY = StrictLayout<ValT, S, CAP>;
     constexpr int LOGS = ilog2(S);
     constexpr int E = CAP / 32;  // sort elements per lane
@@ -496,6 +511,21 @@ __global__ void __launch_bounds__(256, 1) k_num_strict(const OffT* __restrict__ 
                                      const uint32_t h = strict_claim<S>(keys, col, act);
                                      if (act) vals[h] += prod;
                                  });
+        if (dinv) {
+            // Jacobi-fused row: scale E(i,:) by -omega D^-1(i), insert B(i,:)
+            __syncwarp();
+            const ValT sc = (ValT)(-omega * (double)__ldg(dinv + i));
+            for (int t = lane; t < S; t += 32) vals[t] *= sc;
+            __syncwarp();
+            const int64_t bs = ld(brm, i), be = ld(brm, i + 1);
+            for (int64_t q0 = bs; q0 < be; q0 += 32) {
+                const bool act = q0 + lane < be;
+                const uint32_t col = act ? (uint32_t)__ldg(bent + q0 + lane) : EMPTY;
+                const uint32_t h = strict_claim<S>(keys, col, act);
+                if (act) vals[h] += __ldg(bval + q0 + lane);
+                __syncwarp();
+            }
+        }
         // next row's bounds (their loads overlap the epilogue)
         int64_t sn = 0, en = 0;
         if (inext >= 0) {
@@ -645,7 +675,8 @@ __global__ void __launch_bounds__(256, MINB) k_num_pattern(const OffT* __restric
                                                      ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                      const int* __restrict__ bin_start, int bin,
                                                      const uint2* __restrict__ pat, const long long* __restrict__ pat_off,
-                                                     const int* __restrict__ pat_len) {
+                                                     const int* __restrict__ pat_len, const ValT* __restrict__ dinv,
+                                                     double omega) {
     using LY = PatLayout<ValT, CAP>;
     extern __shared__ __align__(16) unsigned char sm_pat[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
@@ -763,6 +794,29 @@ __global__ void __launch_bounds__(256, MINB) k_num_pattern(const OffT* __restric
                                               __syncwarp();
                                           });
         }
+        if (dinv) {
+            // Jacobi-fused row: scale E(i,:) by -omega D^-1(i), add B(i,:)
+            __syncwarp();
+            const ValT sc = (ValT)(-omega * (double)__ldg(dinv + i));
+            for (int t = lane; t < min(clen, CAP); t += 32) vals[t] *= sc;
+            __syncwarp();
+            const int64_t bs = ld(brm, i), be = ld(brm, i + 1);
+            for (int64_t q0 = bs; q0 < be; q0 += 32) {
+                if (q0 + lane < be) {
+                    const uint32_t col = (uint32_t)__ldg(bent + q0 + lane);
+                    const ValT bv = __ldg(bval + q0 + lane);
+                    if constexpr (DENSE) {
+                        acc(mp_rank(sm_pat[o_idx + (col >> 5)], col), bv);
+                    } else {
+                        const uint32_t w = col >> 5;
+                        uint32_t wi = wt_slot(w);
+                        while (wkeys[wi] != w) wi = (wi + 1) & (PAT_SW - 1);
+                        acc(mp_rank(wi, col), bv);
+                    }
+                }
+                __syncwarp();
+            }
+        }
         int64_t sn = 0, en = 0;
         if (inext >= 0) {
             sn = ld(arm, inext);
@@ -825,7 +879,8 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                                                         ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                         const int* __restrict__ bin_start, int bin,
                                                         const uint2* __restrict__ pat, const long long* __restrict__ pat_off,
-                                                        const int* __restrict__ pat_len) {
+                                                        const int* __restrict__ pat_len, const ValT* __restrict__ dinv,
+                                                        double omega) {
     using LY = RankLayout<ValT, CAP>;
     extern __shared__ __align__(16) unsigned char sm_rank[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
@@ -959,6 +1014,25 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
             }
             __syncwarp();
         }
+        if (dinv) {
+            // Jacobi-fused row: C(i,:) = B(i,:) - omega D^-1(i) E(i,:).
+            // E(i,:) is scaled once per entry by the row's scalar, then B(i,:) is added at
+            // its ranks (its columns lie in E's pattern when A(i,i) is stored).
+            const ValT sc = (ValT)(-omega * (double)__ldg(dinv + i));
+            for (int t = lane; t < clen; t += 32) *(ValT*)(sm_rank + o_val + (uint32_t)t * (uint32_t)sizeof(ValT)) *= sc;
+            __syncwarp();
+            const int bs = (int)ld(brm, i), bl = (int)(ld(brm, i + 1) - bs);
+            for (int q0 = 0; q0 < bl; q0 += 32) {
+                const bool valid = q0 + lane < bl;
+                const int q = bs + min(q0 + lane, bl - 1);
+                const int col = __ldg(bent + q);
+                uint32_t rk = rank(col, valid);
+                // a column outside the pattern (A(i,i) not stored) must not land on another rank
+                if (rk < (uint32_t)CAP && *(const int32_t*)(sm_rank + o_col + rk * 4u) != col) rk = CAP;
+                acc(rk, __ldg(bval + q));
+                __syncwarp();
+            }
+        }
         // ---- entries and values, coalesced; reset ----
         for (int t = lane; t < clen; t += 32) {
             cent[cb + t] = *(const int32_t*)(sm_rank + o_col + (uint32_t)t * 4u);
@@ -1003,7 +1077,7 @@ static void launch_num_rank(Launch& L, const NumArgs& a, int bin) {
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                                (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
-                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len);
+                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len, (const ValT*)a.dinv, a.omega);
     L.end(L.stream);
 }
 
@@ -1035,7 +1109,7 @@ static void launch_num_pattern(Launch& L, const NumArgs& a, int bin) {
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                                (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
-                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len);
+                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len, (const ValT*)a.dinv, a.omega);
     L.end(L.stream);
 }
 
@@ -1056,7 +1130,7 @@ static void launch_num_strict_f(Launch& L, const NumArgs& a, int bin) {
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                                (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
-                                               a.bin_start, bin);
+                                               a.bin_start, bin, (const ValT*)a.dinv, a.omega);
     L.end(L.stream);
 }
 
@@ -1241,7 +1315,7 @@ static void launch_num_warp(Launch& L, const NumArgs& a, int bin) {
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                                (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
-                                               a.bin_start, bin, a.logG, a.st);
+                                               a.bin_start, bin, a.logG, a.st, (const ValT*)a.dinv, a.omega);
     L.end(L.stream);
 }
 

@@ -633,4 +633,40 @@ void bin_rows(Launch& L, int64_t m, const uint8_t* binid, int32_t* scratch, int3
     L.end(L.stream, 3);
 }
 
+// ------------------------------------------------------------------------------------
+// Jacobi-fused numeric precondition ("all of its diagonal entries have
+// nonzero values"): count rows of A without a stored A(i,i).  Validate mode only.
+// ------------------------------------------------------------------------------------
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_check_diag(int64_t m, const OffT* __restrict__ arm,
+                                                    const int32_t* __restrict__ aent, int* __restrict__ missing) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int miss = 0;
+    for (int64_t i = gw; i < m; i += nw) {
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        bool found = false;
+        for (int64_t p = s + lane; p < e; p += 32) found |= __ldg(aent + p) == (int32_t)i;
+        miss += __any_sync(FULL, found) ? 0 : 1;
+    }
+    if (lane == 0 && miss) atomicAdd(missing, miss);
+}
+
+bool check_diagonal(Launch& L, bool off64, int64_t m, const void* row_map, const int32_t* entries, int* scratch,
+                    int* missing) {
+    *missing = 0;
+    if (m == 0) return true;
+    cudaMemsetAsync(scratch, 0, sizeof(int), L.stream);
+    const int grid = (int)std::min<int64_t>((m * 32 + 255) / 256, (int64_t)L.num_sms * 8);
+    L.begin("check_diag", L.stream);
+    if (off64)
+        k_check_diag<int64_t><<<grid, 256, 0, L.stream>>>(m, (const int64_t*)row_map, entries, scratch);
+    else
+        k_check_diag<int32_t><<<grid, 256, 0, L.stream>>>(m, (const int32_t*)row_map, entries, scratch);
+    L.end(L.stream);
+    cudaMemcpyAsync(missing, scratch, sizeof(int), cudaMemcpyDeviceToHost, L.stream);
+    return cudaStreamSynchronize(L.stream) == cudaSuccess;
+}
+
 }  // namespace kk

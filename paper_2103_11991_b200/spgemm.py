@@ -126,6 +126,33 @@ class SpGEMM:
                                c_values.data_ptr() if nnz else 0, _stream_ptr(self.device, stream))
         return c_entries, c_values
 
+    def jacobi_numeric(self, omega: float, dinv: torch.Tensor, A, B, c_row_map: torch.Tensor,
+                       nnz: Optional[int] = None, c_entries: Optional[torch.Tensor] = None,
+                       c_values: Optional[torch.Tensor] = None, stream=None):
+        """Jacobi-fused numeric C = (I - omega D^-1 A) B after
+        symbolic(A, B); dinv: device vector of D^-1 (A's value dtype)."""
+        A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
+        a, b = _kk_csr(A, True), _kk_csr(B, True)
+        if nnz is None:
+            nnz = self.stats()["nnz_c"]
+        if dinv.dtype != A.values.dtype or dinv.device != A.values.device or not dinv.is_contiguous():
+            raise ValueError("dinv must be a contiguous device vector of A's value dtype")
+        if c_entries is None:
+            c_entries = torch.empty(nnz, dtype=torch.int32, device=A.row_map.device)
+        if c_values is None:
+            c_values = torch.empty(nnz, dtype=A.values.dtype, device=A.row_map.device)
+        _ffi.kk_spgemm_jacobi_numeric(self._h, omega, dinv.data_ptr() if A.nrows else 0, a, b, c_row_map.data_ptr(),
+                                      c_entries.data_ptr() if nnz else 0, c_values.data_ptr() if nnz else 0,
+                                      _stream_ptr(self.device, stream))
+        return c_entries, c_values
+
+    def jacobi(self, omega: float, dinv: torch.Tensor, A, B, stream=None) -> CsrMatrix:
+        """Both phases of the Jacobi-fused product (usual symbolic, fused numeric)."""
+        A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
+        rm, nnz = self.symbolic(A, B, stream=stream)
+        ent, val = self.jacobi_numeric(omega, dinv, A, B, rm, nnz=nnz, stream=stream)
+        return CsrMatrix(A.nrows, B.ncols, rm, ent, val)
+
     def __call__(self, A, B, stream=None) -> CsrMatrix:
         A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
         rm, nnz = self.symbolic(A, B, stream=stream)
@@ -239,6 +266,17 @@ def spgemm(A, B, **opts) -> CsrMatrix:
     h = SpGEMM(**opts)
     try:
         return h(A, B)
+    finally:
+        torch.cuda.current_stream(h.device).synchronize()
+        h.close()
+
+
+def spgemm_jacobi(omega: float, dinv: torch.Tensor, A, B, **opts) -> CsrMatrix:
+    """One-shot Jacobi-fused product C = (I - omega D^-1 A) B on the device
+    (PAPER.md:188-217): usual symbolic, fused numeric."""
+    h = SpGEMM(**opts)
+    try:
+        return h.jacobi(omega, dinv, A, B)
     finally:
         torch.cuda.current_stream(h.device).synchronize()
         h.close()

@@ -419,7 +419,22 @@ CONFIGS = {
     "C3": "Galerkin R*A*P, 3D 7-point Laplacian 128^3, 3x3x3 aggregation P, R=P^T",
     "C4": "A*A, RMAT scale 20, edge factor 16, directed",
     "C5": "A*A, 3D 27-point block stencil, 3 dof/node, 160^3",
+    "C3J": "Jacobi-fused (I - w D^-1 A) P: smoothed-aggregation prolongator, 7-point 128^3, 3x3x3 aggregates",
 }
+
+
+def diagonal_inverse(A: CSR) -> torch.Tensor:
+    """D^-1 of a square CSR matrix (input preparation for the Jacobi-fused product,
+    PAPER.md:192: "D^-1 represents the inverse of the diagonal matrix of A"): 1 / A(i,i),
+    summed over duplicate diagonal entries; rows without a stored diagonal get 0."""
+    rm = A.row_map.to(torch.int64).cpu()
+    rows = torch.repeat_interleave(torch.arange(A.nrows, dtype=torch.int64), rm[1:] - rm[:-1])
+    ent = A.entries.cpu().to(torch.int64)
+    d = torch.zeros(A.nrows, dtype=torch.float64)
+    on = ent == rows
+    d.index_add_(0, rows[on], A.values.cpu().to(torch.float64)[on])
+    out = torch.where(d != 0, 1.0 / torch.where(d != 0, d, torch.ones_like(d)), torch.zeros_like(d))
+    return out.to(A.values.device)
 
 
 def config(name: str, size: Optional[int] = None, values: str = "int", seed: int = 1, device="cpu"):
@@ -439,6 +454,12 @@ def config(name: str, size: Optional[int] = None, values: str = "int", seed: int
         P = aggregation_prolongator(n, values=values, seed=seed + 1, device=device)
         R = transpose(P)
         return A, P, R
+    elif name == "C3J":
+        # smoothed-aggregation prolongator: returns (A, P, dinv, omega)
+        n = size or 128
+        A = laplacian_3d_7pt(n, values=values, seed=seed, device=device)
+        P = aggregation_prolongator(n, values=values, seed=seed + 1, device=device)
+        return A, P, diagonal_inverse(A), 2.0 / 3.0
     elif name == "C4":
         A = rmat(scale=size or 20, edge_factor=16, seed=seed, values=values, device=device)
     elif name == "C5":
