@@ -46,6 +46,7 @@ WORKLOADS = {
     "C3": "Galerkin R*(A*P): 3D 7-point Laplacian 128^3, 3x3x3 aggregation P, R = P^T (two products)",
     "C4": "A*A RMAT scale 20, edge factor 16, directed (1,048,576 rows)",
     "C5": "A*A 3D 27-point block stencil, 3 dof/node, 160^3 (12,288,000 rows)",
+    "C3J": "Jacobi-fused (I - w D^-1 A) P: 3D 7-point Laplacian 128^3, 3x3x3 aggregation P, w = 2/3 (NEXT-1)",
 }
 
 
@@ -315,13 +316,18 @@ def run_ours(args):
     def conv(M):
         return CsrMatrix(M.nrows, M.ncols, M.row_map.to(odt), M.entries, M.values.to(vdt))
 
+    jac = None
     if world == 1:
-        mats = [conv(M) for M in make_workload(args.config, args.size, args.values, dev)]
+        wl = make_workload(args.config, args.size, args.values, dev)
+        if args.config == "C3J":  # (A, P, dinv, omega)
+            jac = (wl[3], wl[2].to(vdt))
+            wl = wl[:2]
+        mats = [conv(M) for M in wl]
         A, B = mats[0], mats[1]
         r0, r1 = 0, A.nrows
     else:
-        if args.config == "C3":
-            raise SystemExit("C3 (two chained products) is benchmarked on one GPU")
+        if args.config in ("C3", "C3J"):
+            raise SystemExit(f"{args.config} is benchmarked on one GPU")
         from paper_2103_11991_b200.parallel import broadcast_csr, flop_balanced_cuts, slice_rows
 
         if rank == 0:
@@ -351,8 +357,8 @@ def run_ours(args):
     class Product:
         """One C = X*Y of the step: its handle, row map and preallocated C arrays."""
 
-        def __init__(self, X, Y):
-            self.X, self.Y = X, Y
+        def __init__(self, X, Y, jacobi=None):
+            self.X, self.Y, self.jacobi = X, Y, jacobi
             self.h = SpGEMM(device=dev, timing=True, num_streams=args.streams)
             self.crm = torch.empty(X.nrows + 1, dtype=odt, device=dev)
             _, n = self.h.symbolic(X, Y, c_row_map=self.crm)
@@ -364,7 +370,7 @@ def run_ours(args):
             return CsrMatrix(self.X.nrows, self.Y.ncols, self.crm, self.cent[:self.nnz], self.cval[:self.nnz])
 
     # the step's products: A*B, or for C3 T = A*P then Ac = R*T (T stays in HBM)
-    prods = [Product(A, B)]
+    prods = [Product(A, B, jac)]
     if args.config == "C3":
         prods.append(Product(mats[2], prods[0].C()))
     nnz_all = torch.zeros(world, dtype=torch.int64, device=dev)
@@ -379,7 +385,11 @@ def run_ours(args):
                 dist.all_gather_into_tensor(nnz_all, mine)
             if ev is not None:
                 ev[2 * k + 1].record(stream)
-            pr.h.numeric(pr.X, pr.Y, pr.crm, nnz=n, c_entries=pr.cent[:n], c_values=pr.cval[:n])
+            if pr.jacobi is not None:
+                pr.h.jacobi_numeric(pr.jacobi[0], pr.jacobi[1], pr.X, pr.Y, pr.crm, nnz=n, c_entries=pr.cent[:n],
+                                    c_values=pr.cval[:n])
+            else:
+                pr.h.numeric(pr.X, pr.Y, pr.crm, nnz=n, c_entries=pr.cent[:n], c_values=pr.cval[:n])
         if ev is not None:
             ev[2 * len(prods)].record(stream)
 
@@ -482,6 +492,8 @@ def run_ours(args):
         nnz * (4 + val_size) + (prods[-1].X.nrows + 1) * 8
     if args.no_e2e:
         e2e = None
+    elif jac is not None:
+        e2e = {"value": None, "unit": UNIT, "skipped": "C3J: the host-buffer path covers the plain product only"}
     elif host_bytes > 48e9:
         e2e = {"value": None, "unit": UNIT, "skipped": f"inputs + C = {host_bytes / 1e9:.0f} GB of pinned host memory"}
     else:
@@ -541,6 +553,8 @@ def run_ours(args):
         cpu = cpu_baseline(A, B, args.cpu_seconds, rows)
         if args.config == "C3":
             cpu["sample"] = "first product T = A*P only: " + cpu["sample"]
+        if args.config == "C3J":
+            cpu["sample"] = "plain E = A*P (the oracle's usual product): " + cpu["sample"]
 
     if rank == 0:
         out = {"metric": METRIC, "value": round(gflops, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
