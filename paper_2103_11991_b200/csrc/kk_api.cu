@@ -464,7 +464,8 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     // pattern rows only where the numeric walks B rows of ~11+ entries one per warp step
     const bool use_pat = keep_pat && pick_logG(n > 0 ? (double)B->nnz / (double)n : 1.0) >= 4;
     kk::numeric_binid(L, m, (const int32_t*)h->counts.p, use_pat ? (const long long*)h->pat_off.p : nullptr,
-                      (const int*)h->pat_len.p, (const uint2*)h->pat.p, (uint8_t*)h->binid.p, dst);
+                      (const int*)h->pat_len.p, (const uint2*)h->pat.p, (const int64_t*)h->flops.p,
+                      (uint8_t*)h->binid.p, dst);
     kk::bin_rows(L, m, (const uint8_t*)h->binid.p, (int32_t*)h->binscratch.p, (int32_t*)h->perm_num.p, num_start);
     // copy bin starts next to the status block, then the single device->host read
     cudaMemcpyAsync(dst->sym_bin_start, sym_start, sizeof(int) * (kk::NB + 1), cudaMemcpyDeviceToDevice, s);

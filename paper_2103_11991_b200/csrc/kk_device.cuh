@@ -252,4 +252,66 @@ __device__ __forceinline__ uint32_t strict_find(const uint32_t* keys, uint32_t c
     return h;
 }
 
+// ------------------------------------------------------------------------------------
+// a5/a7 for tiny rows (flops_i <= TINY_MAX, so nnz(C_i) <= TINY_MAX): a lane owns a row
+// and keeps its distinct columns (and values: accum = +) in a register list
+// -- the paper's accumulator reduced to K registers.  Insert = unrolled compare against
+// all K slots (empty slots hold INT_MAX, never a column); the row is sorted by an
+// odd-even transposition network before it is written.
+// ------------------------------------------------------------------------------------
+template <int K, typename ValT, bool VALUES>
+struct TinyList {
+    int cols[K];
+    ValT vals[K];
+    int n;
+    __device__ __forceinline__ TinyList() : n(0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            cols[k] = INT_MAX;
+            vals[k] = (ValT)0;
+        }
+    }
+    __device__ __forceinline__ void insert(int c, ValT v) {
+        bool found = false;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (cols[k] == c) {
+                if (VALUES) vals[k] += v;
+                found = true;
+            }
+        }
+        if (!found && n < K) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (k == n) {
+                    cols[k] = c;
+                    if (VALUES) vals[k] = v;
+                }
+            }
+            ++n;
+        }
+    }
+    __device__ __forceinline__ void scale(ValT s) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) vals[k] *= s;
+    }
+    __device__ __forceinline__ void sort() {
+#pragma unroll
+        for (int rnd = 0; rnd < K; ++rnd) {
+#pragma unroll
+            for (int k = rnd & 1; k + 1 < K; k += 2) {
+                const bool sw = cols[k] > cols[k + 1];
+                const int c0 = cols[k], c1 = cols[k + 1];
+                cols[k] = sw ? c1 : c0;
+                cols[k + 1] = sw ? c0 : c1;
+                if (VALUES) {
+                    const ValT v0 = vals[k], v1 = vals[k + 1];
+                    vals[k] = sw ? v1 : v0;
+                    vals[k + 1] = sw ? v0 : v1;
+                }
+            }
+        }
+    }
+};
+
 }  // namespace kk

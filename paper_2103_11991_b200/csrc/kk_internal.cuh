@@ -7,7 +7,7 @@
 
 namespace kk {
 
-constexpr int NB = 16;                       // max work bins per phase
+constexpr int NB = 18;                       // max work bins per phase
 constexpr uint32_t EMPTY = 0xffffffffu;      // empty hash slot (column indices are < 2^31)
 
 // Symbolic bins (by an upper bound ub_i of distinct keys of row i):
@@ -19,7 +19,10 @@ constexpr int SYM_DENSE_BIN = 8;
 // W = 8K, 16K, 32K, 48K, 64K bits (sorted B only; the window comes from the first/last
 // column of each B row, "bit vector for symbolic")
 constexpr int SYM_WIN_BIN0 = 9;
-constexpr int SYM_NBINS = 14;
+// 14: tiny rows (flops_i <= TINY_MAX): a lane owns a row, its columns in registers
+constexpr int SYM_TINY_BIN = 14;
+constexpr int SYM_NBINS = 15;
+constexpr int TINY_MAX = 16;
 // Numeric bins (by exact nnz(C_i)):
 //   0: empty; b = 1..5: warp-owned shared hash with S = 32 << b slots (nnz <= S/2);
 //   6: CTA-owned dense scalar window (column-windowed dense accumulator).
@@ -32,7 +35,9 @@ constexpr int NUM_DENSE_BIN = 6;
 constexpr int NUM_PAT_BIN0 = 7;
 constexpr int NUM_PATH_BIN0 = 12;
 constexpr int PAT_DENSE_WORDS = 2048;  // widest word span of a pattern with a dense word index
-constexpr int NUM_NBINS = 16;
+//   16: tiny rows (flops_i <= TINY_MAX), lane-owned register lists
+constexpr int NUM_TINY_BIN = 16;
+constexpr int NUM_NBINS = 17;
 
 // Device-side status block.  Written by the kernels, copied to pinned host memory
 // once at the end of the symbolic phase (the phase's only device->host sync).
@@ -106,8 +111,9 @@ void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out,
                     unsigned long long* total_dst, int* overflow);
 // pat_off (may be null): rows with a stored pattern (and strictly sorted B) go to the
 // pattern bins NUM_PAT_BIN0 + (b - 1)
+// flops (may be null): rows with flops_i <= TINY_MAX go to NUM_TINY_BIN
 void numeric_binid(Launch& L, int64_t m, const int32_t* counts, const long long* pat_off, const int* pat_len,
-                   const uint2* pat, uint8_t* binid, const DevStatus* st);
+                   const uint2* pat, const int64_t* flops, uint8_t* binid, const DevStatus* st);
 // stable binning of rows by binid: perm lists rows of bin 0, then bin 1, ...
 // (each bin in increasing row order); bin_start_dst (device int[NB+1]).
 int64_t bin_scratch_len(int64_t m);

@@ -1319,6 +1319,63 @@ static void launch_num_warp(Launch& L, const NumArgs& a, int bin) {
     L.end(L.stream);
 }
 
+// a7 + a8 for tiny rows (flops_i <= TINY_MAX): a lane owns a row; columns and values in a
+// register list (TinyList, accum = +), sorted by a transposition network and
+// written to the row.  Jacobi-fused: E(i,:) scaled by -omega D^-1(i),
+// then B(i,:) inserted.
+template <typename OffT, typename ValT>
+__global__ void __launch_bounds__(256) k_num_tiny(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                  const ValT* __restrict__ aval, const OffT* __restrict__ brm,
+                                                  const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                                  const OffT* __restrict__ crm, int32_t* __restrict__ cent,
+                                                  ValT* __restrict__ cval, const int32_t* __restrict__ perm,
+                                                  const int* __restrict__ bin_start, int bin,
+                                                  const ValT* __restrict__ dinv, double omega) {
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    for (int r = r0 + blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += gridDim.x * blockDim.x) {
+        const int i = perm[r];
+        TinyList<TINY_MAX, ValT, true> T;
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        for (int64_t p = s; p < e; ++p) {
+            const int j = __ldg(aent + p);
+            const ValT a = __ldg(aval + p);
+            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+            for (int64_t q = bs; q < be; ++q) T.insert(__ldg(bent + q), a * __ldg(bval + q));
+        }
+        if (dinv) {
+            T.scale((ValT)(-omega * (double)__ldg(dinv + i)));
+            const int64_t bs = ld(brm, i), be = ld(brm, i + 1);
+            for (int64_t q = bs; q < be; ++q) T.insert(__ldg(bent + q), __ldg(bval + q));
+        }
+        T.sort();
+        const int64_t cb = ld(crm, i);
+        const int clen = (int)(ld(crm, i + 1) - cb);
+        const int nn = min(T.n, clen);
+#pragma unroll
+        for (int k = 0; k < TINY_MAX; ++k) {
+            if (k < nn) {
+                cent[cb + k] = T.cols[k];
+                cval[cb + k] = T.vals[k];
+            }
+        }
+    }
+}
+
+template <typename OffT, typename ValT>
+static void launch_num_tiny(Launch& L, const NumArgs& a) {
+    const int rows = a.host_bin_start[NUM_TINY_BIN + 1] - a.host_bin_start[NUM_TINY_BIN];
+    if (rows <= 0) return;
+    auto kern = k_num_tiny<OffT, ValT>;
+    KCfg c = kernel_cfg(kern, 256, 0, L.num_sms);
+    const int grid = (int)std::min<int64_t>((rows + 255) / 256, c.grid_cap);
+    L.begin("num_tiny", L.stream);
+    kern<<<grid, 256, 0, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
+                                     (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
+                                     (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm, a.bin_start,
+                                     NUM_TINY_BIN, (const ValT*)a.dinv, a.omega);
+    L.end(L.stream);
+}
+
 template <typename OffT, typename ValT, bool SORT>
 static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_stream) {
     const int drows = a.host_bin_start[NUM_DENSE_BIN + 1] - a.host_bin_start[NUM_DENSE_BIN];
@@ -1353,6 +1410,7 @@ static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_strea
                                          NUM_DENSE_BIN, a.k, (int)W, a.cursors, a.st);
         L.end(s);
     }
+    launch_num_tiny<OffT, ValT>(L, a);
     if (a.pat) {
         launch_num_pattern<OffT, ValT, 512, true>(L, a, NUM_PAT_BIN0 + 4);
         launch_num_pattern<OffT, ValT, 256, true>(L, a, NUM_PAT_BIN0 + 3);

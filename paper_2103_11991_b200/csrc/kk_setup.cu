@@ -311,7 +311,9 @@ __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t
             flops[i] = acc.f;
             const int64_t ub = comp ? min(acc.fc, kw) : min(acc.f, k);
             int b = sym_bin_of(ub);
-            if (win && b > 0) {
+            if (acc.f > 0 && acc.f <= TINY_MAX) {
+                b = SYM_TINY_BIN;  // lane-owned register list (TinyList)
+            } else if (win && b > 0) {
                 const int wbn = sym_win_bin_of(acc.lo, acc.hi, ub);
                 if (wbn) {
                     b = wbn;
@@ -500,10 +502,15 @@ __device__ __forceinline__ int num_bin_of(int64_t nnz) {
 __global__ void __launch_bounds__(256) k_numeric_binid(int64_t m, const int32_t* __restrict__ counts,
                                                        const long long* __restrict__ pat_off,
                                                        const int* __restrict__ pat_len, const uint2* __restrict__ pat,
+                                                       const int64_t* __restrict__ flops,
                                                        uint8_t* __restrict__ binid, const DevStatus* st) {
     const bool use_pat = pat_off != nullptr && st->b_strict != 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         int b = num_bin_of(counts[i]);
+        if (b > 0 && flops && flops[i] <= TINY_MAX) {
+            binid[i] = (uint8_t)NUM_TINY_BIN;
+            continue;
+        }
         if (use_pat && b >= 1 && b <= NUM_WARP_BINS) {
             const long long o = pat_off[i];
             if (o >= 0) {
@@ -517,11 +524,11 @@ __global__ void __launch_bounds__(256) k_numeric_binid(int64_t m, const int32_t*
 }
 
 void numeric_binid(Launch& L, int64_t m, const int32_t* counts, const long long* pat_off, const int* pat_len,
-                   const uint2* pat, uint8_t* binid, const DevStatus* st) {
+                   const uint2* pat, const int64_t* flops, uint8_t* binid, const DevStatus* st) {
     if (m == 0) return;
     int grid = (int)std::min<int64_t>((m + 255) / 256, (int64_t)L.num_sms * 16);
     L.begin("numeric_binid", L.stream);
-    k_numeric_binid<<<grid, 256, 0, L.stream>>>(m, counts, pat_off, pat_len, pat, binid, st);
+    k_numeric_binid<<<grid, 256, 0, L.stream>>>(m, counts, pat_off, pat_len, pat, flops, binid, st);
     L.end(L.stream);
 }
 

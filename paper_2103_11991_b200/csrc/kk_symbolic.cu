@@ -1094,6 +1094,38 @@ static void launch_sym_hash(Launch& L, const SymArgs& a, int bin) {
     L.end(L.stream);
 }
 
+// a5 for tiny rows (flops_i <= TINY_MAX): a lane owns a row; its distinct columns in a
+// register list (TinyList; the paper's accumulator in K registers, accum = set insert)
+template <typename OffT>
+__global__ void __launch_bounds__(256) k_sym_tiny(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                  const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                                  const int32_t* __restrict__ perm, const int* __restrict__ bin_start,
+                                                  int bin, int32_t* __restrict__ counts) {
+    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
+    for (int r = r0 + blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += gridDim.x * blockDim.x) {
+        const int i = perm[r];
+        TinyList<TINY_MAX, float, false> T;
+        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
+        for (int64_t p = s; p < e; ++p) {
+            const int j = __ldg(aent + p);
+            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+            for (int64_t q = bs; q < be; ++q) T.insert(__ldg(bent + q), 0.0f);
+        }
+        counts[i] = T.n;
+    }
+}
+
+template <typename OffT>
+static void launch_sym_tiny(Launch& L, const SymArgs& a) {
+    auto kern = k_sym_tiny<OffT>;
+    KCfg c = kernel_cfg(kern, 256, 0, L.num_sms);
+    const int grid = (int)std::min<int64_t>((a.A.nrows + 255) / 256, c.grid_cap);
+    L.begin("sym_tiny", L.stream);
+    kern<<<grid, 256, 0, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map, a.B.entries,
+                                     a.perm, a.bin_start, SYM_TINY_BIN, a.counts);
+    L.end(L.stream);
+}
+
 template <typename OffT>
 static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stream) {
     // dense rows first (heaviest), on their own stream when given
@@ -1112,6 +1144,7 @@ static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stre
                                                a.k, wbits, a.cursors, a.counts, a.st);
         L.end(s);
     }
+    launch_sym_tiny<OffT>(L, a);
     launch_sym_window<OffT, 65536>(L, a, SYM_WIN_BIN0 + 4);
     launch_sym_window<OffT, 49152>(L, a, SYM_WIN_BIN0 + 3);
     launch_sym_window<OffT, 32768>(L, a, SYM_WIN_BIN0 + 2);
