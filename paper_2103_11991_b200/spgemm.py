@@ -160,59 +160,126 @@ class SpGEMM:
         return CsrMatrix(A.nrows, B.ncols, rm, ent, val)
 
     # -- end to end from host memory ------------------------------------------------------
-    def multiply_host(self, A, B, stream=None) -> "CsrMatrix":
-        """C = A*B for CSR operands in (pinned) HOST memory: host->device copies of A and B,
-        both phases on the device, device->host copy of C into pinned host tensors.  Device
-        staging buffers are cached on the handle and reused when the sizes allow.  Returns
-        a host CsrMatrix (valid until the next call on this handle)."""
+    def multiply_host(self, A, B, stream=None, blocks: Optional[int] = None) -> "CsrMatrix":
+        """C = A*B for CSR operands in (pinned) HOST memory, C returned in pinned HOST memory.
+
+        B is copied to the device once; A is processed in `blocks` contiguous row blocks
+        (default 8 when A has >= 64K rows): block b's host->device copy, its symbolic and
+        numeric phases and the device->host copy of its rows of C run on three streams, so
+        the copies of neighbouring blocks (both PCIe directions) overlap the kernels.  Row
+        blocks are independent products (Eq. 1); the host assembles the
+        global row map from the blocks' row maps and nnz.  Device and pinned staging buffers
+        are cached on the handle.  The result is valid until the next call on this handle."""
         A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
         dev = self.device
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         cache = self.__dict__.setdefault("_host_cache", {})
+        m = A.nrows
+        if blocks is None:
+            blocks = 8 if m >= 65536 else 1
+        blocks = max(1, min(int(blocks), max(m, 1)))
+        if "s_in" not in cache:
+            cache["s_in"] = torch.cuda.Stream(dev)
+            cache["s_out"] = torch.cuda.Stream(dev)
+        s_in, s_out = cache["s_in"], cache["s_out"]
 
-        def dbuf(key, t):
-            b = cache.get(key)
-            if b is None or b.numel() < t.numel() or b.dtype != t.dtype:
-                b = torch.empty(max(t.numel(), 1), dtype=t.dtype, device=dev)
-                cache[key] = b
-            v = b[:t.numel()]
-            with torch.cuda.stream(st):
-                v.copy_(t, non_blocking=True)
-            return v
+        def dbuf(key, n, dtype):
+            t = cache.get(key)
+            if t is None or t.numel() < n or t.dtype != dtype:
+                t = torch.empty(max(n, 1), dtype=dtype, device=dev)
+                cache[key] = t
+            return t[:n]
 
         def hbuf(key, n, dtype):
-            b = cache.get(key)
-            if b is None or b.numel() < n or b.dtype != dtype:
-                b = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
-                cache[key] = b
-            return b[:n]
+            t = cache.get(key)
+            if t is None or t.numel() < n or t.dtype != dtype:
+                t = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
+                cache[key] = t
+            return t[:n]
 
-        Ad = CsrMatrix(A.nrows, A.ncols, dbuf("arm", A.row_map), dbuf("aent", A.entries), dbuf("aval", A.values))
-        Bd = CsrMatrix(B.nrows, B.ncols, dbuf("brm", B.row_map), dbuf("bent", B.entries), dbuf("bval", B.values))
-        crm = cache.get("crm")
-        if crm is None or crm.numel() < A.nrows + 1 or crm.dtype != A.row_map.dtype:
-            crm = torch.empty(A.nrows + 1, dtype=A.row_map.dtype, device=dev)
-            cache["crm"] = crm
-        crm = crm[:A.nrows + 1]
-        crm, nnz = self.symbolic(Ad, Bd, c_row_map=crm, stream=st)
-        cent = cache.get("cent")
-        if cent is None or cent.numel() < nnz:
-            cent = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
-            cache["cent"] = cent
-        cval = cache.get("cval")
-        if cval is None or cval.numel() < nnz or cval.dtype != A.values.dtype:
-            cval = torch.empty(max(nnz, 1), dtype=A.values.dtype, device=dev)
-            cache["cval"] = cval
-        cent, cval = self.numeric(Ad, Bd, crm, nnz=nnz, c_entries=cent[:nnz], c_values=cval[:nnz], stream=st)
-        h_rm = hbuf("h_crm", A.nrows + 1, crm.dtype)
-        h_ent = hbuf("h_cent", nnz, torch.int32)
-        h_val = hbuf("h_cval", nnz, cval.dtype)
-        with torch.cuda.stream(st):
-            h_rm.copy_(crm, non_blocking=True)
-            h_ent.copy_(cent, non_blocking=True)
-            h_val.copy_(cval, non_blocking=True)
-        st.synchronize()
-        return CsrMatrix(A.nrows, B.ncols, h_rm, h_ent, h_val)
+        def h2d(key, t):
+            d = dbuf(key, t.numel(), t.dtype)
+            d.copy_(t, non_blocking=True)
+            return d
+
+        # B once (every block reads all of it)
+        ev_b = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            Bd = CsrMatrix(B.nrows, B.ncols, h2d("brm", B.row_map), h2d("bent", B.entries), h2d("bval", B.values))
+            ev_b.record(s_in)
+        # A's row blocks; their row maps rebased to 0 in a pinned staging buffer
+        rm = A.row_map
+        cuts = [m * q // blocks for q in range(blocks + 1)]
+        reb = hbuf("a_rm_reb", m + blocks, rm.dtype)
+        roffs = []
+        for q in range(blocks):
+            r0, r1 = cuts[q], cuts[q + 1]
+            o = q + r0
+            torch.sub(rm[r0:r1 + 1], rm[r0], out=reb[o:o + r1 - r0 + 1])
+            roffs.append(o)
+        ev_in = [torch.cuda.Event() for _ in range(blocks)]
+        ev_c = [torch.cuda.Event() for _ in range(blocks)]
+        ev_out = [torch.cuda.Event() for _ in range(blocks)]
+
+        def load_block(q):
+            r0, r1 = cuts[q], cuts[q + 1]
+            e0, e1 = int(rm[r0]), int(rm[r1])
+            sl = q % 2
+            with torch.cuda.stream(s_in):
+                if q >= 2:
+                    s_in.wait_event(ev_c[q - 2])
+                Ab = CsrMatrix(r1 - r0, A.ncols, h2d(f"arm{sl}", reb[roffs[q]:roffs[q] + r1 - r0 + 1]),
+                               h2d(f"aent{sl}", A.entries[e0:e1]), h2d(f"aval{sl}", A.values[e0:e1]))
+                ev_in[q].record(s_in)
+            return Ab
+
+        h_rm = hbuf("h_crm", m + 1, rm.dtype)
+        pending = [load_block(q) for q in range(min(2, blocks))]
+        nnz_off = [0] * (blocks + 1)
+        for q in range(blocks):
+            r0, r1 = cuts[q], cuts[q + 1]
+            Ab = pending[q]
+            sl = q % 2
+            st.wait_event(ev_in[q])
+            st.wait_event(ev_b)
+            if q >= 2:
+                st.wait_event(ev_out[q - 2])
+            crm = dbuf(f"crm{sl}", r1 - r0 + 1, rm.dtype)
+            crm, nnz = self.symbolic(Ab, Bd, c_row_map=crm, stream=st)
+            cent = dbuf(f"cent{sl}", nnz, torch.int32)
+            cval = dbuf(f"cval{sl}", nnz, A.values.dtype)
+            self.numeric(Ab, Bd, crm, nnz=nnz, c_entries=cent, c_values=cval, stream=st)
+            ev_c[q].record(st)
+            nnz_off[q + 1] = nnz_off[q] + nnz
+            # host output capacity (grows only on a first, larger call: earlier blocks are kept)
+            for key, dt in (("h_cent", torch.int32), ("h_cval", A.values.dtype)):
+                t = cache.get(key)
+                if t is None or t.numel() < nnz_off[q + 1] or t.dtype != dt:
+                    s_out.synchronize()
+                    nt = torch.empty(max(int(nnz_off[q + 1] * 1.25), 1), dtype=dt, pin_memory=True)
+                    if t is not None and t.dtype == dt and nnz_off[q]:
+                        nt[:nnz_off[q]].copy_(t[:nnz_off[q]])
+                    cache[key] = nt
+            h_ent, h_val = cache["h_cent"], cache["h_cval"]
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_c[q])
+                h_rm[r0:r1 + 1].copy_(crm, non_blocking=True)
+                h_ent[nnz_off[q]:nnz_off[q + 1]].copy_(cent, non_blocking=True)
+                h_val[nnz_off[q]:nnz_off[q + 1]].copy_(cval, non_blocking=True)
+                ev_out[q].record(s_out)
+            if q + 2 < blocks:
+                pending.append(load_block(q + 2))
+        s_out.synchronize()
+        # global row map: block q's local offsets + the nnz of the blocks before it (block
+        # q+1's copy overwrote the shared boundary entry with its local 0; restored here)
+        for q in range(blocks):
+            r0, r1 = cuts[q], cuts[q + 1]
+            if nnz_off[q]:
+                h_rm[r0 + 1:r1 + 1] += nnz_off[q]
+            h_rm[r0] = nnz_off[q]
+        h_rm[m] = nnz_off[blocks]
+        tot = nnz_off[blocks]
+        return CsrMatrix(m, B.ncols, h_rm, cache["h_cent"][:tot], cache["h_cval"][:tot])
 
     # -- individual steps ----------------------------------------------------------------
     def row_flops(self, A, B, scan: bool = True, total: bool = True, stream=None):

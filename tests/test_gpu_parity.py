@@ -286,3 +286,28 @@ def test_pattern_pool_overflow(oracle_mod):
     B = _banded(n, n, 40, 1000, seed=6)
     got = gpu_spgemm(A, B)
     assert_parity(oracle_mod, A, B, got)
+
+
+@pytest.mark.parametrize("blocks", [1, 3, 8, None])
+@pytest.mark.parametrize("ot", [torch.int32, torch.int64])
+def test_multiply_host_blocks(oracle_mod, blocks, ot):
+    """Host-buffer path (the e2e API): A in row blocks pipelined over three streams; the
+    assembled host C equals the oracle (row map, columns bit-exact)."""
+    from paper_2103_11991_b200 import CsrMatrix, SpGEMM
+
+    A, B = g.config("C2", size=11, values="random")
+
+    def host(M):
+        return CsrMatrix(M.nrows, M.ncols, M.row_map.to(ot).pin_memory(), M.entries.pin_memory(),
+                         M.values.pin_memory())
+
+    h = SpGEMM()
+    for _ in range(2):  # second call reuses the cached staging buffers
+        C = h.multiply_host(host(A), host(B), blocks=blocks)
+        got = (C.row_map.numpy().astype(np.int64), C.entries.numpy().copy(), C.values.numpy().copy())
+        assert_parity(oracle_mod, A, B, got)
+    # a row block count above the row count, and an empty A
+    E = g.random_csr(0, B.nrows, 3, seed=1)
+    C = h.multiply_host(host(E), host(B), blocks=4)
+    assert C.row_map.numel() == 1 and int(C.row_map[0]) == 0 and C.entries.numel() == 0
+    h.close()
