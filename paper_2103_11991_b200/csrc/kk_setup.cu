@@ -548,8 +548,11 @@ __device__ __forceinline__ int warp_bin_hist(int64_t r0, int64_t r1, const uint8
     for (int64_t base = r0; base < r1; base += 32) {
         const int64_t r = base + lane;
         const int b = r < r1 ? (int)binid[r] : 255;
-#pragma unroll
-        for (int t = 0; t < NB; ++t) {
+        // only the bins present among these 32 rows (usually one or two)
+        unsigned pres = __reduce_or_sync(FULL, b < NB ? 1u << b : 0u);
+        while (pres) {
+            const int t = __ffs(pres) - 1;
+            pres &= pres - 1;
             const unsigned bal = __ballot_sync(FULL, b == t);
             if (lane == t) cnt += __popc(bal);
         }
@@ -572,28 +575,32 @@ __global__ void __launch_bounds__(BWARPS * 32) k_bin_count(int64_t m, const uint
     }
 }
 
-// one CTA of 1024 threads: exclusive scan over tiles, bin by bin
-__global__ void __launch_bounds__(1024) k_bin_offsets(int64_t ntiles, int32_t* __restrict__ tilecnt,
-                                                      int* __restrict__ bin_start_dst) {
+// one CTA, one warp per bin: exclusive scan of the bin's tile counts (all bins at once),
+// then the bin starts from the bin totals
+__global__ void __launch_bounds__(NB * 32) k_bin_offsets(int64_t ntiles, int32_t* __restrict__ tilecnt,
+                                                         int* __restrict__ bin_start_dst) {
     __shared__ int64_t totals[NB];
-    for (int b = 0; b < NB; ++b) {
-        int64_t carry = 0;
-        for (int64_t c0 = 0; c0 < ntiles; c0 += blockDim.x) {
-            const int64_t c = c0 + threadIdx.x;
-            const int64_t v = c < ntiles ? tilecnt[c * NB + b] : 0;
-            int64_t ex;
-            const int64_t tot = block_exclusive_scan(v, &ex);
-            if (c < ntiles) tilecnt[c * NB + b] = (int32_t)(carry + ex);
-            carry += tot;
+    const int lane = threadIdx.x & 31, b = threadIdx.x >> 5;
+    int64_t carry = 0;
+    for (int64_t c0 = 0; c0 < ntiles; c0 += 32) {
+        const int64_t c = c0 + lane;
+        const int64_t v = c < ntiles ? tilecnt[c * NB + b] : 0;
+        int64_t x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int64_t y = __shfl_up_sync(FULL, x, d);
+            if (lane >= d) x += y;
         }
-        if (threadIdx.x == 0) totals[b] = carry;
-        __syncthreads();
+        if (c < ntiles) tilecnt[c * NB + b] = (int32_t)(carry + x - v);
+        carry += __shfl_sync(FULL, x, 31);
     }
+    if (lane == 0) totals[b] = carry;
+    __syncthreads();
     if (threadIdx.x == 0) {
         int64_t run = 0;
-        for (int b = 0; b < NB; ++b) {
-            bin_start_dst[b] = (int)run;
-            run += totals[b];
+        for (int t = 0; t < NB; ++t) {
+            bin_start_dst[t] = (int)run;
+            run += totals[t];
         }
         bin_start_dst[NB] = (int)run;
     }
@@ -617,8 +624,10 @@ __global__ void __launch_bounds__(BWARPS * 32) k_bin_scatter(int64_t m, const ui
     for (int64_t base = r0; base < r1; base += 32) {
         const int64_t r = base + lane;
         const int b = r < r1 ? (int)binid[r] : 255;
-#pragma unroll
-        for (int t = 0; t < NB; ++t) {
+        unsigned pres = __reduce_or_sync(FULL, b < NB ? 1u << b : 0u);
+        while (pres) {
+            const int t = __ffs(pres) - 1;
+            pres &= pres - 1;
             const unsigned bal = __ballot_sync(FULL, b == t);
             const int base_t = __shfl_sync(FULL, run, t);
             if (b == t) perm[base_t + __popc(bal & lanemask_lt())] = (int32_t)r;
@@ -635,7 +644,7 @@ void bin_rows(Launch& L, int64_t m, const uint8_t* binid, int32_t* scratch, int3
     }
     L.begin("bin_rows", L.stream);
     k_bin_count<<<(unsigned)ntiles, BWARPS * 32, 0, L.stream>>>(m, binid, scratch);
-    k_bin_offsets<<<1, 1024, 0, L.stream>>>(ntiles, scratch, bin_start_dst);
+    k_bin_offsets<<<1, NB * 32, 0, L.stream>>>(ntiles, scratch, bin_start_dst);
     k_bin_scatter<<<(unsigned)ntiles, BWARPS * 32, 0, L.stream>>>(m, binid, scratch, bin_start_dst, perm);
     L.end(L.stream, 3);
 }
