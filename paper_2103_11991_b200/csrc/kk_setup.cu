@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(256) k_check_compress(int64_t n, int64_t k, co
                                                         const int32_t* __restrict__ bent, int do_comp,
                                                         int validate, int32_t* __restrict__ bc_len,
                                                         uint2* __restrict__ pairs, int4* __restrict__ bmeta,
-                                                        DevStatus* st) {
+                                                        DevStatus* st, int lane_max) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(256) k_check_compress(int64_t n, int64_t k, co
         bool long_row = false;
         if (j < n) {
             const int64_t s = ld(brm, j), e = ld(brm, j + 1);
-            if (e - s > LANE_ROW_MAX) {
+            if (e - s > lane_max) {
                 long_row = true;
             } else {
                 int prev = INT_MIN, cw = -1, outn = 0;
@@ -189,13 +189,21 @@ void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_
     if (B.nrows == 0) return;
     const int threads = 256;
     const int grid = grid_for((B.nrows + 31) / 32, threads, L.num_sms, 16);
+    // rows longer than lane_max are walked by the whole warp (coalesced, segmented OR scan);
+    // shorter ones by one lane each (KK_COMP_LANE_MAX, experiments)
+    static const int lane_max = [] {
+        const char* v = getenv("KK_COMP_LANE_MAX");
+        return v ? atoi(v) : LANE_ROW_MAX;
+    }();
     L.begin(do_comp ? "check_compress" : "check_sorted", L.stream);
     if (off64)
         k_check_compress<int64_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int64_t*)B.row_map, B.entries,
-                                                                  do_comp, validate, bc_len, pairs, bmeta, st);
+                                                                  do_comp, validate, bc_len, pairs, bmeta, st,
+                                                                  lane_max);
     else
         k_check_compress<int32_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int32_t*)B.row_map, B.entries,
-                                                                  do_comp, validate, bc_len, pairs, bmeta, st);
+                                                                  do_comp, validate, bc_len, pairs, bmeta, st,
+                                                                  lane_max);
     L.end(L.stream);
 }
 
