@@ -507,11 +507,12 @@ def run_ours(args):
         def e2e_step():
             # the user-level host path: C = A*B, or T = A*P then Ac = R*T, each call copying
             # its operands in and its result out
-            C = hes[0].multiply_host(hmats[0], hmats[1])
+            nb = int(os.environ["KK_E2E_BLOCKS"]) if os.environ.get("KK_E2E_BLOCKS") else None
+            C = hes[0].multiply_host(hmats[0], hmats[1], blocks=nb)
             ins = [hmats[0], hmats[1]]
             if len(prods) > 1:
                 ins += [hmats[2], C]
-                C = hes[1].multiply_host(hmats[2], C)
+                C = hes[1].multiply_host(hmats[2], C, blocks=nb)
             return ins, C
 
         for _ in range(2):
