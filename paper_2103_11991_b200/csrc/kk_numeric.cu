@@ -851,27 +851,31 @@ __global__ void __launch_bounds__(256, MINB) k_num_pattern(const OffT* __restric
 // k_num_pattern's -- rank(c) = prefix(word(c)) + popc(mask & bits below c) from the
 // pattern kept by symbolic, accum = + into a dense per-row value array (PAPER.md:178,
 // Eq. 1) -- with the instruction stream cut down:
-//   * each 32-entry A chunk is compacted to its non-empty B rows; one B row per warp step
-//     (B rows of <= 32 entries; longer ones take a plain segment loop);
+//   * each 32-entry A chunk becomes steps, one per 32-entry segment of its B rows (empty
+//     B rows give none, a row of L entries ceil(L/32)), 16-byte records in windows of 32;
 //   * steps are branch-free: lanes past the B row's end load a valid entry of it and
 //     accumulate into a dump slot vals[CAP], so no divergent region per step;
 //   * two steps per iteration, loads two steps ahead, and both steps' rank lookups are
 //     issued before either read-modify-write (the lookups only read the pattern tables);
 //   * the prologue writes each rank's column into shared memory once (one popcount scan
 //     of two 16-bit halves), and the epilogue writes entries and values coalesced.
-// Needs B.nnz < 2^31 (32-bit element offsets) and strictly increasing B rows.
+// Needs B.nnz < 2^31 (32-bit element offsets) and strictly increasing B rows.  HASHW: the
+// word index is a hash of the pattern's words (rows whose words span > PAT_NWIN words).
 // ------------------------------------------------------------------------------------
-template <typename ValT, int CAP>
+// HASHW: patterns whose words span more than PAT_NWIN words (wide rows, e.g. C5): the word
+// index is a PAT_SW-slot hash of the words (winfo indexed by hash slot) instead of a dense
+// u8 index over the window.
+template <typename ValT, int CAP, bool HASHW = false>
 struct RankLayout {
     static constexpr size_t vals = 0;  // CAP + 1 values (slot CAP: idle lanes)
     static constexpr size_t cols = ((size_t)(CAP + 1) * sizeof(ValT) + 15) / 16 * 16;  // CAP int32
     static constexpr size_t rec = cols + (size_t)CAP * 4;                                // 32 x {bb, len, a}
-    static constexpr size_t winfo = rec + 32 * 16;                                       // PAT_W x (mask, prefix)
-    static constexpr size_t widx = winfo + (size_t)PAT_W * 8;                            // PAT_NWIN x u8
-    static constexpr size_t bytes = (widx + (size_t)PAT_NWIN + 15) / 16 * 16;
+    static constexpr size_t winfo = rec + 32 * 16;                  // (mask, prefix) per word / hash slot
+    static constexpr size_t widx = winfo + (size_t)(HASHW ? PAT_SW : PAT_W) * 8;  // u8 index | hash keys
+    static constexpr size_t bytes = (widx + (HASHW ? (size_t)PAT_SW * 4 : (size_t)PAT_NWIN) + 15) / 16 * 16;
 };
 
-template <typename OffT, typename ValT, int CAP, int MINB>
+template <typename OffT, typename ValT, int CAP, int MINB, bool HASHW>
 __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                         const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                                         const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
@@ -881,7 +885,7 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                                                         const uint2* __restrict__ pat, const long long* __restrict__ pat_off,
                                                         const int* __restrict__ pat_len, const ValT* __restrict__ dinv,
                                                         double omega) {
-    using LY = RankLayout<ValT, CAP>;
+    using LY = RankLayout<ValT, CAP, HASHW>;
     extern __shared__ __align__(16) unsigned char sm_rank[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     // all shared accesses as sm_rank + 32-bit offset (shared addressing, no generic)
@@ -893,6 +897,9 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
     int r = r0 + blockIdx.x * warps + warp;
     if (r >= r1) return;
     for (int t = lane; t < CAP; t += 32) *(ValT*)(sm_rank + o_val + t * (uint32_t)sizeof(ValT)) = (ValT)0;
+    uint32_t* wkeys = (uint32_t*)(sm_rank + o_w + (uint32_t)LY::widx);  // HASHW only
+    if (HASHW)
+        for (int t = lane; t < PAT_SW; t += 32) wkeys[t] = EMPTY;
     int i = perm[r];
     while (true) {
         const int rn = r + stride;
@@ -919,9 +926,15 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
         const uint32_t wb = __shfl_sync(FULL, p0.x, 0);
         const uint32_t o_idx = o_w + (uint32_t)LY::widx - wb;
         __syncwarp();
+        // word -> (mask, prefix) slot: dense u8 index, or the hash slot of the word
+        uint32_t h0 = (uint32_t)lane, h1 = (uint32_t)lane + 32u;
+        if constexpr (HASHW) {
+            h0 = wt_insert(wkeys, p0.x, lane < pl);
+            h1 = wt_insert(wkeys, p1.x, lane + 32 < pl);
+        }
         if (lane < pl) {
-            sm_rank[o_idx + p0.x] = (uint8_t)lane;
-            *(uint2*)(sm_rank + o_inf + lane * 8u) = make_uint2(p0.y, (uint32_t)pre0);
+            if constexpr (!HASHW) sm_rank[o_idx + p0.x] = (uint8_t)lane;
+            *(uint2*)(sm_rank + o_inf + h0 * 8u) = make_uint2(p0.y, (uint32_t)pre0);
             uint32_t m = p0.y;
             uint32_t o = o_col + (uint32_t)pre0 * 4u;
             while (m) {
@@ -931,8 +944,8 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
             }
         }
         if (lane + 32 < pl) {
-            sm_rank[o_idx + p1.x] = (uint8_t)(lane + 32);
-            *(uint2*)(sm_rank + o_inf + (lane + 32) * 8u) = make_uint2(p1.y, (uint32_t)pre1);
+            if constexpr (!HASHW) sm_rank[o_idx + p1.x] = (uint8_t)(lane + 32);
+            *(uint2*)(sm_rank + o_inf + h1 * 8u) = make_uint2(p1.y, (uint32_t)pre1);
             uint32_t m = p1.y;
             uint32_t o = o_col + (uint32_t)pre1 * 4u;
             while (m) {
@@ -943,7 +956,14 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
         }
         __syncwarp();
         auto rank = [&](int col, bool valid) -> uint32_t {
-            const uint32_t wi = sm_rank[o_idx + ((uint32_t)col >> 5)];
+            uint32_t wi;
+            if constexpr (HASHW) {
+                const uint32_t w = (uint32_t)col >> 5;
+                wi = wt_slot(w);
+                while (wkeys[wi] != w) wi = (wi + 1) & (PAT_SW - 1);  // present: no empty-slot test
+            } else {
+                wi = sm_rank[o_idx + ((uint32_t)col >> 5)];
+            }
             const uint2 mp = *(const uint2*)(sm_rank + o_inf + wi * 8u);
             const uint32_t rk = mp.y + __popc(mp.x & ~(0xffffffffu << (col & 31)));
             return valid ? rk : (uint32_t)CAP;
@@ -953,6 +973,8 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
             *p += prod;
         };
         // ---- products, one 32-entry A chunk at a time ----
+        // A step is one 32-entry segment of a B row (a B row of L entries gives ceil(L/32)
+        // steps); the chunk's steps are written as 16-byte records in windows of 32.
         for (int64_t a0 = s; a0 < e; a0 += 32) {
             const int na = (int)min((int64_t)32, e - a0);
             int bb = 0, bl = 0;
@@ -963,18 +985,8 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                 bb = (int)ld(brm, j);
                 bl = (int)(ld(brm, j + 1) - bb);
             }
-            const unsigned ne = __ballot_sync(FULL, bl > 0);
-            const int nt = __popc(ne);
-            const int maxbl = (int)__reduce_max_sync(FULL, (unsigned)bl);
-            __syncwarp();
-            if (bl > 0)
-                *(int4*)(sm_rank + o_rec + __popc(ne & lanemask_lt()) * 16u) =
-                    make_int4(bb, bl, __double2loint(av), __double2hiint(av));
-            __syncwarp();
-            if (nt == 0) continue;
-            if (maxbl <= 32) {
-                // (step records read back by shuffles instead of LDS.128 measured slower:
-                // 2.28 vs 2.00 ms on C2 -- shuffles share the pipe)
+            // the chunk's nt steps from their records: two per iteration, loads two ahead
+            auto run_steps = [&](int nt) {
                 auto load = [&](int t, int& col, ValT& bv, ValT& a, bool& valid) {
                     const int4 rr = *(const int4*)(sm_rank + o_rec + (uint32_t)min(t, nt - 1) * 16u);
                     valid = t < nt && lane < rr.y;
@@ -1000,18 +1012,39 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                     acc(rB, pB);
                     __syncwarp();
                 }
+            };
+            // (HASHW rows -- wide patterns, e.g. C5's 81-entry B rows -- always take the
+            // segment form: one call site of run_steps measured 221 vs 325 ms on C5)
+            const int maxbl = HASHW ? 33 : (int)__reduce_max_sync(FULL, (unsigned)bl);
+            if (maxbl <= 32) {
+                // one step per non-empty B row: records compacted by ballot
+                const unsigned ne = __ballot_sync(FULL, bl > 0);
+                __syncwarp();
+                if (bl > 0)
+                    *(int4*)(sm_rank + o_rec + __popc(ne & lanemask_lt()) * 16u) =
+                        make_int4(bb, bl, __double2loint(av), __double2hiint(av));
+                __syncwarp();
+                if (ne) run_steps(__popc(ne));
             } else {
-                for (int t = 0; t < nt; ++t) {
-                    const int4 rr = *(const int4*)(sm_rank + o_rec + (uint32_t)t * 16u);
-                    const ValT a = (ValT)__hiloint2double(rr.w, rr.z);
-                    for (int q0 = 0; q0 < rr.y; q0 += 32) {
-                        const bool valid = q0 + lane < rr.y;
-                        const int q = rr.x + min(q0 + lane, rr.y - 1);
-                        const int col = __ldg(bent + q);
-                        const ValT bv = __ldg(bval + q);
-                        acc(rank(col, valid), a * bv);
-                        __syncwarp();
+                // long B rows: one step per 32-entry segment, records in windows of 32
+                const int nseg = (bl + 31) >> 5;
+                int xs = nseg;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int y = __shfl_up_sync(FULL, xs, d);
+                    if (lane >= d) xs += y;
+                }
+                const int T = __shfl_sync(FULL, xs, 31);
+                const int ex = xs - nseg;
+                for (int w0 = 0; w0 < T; w0 += 32) {
+                    __syncwarp();
+                    for (int g = max(ex, w0); g < min(ex + nseg, w0 + 32); ++g) {
+                        const int so = (g - ex) * 32;
+                        *(int4*)(sm_rank + o_rec + (uint32_t)(g - w0) * 16u) =
+                            make_int4(bb + so, min(32, bl - so), __double2loint(av), __double2hiint(av));
                     }
+                    __syncwarp();
+                    run_steps(min(32, T - w0));
                 }
             }
             __syncwarp();
@@ -1028,7 +1061,16 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                 const bool valid = q0 + lane < bl;
                 const int q = bs + min(q0 + lane, bl - 1);
                 const int col = __ldg(bent + q);
-                uint32_t rk = rank(col, valid);
+                // a word outside the dense index's range is not in the pattern
+                bool inpat = HASHW || ((uint32_t)col >> 5) - wb < (uint32_t)PAT_NWIN;
+                if constexpr (HASHW) {
+                    // the word must be present before probing (no empty-slot test in rank())
+                    const uint32_t w = (uint32_t)col >> 5;
+                    uint32_t wi = wt_slot(w);
+                    while (wkeys[wi] != w && wkeys[wi] != EMPTY) wi = (wi + 1) & (PAT_SW - 1);
+                    inpat = wkeys[wi] == w;
+                }
+                uint32_t rk = rank(inpat ? col : (int)(wb * 32u), valid && inpat);
                 // a column outside the pattern (A(i,i) not stored) must not land on another rank
                 if (rk < (uint32_t)CAP && *(const int32_t*)(sm_rank + o_col + rk * 4u) != col) rk = CAP;
                 acc(rk, __ldg(bval + q));
@@ -1036,6 +1078,10 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
             }
         }
         // ---- entries and values, coalesced; reset ----
+        if (HASHW) {
+            if (lane < pl) wkeys[h0] = EMPTY;
+            if (lane + 32 < pl) wkeys[h1] = EMPTY;
+        }
         for (int t = lane; t < clen; t += 32) {
             cent[cb + t] = *(const int32_t*)(sm_rank + o_col + (uint32_t)t * 4u);
             ValT* p = (ValT*)(sm_rank + o_val + (uint32_t)t * (uint32_t)sizeof(ValT));
@@ -1058,24 +1104,24 @@ static bool use_num_rank() {
     return v;
 }
 
-template <typename OffT, typename ValT, int CAP>
+template <typename OffT, typename ValT, int CAP, bool HASHW = false>
 static void launch_num_rank(Launch& L, const NumArgs& a, int bin) {
     const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
     if (rows <= 0) return;
     const int warps = 8;
-    const size_t smem = (size_t)warps * RankLayout<ValT, CAP>::bytes;
+    const size_t smem = (size_t)warps * RankLayout<ValT, CAP, HASHW>::bytes;
     static const int minb = [] {
         const char* v = getenv("KK_RANK_MINB");
         const int x = v ? atoi(v) : 4;
         return (x == 5 || x == 6) ? x : 4;
     }();
-    auto kern = minb == 5 ? k_num_rank<OffT, ValT, CAP, 5>
-              : minb == 6 ? k_num_rank<OffT, ValT, CAP, 6>
-                          : k_num_rank<OffT, ValT, CAP, 4>;
+    auto kern = minb == 5 ? k_num_rank<OffT, ValT, CAP, 5, HASHW>
+              : minb == 6 ? k_num_rank<OffT, ValT, CAP, 6, HASHW>
+                          : k_num_rank<OffT, ValT, CAP, 4, HASHW>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (rows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
-    L.begin(kname("num_rank", CAP), L.stream);
+    L.begin(kname(HASHW ? "num_rank_hash" : "num_rank", CAP), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                                (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
@@ -1085,8 +1131,8 @@ static void launch_num_rank(Launch& L, const NumArgs& a, int bin) {
 
 template <typename OffT, typename ValT, int CAP, bool DENSE>
 static void launch_num_pattern(Launch& L, const NumArgs& a, int bin) {
-    if (DENSE && a.B.nnz < INT32_MAX && use_num_rank()) {
-        launch_num_rank<OffT, ValT, CAP>(L, a, bin);
+    if (a.B.nnz < INT32_MAX && use_num_rank()) {
+        launch_num_rank<OffT, ValT, CAP, !DENSE>(L, a, bin);
         return;
     }
     const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];

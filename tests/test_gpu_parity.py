@@ -311,3 +311,16 @@ def test_multiply_host_blocks(oracle_mod, blocks, ot):
     C = h.multiply_host(host(E), host(B), blocks=4)
     assert C.row_map.numel() == 1 and int(C.row_map[0]) == 0 and C.entries.numel() == 0
     h.close()
+
+
+@pytest.mark.parametrize("vt", [torch.float64, torch.float32])
+def test_wide_pattern_hashed_word_table(oracle_mod, vt):
+    """Rows whose kept pattern (<= 64 words) spans more than the dense word index (2,048
+    words): the numeric rank kernel with the hashed word table (num_rank_hash)."""
+    n, k = 4000, 400000
+    A = _banded(1200, n, 4, 40, seed=21)
+    B = _banded(n, k, 14, 60000, seed=22)
+    got = gpu_spgemm(A, B, value_dtype=vt, offset_dtype=torch.int32)
+    assert_parity(oracle_mod, A, B, got, value_dtype=vt)
+    st = got[3]
+    assert sum(st["numeric_bin_rows"][12:16]) > 0, "expected rows in the hashed-pattern bins"
