@@ -786,15 +786,19 @@ __global__ void __launch_bounds__(256, 1) k_sym_window(const OffT* __restrict__ 
 // shared atomic.
 // ------------------------------------------------------------------------------------
 
-template <typename OffT, int W, bool COMP>
-__global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+// S > 0 (HT): rows whose columns do not fit a window keep their words in a warp-owned hash
+// table (keys[S] | masks[S], bank-major linear probing, write-then-verify claims) instead of
+// the bit vector; the list holds slots, the epilogue sorts the words and re-finds them.
+template <typename OffT, int W, bool COMP, int S = 0>
+__global__ void __launch_bounds__(256, S == 0 ? 4 : 1) k_sym_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                   const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
                                                   const int32_t* __restrict__ bc_len,
                                                   const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
                                                   const int* __restrict__ bin_start, int bin,
                                                   const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
                                                   PatOut po, DevStatus* st, int pblk) {
-    constexpr int NW = W / 32;
+    constexpr bool HT = S > 0;
+    constexpr int NW = HT ? 2 * S : W / 32;   // bitmap words, or keys[S] | masks[S]
     constexpr int WB = NW + 64 + PAT_WORDS;  // words per warp: bitmap | rec[32] (int2) | list
     extern __shared__ __align__(16) uint32_t sm_rows[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
@@ -806,7 +810,19 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
     int r = r0 + blockIdx.x * warps + warp;
     if (r >= r1) return;
     if (COMP != (st->use_comp != 0)) return;  // launched for the other mode
-    for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
+    uint32_t* hkeys = bm;      // HT
+    uint32_t* hmask = bm + S;  // HT
+    auto clear_all = [&]() {
+        if (HT) {
+            for (int t = lane; t < S; t += 32) {
+                hkeys[t] = EMPTY;
+                hmask[t] = 0;
+            }
+        } else {
+            for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
+        }
+    };
+    clear_all();
     long long pcur = 0, pend = 0;  // this warp's block of the pattern pool
     auto pair_at = [&](int q) -> uint2 {
         if (COMP) return __ldg(pairs + q);
@@ -817,7 +833,7 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
     // starts, its first 32 A entries when the row's products are done
     int i = perm[r];
     int64_t s = ld(arm, i), e = ld(arm, i + 1);
-    uint32_t wb = (uint32_t)__ldg(wlo + i) >> 5;
+    uint32_t wb = HT ? 0u : (uint32_t)__ldg(wlo + i) >> 5;
     int jfirst = lane < e - s ? __ldg(aent + s + lane) : 0;
     int inext = r + stride < r1 ? __ldg(perm + r + stride) : -1;
     __syncwarp();
@@ -827,29 +843,41 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
         if (inext >= 0) {
             sn = ld(arm, inext);
             en = ld(arm, inext + 1);
-            wbn = (uint32_t)__ldg(wlo + inext) >> 5;
+            wbn = HT ? 0u : (uint32_t)__ldg(wlo + inext) >> 5;
         }
         const int inext2 = r + 2 * stride < r1 ? __ldg(perm + r + 2 * stride) : -1;
         int cnt = 0, nt = 0;
-        // count the bits a lane added and list the words it turned non-zero
-        auto post = [&](uint32_t w, uint32_t m, uint32_t old, bool act) {
+        // count the bits a lane added and list the words it turned non-zero (tag: the word's
+        // bit-vector index, or its hash slot)
+        auto post = [&](uint32_t tag, uint32_t m, uint32_t old, bool act) {
             const bool fresh = act && old == 0;
             if (act) cnt += __popc(m & ~old);
             const unsigned fb = __ballot_sync(FULL, fresh);
             if (fresh) {
                 const int pos = nt + __popc(fb & lanemask_lt());
-                if (pos < PAT_WORDS) wl[pos] = w - wb;
+                if (pos < PAT_WORDS) wl[pos] = tag;
             }
             nt += __popc(fb);
         };
-        auto rmw = [&](uint32_t w, uint32_t m) -> uint32_t {
-            const uint32_t x = w - wb;
-            if (COMP) {
-                const uint32_t old = bm[x];
-                bm[x] = old | m;
+        // OR m into word w for the lanes with act (warp-collective: HT claims slots); returns
+        // the old mask, tag = bit-vector index or slot.  PLAIN: the active lanes' words are
+        // distinct (one B_C row), else the OR is atomic.
+        auto rmw = [&](uint32_t w, uint32_t m, bool act, bool plain, uint32_t& tag) -> uint32_t {
+            uint32_t* cell;
+            if constexpr (HT) {
+                tag = strict_claim<S>(hkeys, w, act);
+                cell = hmask + tag;
+            } else {
+                tag = w - wb;
+                cell = bm + tag;
+            }
+            if (!act) return 0u;
+            if (plain) {
+                const uint32_t old = *cell;
+                *cell = old | m;
                 return old;
             }
-            return atomicOr(&bm[x], m);
+            return atomicOr(cell, m);
         };
         for (int64_t a0 = s; a0 < e; a0 += 32) {
             const int na = (int)min((int64_t)32, e - a0);
@@ -885,19 +913,24 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
                     uint2 pn;
                     bool actn;
                     fetch(t + R, pn, actn);
-                    uint32_t old = 0;
+                    uint32_t old = 0, tag = 0;
                     if (COMP) {
                         // rows of a step may share words: one row per round
 #pragma unroll
                         for (int k = 0; k < R; ++k) {
-                            if (act && grp == k) old = rmw(p.x, p.y);
+                            uint32_t tg;
+                            const uint32_t o = rmw(p.x, p.y, act && grp == k, true, tg);
+                            if (act && grp == k) {
+                                old = o;
+                                tag = tg;
+                            }
                             __syncwarp();
                         }
                     } else {
-                        if (act) old = rmw(p.x, p.y);
+                        old = rmw(p.x, p.y, act, false, tag);
                         __syncwarp();
                     }
-                    post(p.x, p.y, old, act);
+                    post(tag, p.y, old, act);
                     p = pn;
                     act = actn;
                 }
@@ -916,8 +949,9 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
                     for (int q0 = 0; q0 < rr.y; q0 += 32) {
                         const bool act = q0 + lane < rr.y;
                         const uint2 pq = pair_at(rr.x + min(q0 + lane, rr.y - 1));
-                        const uint32_t old = act ? rmw(pq.x, pq.y) : 0u;
-                        post(pq.x, pq.y, old, act);
+                        uint32_t tag;
+                        const uint32_t old = rmw(pq.x, pq.y, act, COMP, tag);
+                        post(tag, pq.y, old, act);
                         __syncwarp();
                     }
                 }
@@ -944,7 +978,30 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
                     pcur += nt;
                 }
             }
-            if (nt <= 32) {
+            if (HT) {
+                // sort the listed words, re-find their slots, then clear them
+                uint32_t v[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) v[q] = lane * 2 + q < nt ? hkeys[wl[lane * 2 + q]] : 0xffffffffu;
+                warp_bitonic_sort<2>(v);
+                uint32_t sl[2] = {0u, 0u};
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int idx = lane * 2 + q;
+                    if (idx < nt) {
+                        sl[q] = strict_find<S>(hkeys, v[q]);
+                        if (off >= 0) po.pat[off + idx] = make_uint2(v[q], hmask[sl[q]]);
+                    }
+                }
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    if (lane * 2 + q < nt) {
+                        hkeys[sl[q]] = EMPTY;
+                        hmask[sl[q]] = 0;
+                    }
+                }
+            } else if (nt <= 32) {
                 uint32_t v[1] = {lane < nt ? wl[lane] : 0xffffffffu};
                 warp_bitonic_sort<1>(v);
                 if (lane < nt) {
@@ -972,7 +1029,7 @@ __global__ void __launch_bounds__(256, 4) k_sym_rows(const OffT* __restrict__ ar
                 po.len[i] = nt;
             }
         } else {
-            for (int t = lane; t < NW / 4; t += 32) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
+            clear_all();
         }
         __syncwarp();
         if (inext < 0) break;
@@ -1078,9 +1135,37 @@ __global__ void __launch_bounds__(256, 1) k_sym_hash(const OffT* __restrict__ ar
     }
 }
 
+template <typename OffT, int S>
+static void launch_sym_rows_ht(Launch& L, const SymArgs& a, int bin) {
+    const int warps = S <= 1024 ? 8 : (S <= 2048 ? 4 : 2);
+    const size_t smem = (size_t)warps * ((size_t)2 * S + 64 + PAT_WORDS) * 4;
+    auto kern = k_sym_rows<OffT, 32, true, S>;
+    auto kern0 = k_sym_rows<OffT, 32, false, S>;
+    KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
+    kernel_cfg(kern0, warps * 32, smem, L.num_sms);
+    int64_t need = (a.A.nrows + warps - 1) / warps;
+    int grid = (int)std::min<int64_t>(need, c.grid_cap);
+    const int64_t share = a.pat.cap / ((int64_t)grid * warps);
+    const int pblk = (int)std::max<int64_t>(PAT_WORDS, std::min<int64_t>(2048, share));
+    L.begin(kname("sym_rows_ht", S), L.stream);
+    int nl = 0;
+    for (auto k : {kern, kern0}) {
+        if ((k == kern && a.comp_mode == 0) || (k == kern0 && a.comp_mode == 1)) continue;
+        k<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
+                                                a.counts, a.pat, (DevStatus*)a.st, pblk);
+        ++nl;
+    }
+    L.end(L.stream, nl);
+}
+
 // hash bins: rows with ub <= cap = 64 << (bin - 1) words; table S = 2 * cap
 template <typename OffT, int S>
 static void launch_sym_hash(Launch& L, const SymArgs& a, int bin) {
+    if (a.B.nnz < INT32_MAX && use_sym_rows()) {
+        launch_sym_rows_ht<OffT, S>(L, a, bin);
+        return;
+    }
     const int warps = S <= 1024 ? 8 : (S <= 4096 ? 4 : 2);
     const size_t smem = (size_t)warps * (2 * S + 672 + PAT_WORDS) * 4;
     auto kern = k_sym_hash<OffT, S>;
