@@ -789,14 +789,13 @@ __global__ void __launch_bounds__(256, 1) k_sym_window(const OffT* __restrict__ 
 // S > 0 (HT): rows whose columns do not fit a window keep their words in a warp-owned hash
 // table (keys[S] | masks[S], bank-major linear probing, write-then-verify claims) instead of
 // the bit vector; the list holds slots, the epilogue sorts the words and re-finds them.
-template <typename OffT, int W, bool COMP, int S = 0>
-__global__ void __launch_bounds__(256, S == 0 ? 4 : 1) k_sym_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
-                                                  const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
-                                                  const int32_t* __restrict__ bc_len,
-                                                  const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
-                                                  const int* __restrict__ bin_start, int bin,
-                                                  const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
-                                                  PatOut po, DevStatus* st, int pblk) {
+template <typename OffT, int W, bool COMP, int S>
+__device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                              const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                              const int32_t* __restrict__ bc_len, const uint2* __restrict__ pairs,
+                                              const int32_t* __restrict__ perm, const int* __restrict__ bin_start,
+                                              int bin, const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
+                                              PatOut po, DevStatus* st, int pblk) {
     constexpr bool HT = S > 0;
     constexpr int NW = HT ? 2 * S : W / 32;   // bitmap words, or keys[S] | masks[S]
     constexpr int WB = NW + 64 + PAT_WORDS;  // words per warp: bitmap | rec[32] (int2) | list
@@ -809,7 +808,6 @@ __global__ void __launch_bounds__(256, S == 0 ? 4 : 1) k_sym_rows(const OffT* __
     const int stride = gridDim.x * warps;
     int r = r0 + blockIdx.x * warps + warp;
     if (r >= r1) return;
-    if (COMP != (st->use_comp != 0)) return;  // launched for the other mode
     uint32_t* hkeys = bm;      // HT
     uint32_t* hmask = bm + S;  // HT
     auto clear_all = [&]() {
@@ -1042,6 +1040,24 @@ __global__ void __launch_bounds__(256, S == 0 ? 4 : 1) k_sym_rows(const OffT* __
     }
 }
 
+// one launch for both compression modes (decided on the device in a1): the body is
+// instantiated for B_C pairs and for plain B entries
+template <typename OffT, int W, int S = 0>
+__global__ void __launch_bounds__(256, S == 0 ? 4 : 1) k_sym_rows(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+                                                  const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+                                                  const int32_t* __restrict__ bc_len,
+                                                  const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
+                                                  const int* __restrict__ bin_start, int bin,
+                                                  const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
+                                                  PatOut po, DevStatus* st, int pblk) {
+    if (st->use_comp)
+        sym_rows_body<OffT, W, true, S>(arm, aent, brm, bent, bc_len, pairs, perm, bin_start, bin, wlo, counts, po, st,
+                                        pblk);
+    else
+        sym_rows_body<OffT, W, false, S>(arm, aent, brm, bent, bc_len, pairs, perm, bin_start, bin, wlo, counts, po,
+                                         st, pblk);
+}
+
 // KK_SYM_ROWS=0 selects k_sym_window for the window bins (experiments)
 static bool use_sym_rows() {
     static const bool v = [] {
@@ -1055,26 +1071,17 @@ template <typename OffT, int W>
 static void launch_sym_rows(Launch& L, const SymArgs& a, int bin) {
     const int warps = 8;
     const size_t smem = (size_t)warps * ((size_t)W / 32 + 64 + PAT_WORDS) * 4;
-    // compression may be decided on the device (a1, comp_mode -1): then both kernels are
-    // launched and the one that does not match the device flag exits
-    auto kern = k_sym_rows<OffT, W, true>;
-    auto kern0 = k_sym_rows<OffT, W, false>;
+    auto kern = k_sym_rows<OffT, W>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
-    kernel_cfg(kern0, warps * 32, smem, L.num_sms);
     int64_t need = (a.A.nrows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
     const int64_t share = a.pat.cap / ((int64_t)grid * warps);
     const int pblk = (int)std::max<int64_t>(PAT_WORDS, std::min<int64_t>(2048, share));
     L.begin(kname("sym_rows", W), L.stream);
-    int nl = 0;
-    for (auto k : {kern, kern0}) {
-        if ((k == kern && a.comp_mode == 0) || (k == kern0 && a.comp_mode == 1)) continue;
-        k<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
-                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
-                                                a.counts, a.pat, (DevStatus*)a.st, pblk);
-        ++nl;
-    }
-    L.end(L.stream, nl);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+                                               a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
+                                               a.counts, a.pat, (DevStatus*)a.st, pblk);
+    L.end(L.stream);
 }
 
 template <typename OffT, int W>
@@ -1139,24 +1146,17 @@ template <typename OffT, int S>
 static void launch_sym_rows_ht(Launch& L, const SymArgs& a, int bin) {
     const int warps = S <= 1024 ? 8 : (S <= 2048 ? 4 : 2);
     const size_t smem = (size_t)warps * ((size_t)2 * S + 64 + PAT_WORDS) * 4;
-    auto kern = k_sym_rows<OffT, 32, true, S>;
-    auto kern0 = k_sym_rows<OffT, 32, false, S>;
+    auto kern = k_sym_rows<OffT, 32, S>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
-    kernel_cfg(kern0, warps * 32, smem, L.num_sms);
     int64_t need = (a.A.nrows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
     const int64_t share = a.pat.cap / ((int64_t)grid * warps);
     const int pblk = (int)std::max<int64_t>(PAT_WORDS, std::min<int64_t>(2048, share));
     L.begin(kname("sym_rows_ht", S), L.stream);
-    int nl = 0;
-    for (auto k : {kern, kern0}) {
-        if ((k == kern && a.comp_mode == 0) || (k == kern0 && a.comp_mode == 1)) continue;
-        k<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
-                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
-                                                a.counts, a.pat, (DevStatus*)a.st, pblk);
-        ++nl;
-    }
-    L.end(L.stream, nl);
+    kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+                                               a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
+                                               a.counts, a.pat, (DevStatus*)a.st, pblk);
+    L.end(L.stream);
 }
 
 // hash bins: rows with ub <= cap = 64 << (bin - 1) words; table S = 2 * cap
