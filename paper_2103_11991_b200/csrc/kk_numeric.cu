@@ -1428,7 +1428,11 @@ template <typename OffT, typename ValT, bool SORT>
 static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_stream) {
     const int drows = a.host_bin_start[NUM_DENSE_BIN + 1] - a.host_bin_start[NUM_DENSE_BIN];
     const size_t hsm = hub_smem(a.k);
-    if (drows > 0 && a.k > 25600 && hsm <= 220 * 1024) {
+    static const bool force_windowed = [] {  // KK_NUM_WINDOWED=1: windowed dense tier for all k
+        const char* v = getenv("KK_NUM_WINDOWED");
+        return v && v[0] == '1';
+    }();
+    if (drows > 0 && a.k > 25600 && hsm <= 220 * 1024 && !force_windowed) {
         // long rows, one column window would not do: bit vector over all of k (k_num_hub)
         auto kern = k_num_hub<OffT, ValT>;
         KCfg c = kernel_cfg(kern, HUB_THREADS, hsm, L.num_sms);
