@@ -60,6 +60,12 @@ def _load():
             lib.kko_jacobi_fill.argtypes = [ctypes.c_int64] * 2 + [_i64p, _i32p, _f64p, _i64p, _i32p, _f64p,
                                                                    ctypes.c_double, _f64p, _i64p, _i32p, _f64p,
                                                                    _f64p]
+            lib.kko_spadd_counts.restype = ctypes.c_int
+            lib.kko_spadd_counts.argtypes = [ctypes.c_int64] * 2 + [_i64p, _i32p, _i64p, _i32p, _i64p]
+            lib.kko_spadd_fill.restype = ctypes.c_int
+            lib.kko_spadd_fill.argtypes = [ctypes.c_int64] * 2 + [_i64p, _i32p, _f64p, _i64p, _i32p, _f64p,
+                                                                  ctypes.c_double, ctypes.c_double, _i64p, _i32p,
+                                                                  _f64p, _f64p]
             lib.kko_num_threads.restype = ctypes.c_int
             lib.kko_set_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
@@ -182,4 +188,31 @@ def jacobi(omega, dinv, A, B):
                            _p(bent, _i32p), _p(bval, _f64p), float(omega), _p(d, _f64p), _p(rm, _i64p),
                            _p(ent, _i32p), _p(val, _f64p), _p(bnd, _f64p)) != 0:
         raise ValueError("oracle jacobi: bad input")
+    return rm, ent[:nnz], val[:nnz], bnd[:nnz]
+
+
+def spadd(alpha, A, beta, B):
+    """SpAdd reference C = alpha A + beta B (Sec. 2.3): entries of equal
+    (row, column) merged, duplicates inside A or B included; rows sorted; structural pattern.
+    Returns (row_map[int64], entries[int32], values[f64], bound[f64]) with
+    bound = |alpha| sum|a| + |beta| sum|b|."""
+    lib = _load()
+    m, k, arm, aent, aval = _csr(A)
+    mb, kb, brm, bent, bval = _csr(B)
+    if m != mb or k != kb:
+        raise ValueError("SpAdd needs A and B of the same shape")
+    counts = np.zeros(max(m, 1), dtype=np.int64)
+    if lib.kko_spadd_counts(m, k, _p(arm, _i64p), _p(aent, _i32p), _p(brm, _i64p), _p(bent, _i32p),
+                            _p(counts, _i64p)) != 0:
+        raise ValueError("oracle spadd: bad input")
+    rm = np.zeros(m + 1, dtype=np.int64)
+    rm[1:] = np.cumsum(counts[:m])
+    nnz = int(rm[-1])
+    ent = np.zeros(max(nnz, 1), dtype=np.int32)
+    val = np.zeros(max(nnz, 1), dtype=np.float64)
+    bnd = np.zeros(max(nnz, 1), dtype=np.float64)
+    if lib.kko_spadd_fill(m, k, _p(arm, _i64p), _p(aent, _i32p), _p(aval, _f64p), _p(brm, _i64p), _p(bent, _i32p),
+                          _p(bval, _f64p), float(alpha), float(beta), _p(rm, _i64p), _p(ent, _i32p),
+                          _p(val, _f64p), _p(bnd, _f64p)) != 0:
+        raise ValueError("oracle spadd: bad input")
     return rm, ent[:nnz], val[:nnz], bnd[:nnz]

@@ -341,3 +341,47 @@ def test_jacobi_oracle_smoothed_aggregation_1d(oracle_mod):
         col = S[3 * c - 1: 3 * c + 4, c]
         assert np.allclose(col, [1 / 3, 2 / 3, 1.0, 2 / 3, 1 / 3], rtol=0, atol=1e-15)
         assert np.count_nonzero(S[:, c]) == 5
+
+
+# ---- SpAdd reference (Sec. 2.3) ------------------------------------------
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("kw", [{}, dict(sorted_rows=False), dict(duplicates=True, sorted_rows=False),
+                                dict(explicit_zeros=True)])
+def test_spadd_oracle_vs_dense(oracle_mod, seed, kw):
+    """alpha A + beta B against dense evaluation; pattern = Boolean union (structural, R1);
+    duplicates inside A or B merged."""
+    m, k = 40, 33
+    A = g.random_csr(m, k, 9, seed=seed, **kw)
+    B = g.random_csr(m, k, 12, seed=seed + 20, **kw)
+    al, be = 0.75, -1.5
+    rm, ent, val, bnd = oracle_mod.spadd(al, A, be, B)
+    Ad, Bd = A.to_dense().numpy(), B.to_dense().numpy()
+    pa = g.CSR(m, k, A.row_map, A.entries, torch.ones(A.nnz, dtype=torch.float64)).to_dense().numpy()
+    pb = g.CSR(m, k, B.row_map, B.entries, torch.ones(B.nnz, dtype=torch.float64)).to_dense().numpy()
+    pat = (pa + pb) > 0
+    assert np.array_equal(np.diff(rm), pat.sum(1))
+    for i in range(m):
+        assert np.array_equal(ent[rm[i]:rm[i + 1]], np.nonzero(pat[i])[0])
+    got = csr_to_dense_np(m, k, rm, ent, val)
+    absA = g.CSR(m, k, A.row_map, A.entries, A.values.abs()).to_dense().numpy()
+    absB = g.CSR(m, k, B.row_map, B.entries, B.values.abs()).to_dense().numpy()
+    bound = abs(al) * absA + abs(be) * absB
+    assert np.all(np.abs(got - (al * Ad + be * Bd)) <= 1e-15 * bound + 1e-300)
+    assert np.allclose(csr_to_dense_np(m, k, rm, ent, bnd), bound, rtol=1e-14, atol=0)
+
+
+def test_spadd_oracle_special_cases(oracle_mod):
+    """A + A = 2A on A's pattern; A - A keeps the structural zeros; adding an empty matrix
+    returns the merged, sorted A; empty shapes."""
+    A = g.random_csr(25, 30, 7, seed=9, duplicates=True, sorted_rows=False)
+    Z = g.random_csr(25, 30, 0, seed=1)
+    rmz, entz, valz, _ = oracle_mod.spadd(1.0, A, 1.0, Z)
+    rm2, ent2, val2, _ = oracle_mod.spadd(1.0, A, 1.0, A)
+    assert np.array_equal(rm2, rmz) and np.array_equal(ent2, entz) and np.array_equal(val2, 2 * valz)
+    rm0, ent0, val0, _ = oracle_mod.spadd(1.0, A, -1.0, A)
+    assert np.array_equal(rm0, rmz) and np.all(val0 == 0)
+    D = A.to_dense().numpy()
+    assert np.array_equal(csr_to_dense_np(25, 30, rmz, entz, valz), D)
+    rm, ent, val, _ = oracle_mod.spadd(2.0, g.random_csr(0, 5, 3, seed=1), 3.0, g.random_csr(0, 5, 3, seed=2))
+    assert list(rm) == [0] and len(ent) == 0
