@@ -167,6 +167,25 @@ kk_status_t kk_spgemm_jacobi_numeric(kk_spgemm_handle_t handle, double omega, co
                                      const kk_csr_t* B, const void* c_row_map, int32_t* c_entries, void* c_values,
                                      void* stream);
 
+/* SpAdd symbolic (Sec. 2.3.1, Alg. 1): C = alpha A + beta B for A, B of
+ * the same shape (else KK_ERR_DIM_MISMATCH) and offset type.  Fills c_row_map (device,
+ * A.nrows+1 of A.offset_type, caller-allocated), returns nnz(C) in *c_nnz (host), and keeps
+ * in the handle the scatter position of every entry of A and B in its row of C (the
+ * paper's Apos / Bpos).  Rows may be unsorted and unmerged (duplicate columns inside A or
+ * B are merged into one entry of C); C's pattern is the structural union.  Rows with
+ * nnz(A_i) + nnz(B_i) > 256 return KK_ERR_UNSUPPORTED_TYPE.  Synchronises `stream`. */
+kk_status_t kk_spadd_symbolic(kk_spgemm_handle_t handle, const kk_csr_t* A, const kk_csr_t* B, void* c_row_map,
+                              int64_t* c_nnz, void* stream);
+
+/* SpAdd numeric: writes C's sorted column indices (c_entries, device, nnz(C)
+ * int32) and values alpha*a + beta*b (c_values, device, A.value_type) by scattering A's and
+ * B's entries to the positions kept by kk_spadd_symbolic on the same patterns (same sizes,
+ * pointers, types, row map; else KK_ERR_STALE_HANDLE).  Values may change between calls.
+ * Asynchronous on `stream`. */
+kk_status_t kk_spadd_numeric(kk_spgemm_handle_t handle, double alpha, const kk_csr_t* A, double beta,
+                             const kk_csr_t* B, const void* c_row_map, int32_t* c_entries, void* c_values,
+                             void* stream);
+
 /* Per-kernel device times (opts.timing = 1).  One record per kernel (or fixed group of
  * launches, e.g. the three launches of a scan), accumulated since the last
  * kk_spgemm_timing_reset: number of launches, total and maximum duration in ms, from

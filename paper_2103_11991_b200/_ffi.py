@@ -79,11 +79,15 @@ def load() -> ctypes.CDLL:
         lib.kk_spgemm_numeric.argtypes = [H, P(kk_csr_t), P(kk_csr_t), _vp, _vp, _vp, _vp]
         lib.kk_spgemm_jacobi_numeric.argtypes = [H, ctypes.c_double, _vp, P(kk_csr_t), P(kk_csr_t), _vp, _vp, _vp,
                                                  _vp]
+        lib.kk_spadd_symbolic.argtypes = [H, P(kk_csr_t), P(kk_csr_t), _vp, P(_i64), _vp]
+        lib.kk_spadd_numeric.argtypes = [H, ctypes.c_double, P(kk_csr_t), ctypes.c_double, P(kk_csr_t), _vp, _vp,
+                                         _vp, _vp]
         lib.kk_spgemm_stats.argtypes = [H, P(kk_spgemm_stats_t)]
         lib.kk_spgemm_kernel_times.argtypes = [H, P(kk_kernel_time_t), P(ctypes.c_int)]
         lib.kk_spgemm_timing_reset.argtypes = [H]
         for fn in ("kk_spgemm_create", "kk_spgemm_destroy", "kk_spgemm_row_flops", "kk_spgemm_compress",
                    "kk_spgemm_symbolic", "kk_spgemm_numeric", "kk_spgemm_jacobi_numeric", "kk_spgemm_stats",
+                   "kk_spadd_symbolic", "kk_spadd_numeric",
                    "kk_spgemm_kernel_times",
                    "kk_spgemm_timing_reset"):
             getattr(lib, fn).restype = ctypes.c_int
@@ -161,6 +165,20 @@ def kk_spgemm_jacobi_numeric(h, omega: float, dinv_ptr: int, A: kk_csr_t, B: kk_
     _check(h, load().kk_spgemm_jacobi_numeric(h, float(omega), dinv_ptr or None, ctypes.byref(A), ctypes.byref(B),
                                               c_row_map_ptr or None, c_entries_ptr or None, c_values_ptr or None,
                                               stream or None))
+
+
+def kk_spadd_symbolic(h, A: kk_csr_t, B: kk_csr_t, c_row_map_ptr: int, stream: int) -> int:
+    nnz = _i64(0)
+    _check(h, load().kk_spadd_symbolic(h, ctypes.byref(A), ctypes.byref(B), c_row_map_ptr, ctypes.byref(nnz),
+                                       stream or None))
+    return int(nnz.value)
+
+
+def kk_spadd_numeric(h, alpha: float, A: kk_csr_t, beta: float, B: kk_csr_t, c_row_map_ptr: int,
+                     c_entries_ptr: int, c_values_ptr: int, stream: int) -> None:
+    _check(h, load().kk_spadd_numeric(h, float(alpha), ctypes.byref(A), float(beta), ctypes.byref(B),
+                                      c_row_map_ptr or None, c_entries_ptr or None, c_values_ptr or None,
+                                      stream or None))
 
 
 def kk_spgemm_stats(h) -> dict:

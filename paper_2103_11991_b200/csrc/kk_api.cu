@@ -103,7 +103,7 @@ struct kk_spgemm_handle_s {
     long long launches = 0;
     // workspace
     Buf flops, fscan, binid, perm_sym, perm_num, counts, binscratch, binstart, bc_len, pairs, cursors, partial,
-        status, bmeta, wlo, pat, pat_off, pat_len, diagchk;
+        status, bmeta, wlo, pat, pat_off, pat_len, diagchk, apos, bpos, spdup, spflag;
     DevStatus* h_status = nullptr;  // pinned
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -114,6 +114,13 @@ struct kk_spgemm_handle_s {
         const void *arm = nullptr, *aent = nullptr, *brm = nullptr, *bent = nullptr, *crm = nullptr;
         int offt = 0;
     } rec;
+    // record of the last SpAdd symbolic
+    struct AddRec {
+        bool valid = false;
+        int64_t m = 0, k = 0, nnzA = 0, nnzB = 0;
+        const void *arm = nullptr, *aent = nullptr, *brm = nullptr, *bent = nullptr, *crm = nullptr;
+        int offt = 0;
+    } addrec;
     int host_num_bin_start[kk::NB + 1] = {0};
     kk_spgemm_stats_t stats;
     kk::KTimer* timer = nullptr;
@@ -635,6 +642,95 @@ kk_status_t kk_spgemm_stats(kk_spgemm_handle_t h, kk_spgemm_stats_t* out) {
     for (const Buf* b : bufs) ws += (int64_t)b->bytes;
     out->workspace_bytes = ws;
     return KK_OK;
+}
+
+// ---- SpAdd (Sec. 2.3) -------------------------------------------------
+static kk_status_t check_add_pair(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, bool need_values) {
+    kk_status_t s;
+    if ((s = check_csr(h, A, "A", need_values)) != KK_OK) return s;
+    if ((s = check_csr(h, B, "B", need_values)) != KK_OK) return s;
+    if (A->nrows != B->nrows || A->ncols != B->ncols)
+        return fail(h, KK_ERR_DIM_MISMATCH, "SpAdd: A is %lld x %lld, B is %lld x %lld", (long long)A->nrows,
+                    (long long)A->ncols, (long long)B->nrows, (long long)B->ncols);
+    if (A->offset_type != B->offset_type)
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE, "A and B must use the same offset type");
+    if (need_values && A->value_type != B->value_type)
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE, "A and B must use the same value type");
+    return KK_OK;
+}
+
+kk_status_t kk_spadd_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, void* c_row_map,
+                              int64_t* c_nnz, void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    h->addrec.valid = false;
+    kk_status_t st;
+    if ((st = check_add_pair(h, A, B, false)) != KK_OK) return st;
+    if (!c_row_map) return fail(h, KK_ERR_INVALID_ARG, "c_row_map is NULL");
+    if (!c_nnz) return fail(h, KK_ERR_INVALID_ARG, "c_nnz is NULL");
+    cudaSetDevice(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t m = A->nrows;
+    const bool off64 = A->offset_type == KK_I64;
+    if ((st = ensure(h, h->status, sizeof(DevStatus), s)) != KK_OK) return st;
+    if ((st = ensure(h, h->counts, (size_t)m * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->partial, (size_t)kk::scan_partial_len(m) * 8, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->apos, (size_t)A->nnz * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->bpos, (size_t)B->nnz * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->spdup, (size_t)m, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->spflag, sizeof(int), s)) != KK_OK) return st;
+    DevStatus* dst = (DevStatus*)h->status.p;
+    kk::Launch L = make_launch(h, s);
+    kk::init_status(L, dst);
+    cudaMemsetAsync(h->spflag.p, 0, sizeof(int), s);
+    kk::spadd_symbolic(L, off64, m, view(A), view(B), (int32_t*)h->counts.p, (int32_t*)h->apos.p,
+                       (int32_t*)h->bpos.p, (uint8_t*)h->spdup.p, (int*)h->spflag.p);
+    kk::exclusive_scan(L, false, h->counts.p, off64, c_row_map, m, (int64_t*)h->partial.p, &dst->nnz_c,
+                       &dst->overflow);
+    cudaMemcpyAsync(h->h_status, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
+    int too_long = 0;
+    cudaMemcpyAsync(&too_long, h->spflag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if ((st = cuda_check(h, cudaGetLastError(), "kk_spadd_symbolic launch")) != KK_OK) return st;
+    if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spadd_symbolic sync")) != KK_OK) return st;
+    if (too_long)
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE, "SpAdd: a row has nnz(A_i) + nnz(B_i) > 256 (warp sort limit)");
+    if (h->h_status->overflow)
+        return fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) = %llu exceeds int32 row offsets; use KK_I64",
+                    (unsigned long long)h->h_status->nnz_c);
+    *c_nnz = (int64_t)h->h_status->nnz_c;
+    auto& R = h->addrec;
+    R.valid = true;
+    R.m = m;
+    R.k = A->ncols;
+    R.nnzA = A->nnz;
+    R.nnzB = B->nnz;
+    R.arm = A->row_map;
+    R.aent = A->entries;
+    R.brm = B->row_map;
+    R.bent = B->entries;
+    R.crm = c_row_map;
+    R.offt = (int)A->offset_type;
+    return KK_OK;
+}
+
+kk_status_t kk_spadd_numeric(kk_spgemm_handle_t h, double alpha, const kk_csr_t* A, double beta, const kk_csr_t* B,
+                             const void* c_row_map, int32_t* c_entries, void* c_values, void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    kk_status_t st;
+    if ((st = check_add_pair(h, A, B, true)) != KK_OK) return st;
+    const auto& R = h->addrec;
+    if (!R.valid || R.m != A->nrows || R.k != A->ncols || R.nnzA != A->nnz || R.nnzB != B->nnz ||
+        R.arm != A->row_map || R.aent != A->entries || R.brm != B->row_map || R.bent != B->entries ||
+        R.crm != c_row_map || R.offt != (int)A->offset_type)
+        return fail(h, KK_ERR_STALE_HANDLE, "spadd numeric: no matching spadd symbolic for these matrices / row map");
+    if (h->h_status->nnz_c > 0 && (!c_entries || !c_values))
+        return fail(h, KK_ERR_INVALID_ARG, "c_entries/c_values is NULL");
+    cudaSetDevice(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    kk::Launch L = make_launch(h, s);
+    kk::spadd_numeric(L, A->offset_type == KK_I64, A->value_type == KK_F64, A->nrows, alpha, view(A), beta, view(B),
+                      c_row_map, c_entries, c_values, (const int32_t*)h->apos.p, (const int32_t*)h->bpos.p,
+                      (const uint8_t*)h->spdup.p);
+    return cuda_check(h, cudaGetLastError(), "kk_spadd_numeric launch");
 }
 
 }  // extern "C"

@@ -161,6 +161,13 @@ struct NumArgs {
     double omega = 0.0;
 };
 void numeric_bins(Launch& L, const NumArgs& a, cudaStream_t dense_stream);
+// SpAdd (kk_spadd.cu): symbolic fills counts[m], apos[nnzA], bpos[nnzB], dup[m] (row has
+// an unmerged column); *too_long (device) set when a row has nnz(A_i) + nnz(B_i) > 256
+void spadd_symbolic(Launch& L, bool off64, int64_t m, const MatView& A, const MatView& B, int32_t* counts,
+                    int32_t* apos, int32_t* bpos, uint8_t* dup, int* too_long);
+void spadd_numeric(Launch& L, bool off64, bool f64, int64_t m, double alpha, const MatView& A, double beta,
+                   const MatView& B, const void* crm, int32_t* cent, void* cval, const int32_t* apos,
+                   const int32_t* bpos, const uint8_t* dup);
 // validate for the Jacobi-fused numeric: *missing (host) = rows of the square A without a
 // stored diagonal entry; scratch: one device int.  Synchronises L.stream.  false on a CUDA error.
 bool check_diagonal(Launch& L, bool off64, int64_t m, const void* row_map, const int32_t* entries, int* scratch,

@@ -153,6 +153,35 @@ class SpGEMM:
         ent, val = self.jacobi_numeric(omega, dinv, A, B, rm, nnz=nnz, stream=stream)
         return CsrMatrix(A.nrows, B.ncols, rm, ent, val)
 
+    # -- SpAdd ---------------------------------------------------------
+    def spadd_symbolic(self, A, B, c_row_map: Optional[torch.Tensor] = None, stream=None):
+        """Row pointers of C = alpha A + beta B and nnz(C); keeps the scatter positions."""
+        A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
+        a, b = _kk_csr(A, False), _kk_csr(B, False)
+        if c_row_map is None:
+            c_row_map = torch.empty(A.nrows + 1, dtype=A.row_map.dtype, device=A.row_map.device)
+        nnz = _ffi.kk_spadd_symbolic(self._h, a, b, c_row_map.data_ptr(), _stream_ptr(self.device, stream))
+        return c_row_map, nnz
+
+    def spadd_numeric(self, alpha: float, A, beta: float, B, c_row_map: torch.Tensor, nnz: int,
+                      c_entries: Optional[torch.Tensor] = None, c_values: Optional[torch.Tensor] = None, stream=None):
+        """Sorted columns and values alpha*a + beta*b of C (asynchronous)."""
+        A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
+        a, b = _kk_csr(A, True), _kk_csr(B, True)
+        if c_entries is None:
+            c_entries = torch.empty(nnz, dtype=torch.int32, device=A.row_map.device)
+        if c_values is None:
+            c_values = torch.empty(nnz, dtype=A.values.dtype, device=A.row_map.device)
+        _ffi.kk_spadd_numeric(self._h, alpha, a, beta, b, c_row_map.data_ptr(), c_entries.data_ptr() if nnz else 0,
+                              c_values.data_ptr() if nnz else 0, _stream_ptr(self.device, stream))
+        return c_entries, c_values
+
+    def spadd(self, alpha: float, A, beta: float, B, stream=None) -> CsrMatrix:
+        A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
+        rm, nnz = self.spadd_symbolic(A, B, stream=stream)
+        ent, val = self.spadd_numeric(alpha, A, beta, B, rm, nnz, stream=stream)
+        return CsrMatrix(A.nrows, A.ncols, rm, ent, val)
+
     def __call__(self, A, B, stream=None) -> CsrMatrix:
         A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
         rm, nnz = self.symbolic(A, B, stream=stream)
@@ -344,6 +373,16 @@ def spgemm_jacobi(omega: float, dinv: torch.Tensor, A, B, **opts) -> CsrMatrix:
     h = SpGEMM(**opts)
     try:
         return h.jacobi(omega, dinv, A, B)
+    finally:
+        torch.cuda.current_stream(h.device).synchronize()
+        h.close()
+
+
+def spadd(alpha: float, A, beta: float, B, **opts) -> CsrMatrix:
+    """One-shot SpAdd C = alpha A + beta B on the device."""
+    h = SpGEMM(**opts)
+    try:
+        return h.spadd(alpha, A, beta, B)
     finally:
         torch.cuda.current_stream(h.device).synchronize()
         h.close()
