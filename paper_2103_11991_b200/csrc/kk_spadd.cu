@@ -4,10 +4,10 @@
 // and B(i,:) become keys (col, matrix, index) that are sorted by column; the unique
 // columns are counted and every entry gets its scatter position Apos / Bpos in the row of
 // C.  The paper's team bitonic sort becomes a warp bitonic sort of 64-bit keys held E per
-// lane (rows with nnz(A_i) + nnz(B_i) <= 32E, E <= 8).  Sorted inputs take the same path:
-// a sort of already-sorted runs costs what the paper's bitonic merge does up to a constant,
-// and one path serves sorted, unsorted and unmerged rows alike.  A row map scan follows
-// (kk_setup.cu).
+// lane (rows with nnz(A_i) + nnz(B_i) <= 32E, E <= 8).  Sorted rows (checked per row) take
+// the paper's sorted-input path: A's keys followed by B's in reverse form
+// a bitonic sequence that the bitonic merge alone sorts (log2(32E) steps instead of the
+// full sort's log2(32E)(log2(32E)+1)/2).  A row map scan follows (kk_setup.cu).
 // Numeric: scatter alpha*a to Apos and beta*b to Bpos.  A warp owns a row
 // and accumulates it in shared memory (entries of A or B with equal columns -- unmerged
 // input -- add one at a time), then writes columns and values coalesced.
@@ -54,6 +54,36 @@ __device__ __forceinline__ void warp_bitonic_sort64(unsigned long long (&v)[E]) 
     }
 }
 
+// the final merge of the bitonic sort: a bitonic sequence of 32*E keys (ascending then
+// descending) sorted ascending in log2(32E) steps -- the paper's sorted-input SpAdd merge
+// (A's entries followed by B's entries in reverse)
+template <int E>
+__device__ __forceinline__ void warp_bitonic_merge64(unsigned long long (&v)[E]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 16 * E; j > 0; j >>= 1) {
+        if (j >= E) {
+            const int lj = j / E;
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const int e = lane * E + r;
+                const unsigned long long o = __shfl_xor_sync(FULL, v[r], lj);
+                v[r] = ((e & j) == 0) ? min(v[r], o) : max(v[r], o);
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const int pr = r ^ j;
+                if (pr > r) {
+                    const unsigned long long x = v[r], y = v[pr];
+                    v[r] = min(x, y);
+                    v[pr] = max(x, y);
+                }
+            }
+        }
+    }
+}
+
 // key = col << 9 | matrix << 8 | index in its row (index < 256)
 template <typename OffT, int E>
 __global__ void __launch_bounds__(256) k_spadd_symbolic(int64_t m, const OffT* __restrict__ arm,
@@ -73,19 +103,33 @@ __global__ void __launch_bounds__(256) k_spadd_symbolic(int64_t m, const OffT* _
             if (E == SPADD_MAXE && n > 32 * E && lane == 0) atomicExch(too_long, 1);
             continue;
         }
+        // A's keys ascending from position 0, B's from the end backwards, padding between:
+        // with sorted rows this is a bitonic sequence and the merge alone sorts it
         unsigned long long v[E];
+        constexpr int NP = 32 * E;
+        bool ok = true;  // the sequence is bitonic (ascending, then descending)
 #pragma unroll
         for (int r = 0; r < E; ++r) {
             const int e = lane * E + r;
             unsigned long long key = ~0ull;
             if (e < na)
                 key = ((unsigned long long)(uint32_t)__ldg(aent + sa + e) << 9) | (unsigned long long)e;
-            else if (e < n)
-                key = ((unsigned long long)(uint32_t)__ldg(bent + sb + (e - na)) << 9) | 256ull |
-                      (unsigned long long)(e - na);
+            else if (e >= NP - nb)
+                key = ((unsigned long long)(uint32_t)__ldg(bent + sb + (NP - 1 - e)) << 9) | 256ull |
+                      (unsigned long long)(NP - 1 - e);
             v[r] = key;
         }
-        warp_bitonic_sort64<E>(v);
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+            const int e = lane * E + r;
+            const unsigned long long nx = r + 1 < E ? v[r + 1 < E ? r + 1 : r] : __shfl_down_sync(FULL, v[0], 1);
+            if (e + 1 < na) ok &= v[r] <= nx;           // A ascending
+            if (e >= NP - nb && e + 1 < NP) ok &= v[r] >= nx;  // B (reversed) descending
+        }
+        if (__all_sync(FULL, ok))
+            warp_bitonic_merge64<E>(v);
+        else
+            warp_bitonic_sort64<E>(v);
         // heads of equal-column runs; a repeated (column, matrix) marks unmerged input
         const unsigned long long last_prev = __shfl_up_sync(FULL, v[E - 1], 1);
         int h[E];

@@ -409,6 +409,21 @@ def random_csr(m: int, n: int, max_row_nnz: int, seed: int = 1, sorted_rows: boo
     return CSR(m, n, row_map.to(device), cols.to(torch.int32).to(device), vals.to(device))
 
 
+def random_rows_csr(m: int, k: int, per_row: int, seed: int = 1, device="cpu") -> CSR:
+    """m x k CSR with `per_row` uniformly random columns in every row (vectorised; repeated
+    columns are kept as unmerged entries, rows sorted), values u in [-1, 1): the paper's
+    SpAdd test matrices ("each have 30 randomized entries per row")."""
+    nnz = m * per_row
+    pos = torch.arange(nnz, dtype=torch.int64)
+    rows = pos // max(per_row, 1)
+    cols = (uniform01(seed, pos, 31) * k).floor().to(torch.int64).clamp(max=max(k - 1, 0))
+    order = torch.argsort(rows * max(k, 1) + cols)
+    rows, cols = rows[order], cols[order]
+    vals = random_value(seed, rows, cols * 7 + pos)
+    row_map = torch.arange(0, nnz + 1, max(per_row, 1), dtype=torch.int64)[: m + 1]
+    return CSR(m, k, row_map.to(device), cols.to(torch.int32).to(device), vals.to(device))
+
+
 # ---------------------------------------------------------------------------
 # named workloads (BASELINE.json configs)
 # ---------------------------------------------------------------------------
