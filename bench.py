@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=None, help="rows of A in the oracle sample")
     ap.add_argument("--kernel-table", action="store_true", help="print the per-kernel timing table to stderr")
     ap.add_argument("--streams", type=int, default=2, help="library internal streams (1 = serialise the bins)")
+    ap.add_argument("--halo", action="store_true",
+                    help="N>1: B row-distributed, each rank fetches only the B rows its A block references "
+                         "(NEXT-2) instead of a broadcast of B")
     return ap.parse_args()
 
 
@@ -328,29 +331,52 @@ def run_ours(args):
     else:
         if args.config in ("C3", "C3J"):
             raise SystemExit(f"{args.config} is benchmarked on one GPU")
-        from paper_2103_11991_b200.parallel import broadcast_csr, flop_balanced_cuts, slice_rows
+        from paper_2103_11991_b200.parallel import broadcast_csr, flop_balanced_cuts, halo_exchange_b, slice_rows
 
-        if rank == 0:
-            B0 = conv(make_workload(args.config, args.size, args.values, dev)[1])
+        if args.halo:
+            # every rank holds its row block of B (here: generated whole, then sliced -- the
+            # input of a row-distributed solver) and fetches the rows its A block needs
+            full = conv(make_workload(args.config, args.size, args.values, dev)[1])
+            hf = SpGEMM(device=dev)
+            _, F, _ = hf.row_flops(full, full, scan=True, total=False)
+            hf.close()
+            cuts = flop_balanced_cuts(F.cpu().numpy(), world)
+            r0, r1 = cuts[rank], cuts[rank + 1]
+            A = slice_rows(full, r0, r1)
+            B_loc = slice_rows(full, r0, r1)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            B = halo_exchange_b(A, B_loc, cuts)
+            e1.record()
+            torch.cuda.synchronize()
+            t_bcast = e0.elapsed_time(e1)
+            A = CsrMatrix(A.nrows, A.ncols, A.row_map.contiguous(), A.entries.contiguous(), A.values.contiguous())
+            del full
+            mats = [A, B]
         else:
-            B0 = None
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        B = broadcast_csr(B0, src=0, device=dev)
-        e1.record()
-        torch.cuda.synchronize()
-        t_bcast = e0.elapsed_time(e1)
-        # A*A: A is B (a separate copy on every rank would only double memory; row block
-        # of the broadcast matrix, SURVEY §8e "A needs no extra traffic")
-        hf = SpGEMM(device=dev)
-        _, F, _ = hf.row_flops(B, B, scan=True, total=False)
-        hf.close()
-        cuts = flop_balanced_cuts(F.cpu().numpy(), world)
-        r0, r1 = cuts[rank], cuts[rank + 1]
-        A = slice_rows(B, r0, r1)
-        mats = [A, B]
+            if rank == 0:
+                B0 = conv(make_workload(args.config, args.size, args.values, dev)[1])
+            else:
+                B0 = None
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            B = broadcast_csr(B0, src=0, device=dev)
+            e1.record()
+            torch.cuda.synchronize()
+            t_bcast = e0.elapsed_time(e1)
+            # A*A: A is B (a separate copy on every rank would only double memory; row block
+            # of the broadcast matrix, SURVEY §8e "A needs no extra traffic")
+            hf = SpGEMM(device=dev)
+            _, F, _ = hf.row_flops(B, B, scan=True, total=False)
+            hf.close()
+            cuts = flop_balanced_cuts(F.cpu().numpy(), world)
+            r0, r1 = cuts[rank], cuts[rank + 1]
+            A = slice_rows(B, r0, r1)
+            mats = [A, B]
 
     stream = torch.cuda.current_stream(dev)
 
@@ -570,7 +596,8 @@ def run_ours(args):
                           "multiply_adds": int(muladds_all)},
                "hbm_gbs": round(hbm_gbs, 1), "hbm_frac": round(hbm_gbs / peak, 4),
                "phases_ms": {"symbolic": round(sym_ms_max, 4), "numeric": round(num_ms_max, 4),
-                             "broadcast_B": round(t_bcast, 3) if t_bcast is not None else None},
+                             "broadcast_B": round(t_bcast, 3) if t_bcast is not None else None,
+                             "B_exchange": (("halo" if args.halo else "broadcast") if world > 1 else None)},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                "clocks": clocks}
         print(json.dumps(out), flush=True)

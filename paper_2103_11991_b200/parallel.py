@@ -102,6 +102,102 @@ def allgather_nnz(nnz_local: int, device, group=None) -> List[int]:
     return [int(p.item()) for p in parts]
 
 
+def _all_to_all_var(send: torch.Tensor, send_counts: List[int], group=None) -> Tuple[torch.Tensor, List[int]]:
+    """Variable-size all-to-all of a 1-D tensor: send_counts[q] elements go to rank q.
+    NCCL: all_to_all_single; gloo (CPU tests): pairwise isend/irecv."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = send.device
+    sc = torch.tensor(send_counts, dtype=torch.int64, device=dev)
+    rc = torch.empty(world, dtype=torch.int64, device=dev)
+    if dist.get_backend(group) == "nccl":
+        dist.all_to_all_single(rc, sc, group=group)
+    else:
+        allc = [torch.zeros(world, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(allc, sc.cpu(), group=group)
+        rc = torch.stack([allc[q][rank] for q in range(world)]).to(dev)
+    recv_counts = [int(x) for x in rc.tolist()]
+    recv = torch.empty(sum(recv_counts), dtype=send.dtype, device=dev)
+    if dist.get_backend(group) == "nccl":
+        dist.all_to_all_single(recv, send, output_split_sizes=recv_counts, input_split_sizes=send_counts, group=group)
+    else:
+        so = [0]
+        for c in send_counts:
+            so.append(so[-1] + c)
+        ro = [0]
+        for c in recv_counts:
+            ro.append(ro[-1] + c)
+        reqs = []
+        for q in range(world):
+            if q == rank:
+                recv[ro[q]:ro[q + 1]] = send[so[q]:so[q + 1]]
+                continue
+            if send_counts[q]:
+                reqs.append(dist.isend(send[so[q]:so[q + 1]].contiguous(), q, group=group))
+            if recv_counts[q]:
+                buf = torch.empty(recv_counts[q], dtype=send.dtype, device=dev)
+                reqs.append((dist.irecv(buf, q, group=group), buf, ro[q]))
+        for r in reqs:
+            if isinstance(r, tuple):
+                r[0].wait()
+                recv[r[2]:r[2] + len(r[1])] = r[1]
+            else:
+                r.wait()
+    return recv, recv_counts
+
+
+def halo_exchange_b(A_local: CsrMatrix, B_local: CsrMatrix, b_cuts: Sequence[int], group=None) -> CsrMatrix:
+    """Halo-only B exchange: B is row-distributed
+    (rank q owns rows [b_cuts[q], b_cuts[q+1]) as B_local, row map rebased to 0); each rank
+    fetches only the B rows its A block references (the distinct column indices of A_local)
+    instead of a broadcast of all of B.  Returns a B of full shape (n x k) whose row map has
+    the fetched rows and empty rows elsewhere, so A_local's column indices need no remap and
+    the single-GPU SpGEMM applies unchanged.  Collectives: two variable all-to-alls for the
+    requests (row ids) and one each for the replies' row lengths, entries and values."""
+    world = dist.get_world_size(group)
+    dev = A_local.row_map.device
+    n = int(b_cuts[-1])
+    need = torch.unique(A_local.entries.to(torch.int64)) if A_local.nnz else torch.zeros(0, dtype=torch.int64,
+                                                                                          device=dev)
+    cuts_t = torch.tensor(list(b_cuts), dtype=torch.int64, device=dev)
+    owner = torch.searchsorted(cuts_t, need, right=True) - 1
+    req_counts = [int(x) for x in torch.bincount(owner, minlength=world).tolist()] if need.numel() else [0] * world
+    # requests: row ids (sorted, grouped by owner since `need` is sorted and cuts increase)
+    got_req, got_counts = _all_to_all_var(need, req_counts, group)
+    # serve: rows got_req (global ids in my range) -> lengths, entries, values
+    rank = dist.get_rank(group)
+    my0 = int(b_cuts[rank])
+    loc = got_req - my0
+    brm = B_local.row_map.to(torch.int64)
+    lens = (brm[loc + 1] - brm[loc]) if loc.numel() else torch.zeros(0, dtype=torch.int64, device=dev)
+    starts = brm[loc] if loc.numel() else torch.zeros(0, dtype=torch.int64, device=dev)
+    # gather the entries of the requested rows (in request order)
+    if lens.numel():
+        rows_rep = torch.repeat_interleave(torch.arange(lens.numel(), device=dev), lens)
+        offs_in = torch.cumsum(lens, 0) - lens
+        idx = starts[rows_rep] + (torch.arange(rows_rep.numel(), device=dev) - offs_in[rows_rep])
+        ent_out = B_local.entries[idx]
+        val_out = B_local.values[idx]
+    else:
+        ent_out = torch.zeros(0, dtype=torch.int32, device=dev)
+        val_out = torch.zeros(0, dtype=B_local.values.dtype, device=dev)
+    # reply sizes per requesting rank
+    ro = [0]
+    for c in got_counts:
+        ro.append(ro[-1] + c)
+    ent_counts = [int(lens[ro[q]:ro[q + 1]].sum()) for q in range(world)]
+    rlens, _ = _all_to_all_var(lens, got_counts, group)
+    rent, _ = _all_to_all_var(ent_out, ent_counts, group)
+    rval, _ = _all_to_all_var(val_out, ent_counts, group)
+    # assemble: full-shape row map with the fetched rows (need order = reply order)
+    rowlen = torch.zeros(n, dtype=torch.int64, device=dev)
+    if need.numel():
+        rowlen[need] = rlens
+    rm = torch.zeros(n + 1, dtype=B_local.row_map.dtype, device=dev)
+    rm[1:] = torch.cumsum(rowlen, 0).to(rm.dtype)
+    return CsrMatrix(n, B_local.ncols, rm, rent.to(torch.int32), rval)
+
+
 class ShardedSpGEMM:
     """C = A*B with rows of A block-distributed over the ranks of `group`.
 

@@ -112,3 +112,60 @@ def test_gloo_broadcast_and_allgather():
         assert r[1] == A.nrows and r[2] == A.ncols
         assert r[3] == A.row_map.tolist() and r[4] == A.entries.tolist() and r[5] == A.values.tolist()
         assert r[6] == [7, 17] and r[7] == [0, 7]
+
+
+def _halo_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_2103_11991_b200.parallel import halo_exchange_b, slice_rows
+        from paper_2103_11991_b200.spgemm import CsrMatrix
+
+        A, B = g.config("C2", size=7, values="random")
+        n = B.nrows
+        cuts = [n * p // world for p in range(world + 1)]
+        Bfull = CsrMatrix(B.nrows, B.ncols, B.row_map, B.entries, B.values)
+        Af = CsrMatrix(A.nrows, A.ncols, A.row_map, A.entries, A.values)
+        B_loc = slice_rows(Bfull, cuts[rank], cuts[rank + 1])
+        A_loc = slice_rows(Af, cuts[rank], cuts[rank + 1])
+        Bh = halo_exchange_b(A_loc, B_loc, cuts)
+        # the product of the local block with the fetched rows equals the rows of A*B
+        Ap = g.CSR(A_loc.nrows, A_loc.ncols, A_loc.row_map, A_loc.entries, A_loc.values)
+        Bp = g.CSR(Bh.nrows, Bh.ncols, Bh.row_map, Bh.entries, Bh.values)
+        rm, ent, val, _ = oracle.spgemm(Ap, Bp)
+        need = sorted(set(A_loc.entries.tolist()))
+        fetched = int(Bh.row_map[-1])
+        q.put((rank, rm.tolist(), ent.tolist(), val.tolist(), len(need), fetched,
+               int((B.row_map[1:] - B.row_map[:-1])[need].sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_halo_exchange(oracle_mod, world):
+    """NEXT-2: each rank fetches only the B rows its A block references; the local product
+    with the fetched rows equals its rows of the full product, and exactly the referenced
+    rows' entries travel."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A, B = g.config("C2", size=7, values="random")
+    rm_full, ent_full, val_full, _ = oracle_mod.spgemm(A, B)
+    n = B.nrows
+    cuts = [n * p // world for p in range(world + 1)]
+    for rank, rm, ent, val, nneed, fetched, want_fetched in res:
+        r0, r1 = cuts[rank], cuts[rank + 1]
+        s, e = int(rm_full[r0]), int(rm_full[r1])
+        assert np.array_equal(np.asarray(rm), rm_full[r0:r1 + 1] - s)
+        assert np.array_equal(np.asarray(ent, dtype=np.int32), ent_full[s:e])
+        assert np.array_equal(np.asarray(val), val_full[s:e])
+        assert fetched == want_fetched and nneed < n
