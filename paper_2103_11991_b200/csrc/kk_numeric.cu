@@ -1083,9 +1083,11 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
             if (lane + 32 < pl) wkeys[h1] = EMPTY;
         }
         for (int t = lane; t < clen; t += 32) {
-            cent[cb + t] = *(const int32_t*)(sm_rank + o_col + (uint32_t)t * 4u);
+            // C is written once and not read again here: streaming (evict-first) stores keep
+            // L2 for B's rows, which neighbouring rows of C read again
+            __stcs(cent + cb + t, *(const int32_t*)(sm_rank + o_col + (uint32_t)t * 4u));
             ValT* p = (ValT*)(sm_rank + o_val + (uint32_t)t * (uint32_t)sizeof(ValT));
-            cval[cb + t] = *p;
+            __stcs(cval + cb + t, *p);
             *p = (ValT)0;
         }
         __syncwarp();
