@@ -282,7 +282,7 @@ def run_reference(args):
            "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"{args.config}: {WORKLOADS[args.config]}", "values": args.values,
-                      "offsets": "int64"},
+                      "offsets": "int32" if offset_dtype_for(args.config) == torch.int32 else "int64"},
            "impl": "reference",
            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                             "sample": sample},
