@@ -16,7 +16,7 @@ cat $OUT/bench_$TAG.json; tail -30 $OUT/bench_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k regex:"num_rank<int, double, \(int\)128,|sym_rows<int, \(int\)49152, \(bool\)1" -s 2 -c 2 \
+    -k regex:"num_rank<int, double, \(int\)128,|sym_rows<int, \(int\)49152, \(int\)0" -s 2 -c 2 \
     -o /tmp/prof_top_$TAG -f python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 ncu -i /tmp/prof_top_$TAG.ncu-rep --page raw --csv > $OUT/raw_top_$TAG.csv 2>/dev/null
 ncu -i /tmp/prof_top_$TAG.ncu-rep --page source --csv --print-source sass > $OUT/sass_top_$TAG.csv 2>/dev/null
