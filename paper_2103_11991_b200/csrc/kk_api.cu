@@ -432,6 +432,10 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     kk::exclusive_scan(L, true, h->flops.p, true, h->fscan.p, m, (int64_t*)h->partial.p, nullptr, nullptr);
     // a3: bin rows by symbolic work
     kk::bin_rows(L, m, (const uint8_t*)h->binid.p, (int32_t*)h->binscratch.p, (int32_t*)h->perm_sym.p, sym_start);
+    // the symbolic bin sizes on the host (one sync): empty bins are not launched and grids
+    // are sized to their bins
+    cudaMemcpyAsync(h->h_status->sym_bin_start, sym_start, sizeof(int) * (kk::NB + 1), cudaMemcpyDeviceToHost, s);
+    if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_symbolic bins")) != KK_OK) return st;
     // a5: symbolic kernels per bin (dense bin on the side stream)
     kk::SymArgs sa;
     sa.off64 = off64;
@@ -445,7 +449,7 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     sa.counts = (int32_t*)h->counts.p;
     sa.cursors = (int32_t*)h->cursors.p;
     sa.wlo = (const int32_t*)h->wlo.p;
-    sa.host_bin_start = nullptr;
+    sa.host_bin_start = h->h_status->sym_bin_start;
     sa.pat.pat = keep_pat ? (uint2*)h->pat.p : nullptr;
     sa.pat.cap = pat_cap;
     sa.pat.off = keep_pat ? (long long*)h->pat_off.p : nullptr;

@@ -202,6 +202,11 @@ __global__ void __launch_bounds__(512) k_sym_dense(const OffT* __restrict__ arm,
 
 static int sym_warps_for(int S) { return S <= 512 ? 8 : (S == 1024 ? 4 : (S == 2048 ? 2 : 1)); }
 
+// rows of symbolic bin `bin` when the host holds the bin starts (else -1: launch anyway)
+static inline int64_t host_rows(const SymArgs& a, int bin) {
+    return a.host_bin_start ? (int64_t)a.host_bin_start[bin + 1] - a.host_bin_start[bin] : -1;
+}
+
 template <typename OffT, int S>
 static void launch_sym_warp(Launch& L, const SymArgs& a, int bin) {
     const int warps = sym_warps_for(S);
@@ -209,7 +214,9 @@ static void launch_sym_warp(Launch& L, const SymArgs& a, int bin) {
     auto kern = k_sym_warp<OffT, S>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int grid = c.grid_cap;
-    int64_t need = (a.A.nrows + warps - 1) / warps;
+    const int64_t hr = host_rows(a, bin);
+    if (hr == 0) return;
+    int64_t need = ((hr > 0 ? hr : a.A.nrows) + warps - 1) / warps;
     if (need < grid) grid = (int)(need > 0 ? need : 1);
     L.begin(kname("sym_warp", S), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
@@ -1073,7 +1080,9 @@ static void launch_sym_rows(Launch& L, const SymArgs& a, int bin) {
     const size_t smem = (size_t)warps * ((size_t)W / 32 + 64 + PAT_WORDS) * 4;
     auto kern = k_sym_rows<OffT, W>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
-    int64_t need = (a.A.nrows + warps - 1) / warps;
+    const int64_t hr = host_rows(a, bin);
+    if (hr == 0) return;
+    int64_t need = ((hr > 0 ? hr : a.A.nrows) + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
     const int64_t share = a.pat.cap / ((int64_t)grid * warps);
     const int pblk = (int)std::max<int64_t>(PAT_WORDS, std::min<int64_t>(2048, share));
@@ -1148,7 +1157,9 @@ static void launch_sym_rows_ht(Launch& L, const SymArgs& a, int bin) {
     const size_t smem = (size_t)warps * ((size_t)2 * S + 64 + PAT_WORDS) * 4;
     auto kern = k_sym_rows<OffT, 32, S>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
-    int64_t need = (a.A.nrows + warps - 1) / warps;
+    const int64_t hr = host_rows(a, bin);
+    if (hr == 0) return;
+    int64_t need = ((hr > 0 ? hr : a.A.nrows) + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
     const int64_t share = a.pat.cap / ((int64_t)grid * warps);
     const int pblk = (int)std::max<int64_t>(PAT_WORDS, std::min<int64_t>(2048, share));
@@ -1202,9 +1213,11 @@ __global__ void __launch_bounds__(256) k_sym_tiny(const OffT* __restrict__ arm, 
 
 template <typename OffT>
 static void launch_sym_tiny(Launch& L, const SymArgs& a) {
+    const int64_t hr = host_rows(a, SYM_TINY_BIN);
+    if (hr == 0) return;
     auto kern = k_sym_tiny<OffT>;
     KCfg c = kernel_cfg(kern, 256, 0, L.num_sms);
-    const int grid = (int)std::min<int64_t>((a.A.nrows + 255) / 256, c.grid_cap);
+    const int grid = (int)std::min<int64_t>(((hr > 0 ? hr : a.A.nrows) + 255) / 256, c.grid_cap);
     L.begin("sym_tiny", L.stream);
     kern<<<grid, 256, 0, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map, a.B.entries,
                                      a.perm, a.bin_start, SYM_TINY_BIN, a.counts);
@@ -1214,7 +1227,8 @@ static void launch_sym_tiny(Launch& L, const SymArgs& a) {
 template <typename OffT>
 static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stream) {
     // dense rows first (heaviest), on their own stream when given
-    {
+    const int64_t hdense = host_rows(a, SYM_DENSE_BIN);
+    if (hdense != 0) {
         const int threads = 512;
         int64_t wbits = 200 * 1024 * 8;  // 200 KB bit vector
         const int64_t k32 = ((a.k + 31) / 32) * 32;
@@ -1224,7 +1238,8 @@ static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stre
         KCfg c = kernel_cfg(kern, threads, smem, L.num_sms);
         cudaStream_t s = dense_stream ? dense_stream : L.stream;
         L.begin("sym_dense", s);
-        kern<<<c.grid_cap, threads, smem, s>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
+        const int grid = (int)(hdense > 0 ? std::min<int64_t>(hdense, c.grid_cap) : c.grid_cap);
+        kern<<<grid, threads, smem, s>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, SYM_DENSE_BIN,
                                                a.k, wbits, a.cursors, a.counts, a.st);
         L.end(s);
