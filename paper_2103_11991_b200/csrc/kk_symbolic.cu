@@ -802,7 +802,7 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
                                               const int32_t* __restrict__ bc_len, const uint2* __restrict__ pairs,
                                               const int32_t* __restrict__ perm, const int* __restrict__ bin_start,
                                               int bin, const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
-                                              PatOut po, DevStatus* st, int pblk) {
+                                              PatOut po, DevStatus* st, int pblk, int atom) {
     constexpr bool HT = S > 0;
     constexpr int NW = HT ? 2 * S : W / 32;   // bitmap words, or keys[S] | masks[S]
     constexpr int WB = NW + 64 + PAT_WORDS;  // words per warp: bitmap | rec[32] (int2) | list
@@ -919,7 +919,13 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
                     bool actn;
                     fetch(t + R, pn, actn);
                     uint32_t old = 0, tag = 0;
-                    if (COMP) {
+                    if (COMP && !HT && atom) {
+                        // all R rows in one round of shared atomic ORs: lanes sharing a word
+                        // are ordered by the atomics, so each new bit is counted once and
+                        // exactly one lane sees the word's old mask as 0 (default)
+                        old = rmw(p.x, p.y, act, false, tag);
+                        __syncwarp();
+                    } else if (COMP) {
                         // rows of a step may share words: one row per round
 #pragma unroll
                         for (int k = 0; k < R; ++k) {
@@ -1056,13 +1062,13 @@ __global__ void __launch_bounds__(256, S == 0 ? 4 : 1) k_sym_rows(const OffT* __
                                                   const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
                                                   const int* __restrict__ bin_start, int bin,
                                                   const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
-                                                  PatOut po, DevStatus* st, int pblk) {
+                                                  PatOut po, DevStatus* st, int pblk, int atom) {
     if (st->use_comp)
         sym_rows_body<OffT, W, true, S>(arm, aent, brm, bent, bc_len, pairs, perm, bin_start, bin, wlo, counts, po, st,
-                                        pblk);
+                                        pblk, atom);
     else
         sym_rows_body<OffT, W, false, S>(arm, aent, brm, bent, bc_len, pairs, perm, bin_start, bin, wlo, counts, po,
-                                         st, pblk);
+                                         st, pblk, atom);
 }
 
 // KK_SYM_ROWS=0 selects k_sym_window for the window bins (experiments)
@@ -1070,6 +1076,16 @@ static bool use_sym_rows() {
     static const bool v = [] {
         const char* s = getenv("KK_SYM_ROWS");
         return !(s && s[0] == '0');
+    }();
+    return v;
+}
+
+// Window rows take a step's B_C rows in one round of shared atomic ORs (default; C2
+// sym_rows 1.13 -> 1.04 ms); KK_SYM_ATOM=0 restores one plain read-OR-write round per row
+static int sym_atom() {
+    static const int v = [] {
+        const char* s = getenv("KK_SYM_ATOM");
+        return (s && s[0] == '0') ? 0 : 1;
     }();
     return v;
 }
@@ -1089,7 +1105,7 @@ static void launch_sym_rows(Launch& L, const SymArgs& a, int bin) {
     L.begin(kname("sym_rows", W), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
-                                               a.counts, a.pat, (DevStatus*)a.st, pblk);
+                                               a.counts, a.pat, (DevStatus*)a.st, pblk, sym_atom());
     L.end(L.stream);
 }
 
@@ -1166,7 +1182,7 @@ static void launch_sym_rows_ht(Launch& L, const SymArgs& a, int bin) {
     L.begin(kname("sym_rows_ht", S), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
-                                               a.counts, a.pat, (DevStatus*)a.st, pblk);
+                                               a.counts, a.pat, (DevStatus*)a.st, pblk, 0);
     L.end(L.stream);
 }
 
