@@ -24,7 +24,9 @@
  *   - C's pattern is the structural product: an entry exists wherever a stored
  *     A(i,j) meets a stored B(j,c), whatever the value (cancelled zeros are kept).
  *   - All device work is enqueued on `stream` (a cudaStream_t, 0 = legacy default).
- *     kk_spgemm_symbolic synchronises `stream` once, to return nnz(C) to the host.
+ *     kk_spgemm_symbolic synchronises `stream` twice: once to read the row-bin sizes
+ *     (so empty bins are not launched and grids fit their bins) and once to return
+ *     nnz(C) to the host.
  *     kk_spgemm_numeric is fully asynchronous.
  *   - Errors are returned as kk_status_t; nothing is thrown across the ABI.  On an
  *     error, kk_last_error_detail() gives a one-line description.
@@ -92,6 +94,8 @@ typedef struct {
     void* alloc_ctx;
 } kk_spgemm_opts_t;
 
+#define KK_STATS_MAX_BINS 24
+
 typedef struct {
     int64_t muladds;          /* sum_i sum_{j in A(i,:)} nnz(B(j,:)) */
     int64_t nnz_c;            /* row_map[m] of the last symbolic */
@@ -101,8 +105,8 @@ typedef struct {
     int b_strict;             /* 1 if every row of B was strictly increasing */
     int num_symbolic_bins;
     int num_numeric_bins;
-    int64_t symbolic_bin_rows[16]; /* rows per symbolic work bin */
-    int64_t numeric_bin_rows[16];  /* rows per numeric work bin */
+    int64_t symbolic_bin_rows[KK_STATS_MAX_BINS]; /* rows per symbolic work bin (num_symbolic_bins used) */
+    int64_t numeric_bin_rows[KK_STATS_MAX_BINS];  /* rows per numeric work bin (num_numeric_bins used) */
     int64_t kernel_launches;  /* total kernels this handle launched since creation */
     int64_t workspace_bytes;  /* bytes currently held */
 } kk_spgemm_stats_t;

@@ -17,6 +17,7 @@ KK_OK, KK_ERR_INVALID_ARG, KK_ERR_DIM_MISMATCH, KK_ERR_UNSUPPORTED_TYPE = 0, 1, 
 KK_ERR_INDEX_OVERFLOW, KK_ERR_STALE_HANDLE, KK_ERR_OUT_OF_MEMORY, KK_ERR_CUDA = 4, 5, 6, 7
 KK_I32, KK_I64 = 0, 1
 KK_F32, KK_F64 = 0, 1
+KK_STATS_MAX_BINS = 24  # include/kk_spgemm.h
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -40,8 +41,8 @@ class kk_spgemm_opts_t(ctypes.Structure):
 class kk_spgemm_stats_t(ctypes.Structure):
     _fields_ = [("muladds", _i64), ("nnz_c", _i64), ("compressed_words", _i64), ("compression_used", ctypes.c_int),
                 ("b_sorted", ctypes.c_int), ("b_strict", ctypes.c_int), ("num_symbolic_bins", ctypes.c_int),
-                ("num_numeric_bins", ctypes.c_int), ("symbolic_bin_rows", _i64 * 16),
-                ("numeric_bin_rows", _i64 * 16), ("kernel_launches", _i64), ("workspace_bytes", _i64)]
+                ("num_numeric_bins", ctypes.c_int), ("symbolic_bin_rows", _i64 * KK_STATS_MAX_BINS),
+                ("numeric_bin_rows", _i64 * KK_STATS_MAX_BINS), ("kernel_launches", _i64), ("workspace_bytes", _i64)]
 
 
 class kk_kernel_time_t(ctypes.Structure):

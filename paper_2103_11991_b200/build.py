@@ -55,12 +55,19 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
     cc = nvcc()
     objs = []
     jobs = []
+    hdr_t = max(os.path.getmtime(d) for d in _deps() if not d.endswith(".cu"))
     for src in _sources():
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         objs.append(obj)
+        # incremental: an object is rebuilt when it is missing or older than its source or
+        # any header (every .cu includes the shared headers)
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_t):
+            continue
         cmd = [cc] + ARCH + NVCC_FLAGS + (["-Xptxas", "-v"] if ptxas_v else []) + ["-c", src, "-o", obj]
         jobs.append(cmd)
-    with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
+    # the largest translation units first (they bound the parallel build)
+    jobs.sort(key=lambda c: -os.path.getsize(c[-3]))
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(8, len(jobs)))) as ex:
         futs = [ex.submit(subprocess.run, cmd, capture_output=True, text=True) for cmd in jobs]
         for cmd, f in zip(jobs, futs):
             r = f.result()

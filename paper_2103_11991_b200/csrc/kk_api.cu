@@ -1,10 +1,11 @@
 // kk_api.cu -- C ABI (include/kk_spgemm.h): handle, workspace, phase orchestration.
 //
 // Symbolic: init status -> a4 check/compress B -> a1 row flops + bins
-// -> a2 scan of flops -> a3 stable binning -> a5 per-bin symbolic kernels -> a6 scan of
-// counts into the caller's row map -> numeric bins from exact counts -> ONE device->host
-// copy of the status block + stream sync (nnz(C) must reach the host before C's arrays
-// can be allocated).
+// -> a2 scan of flops -> a3 stable binning -> host read of the symbolic bin sizes (sync 1:
+// empty bins are not launched and grids are sized to their bins) -> a5 per-bin symbolic
+// kernels -> a6 scan of counts into the caller's row map -> numeric bins from exact counts
+// -> device->host copy of the status block + stream sync (sync 2: nnz(C) must reach the
+// host before C's arrays can be allocated).
 // Numeric: per-bin numeric kernels with the fused sort; asynchronous.
 #include <cuda_runtime.h>
 
@@ -103,7 +104,11 @@ struct kk_spgemm_handle_s {
     long long launches = 0;
     // workspace
     Buf flops, fscan, binid, perm_sym, perm_num, counts, binscratch, binstart, bc_len, pairs, cursors, partial,
-        status, bmeta, wlo, pat, pat_off, pat_len, diagchk, apos, bpos, spdup, spflag;
+        status, bmeta, wlo, pat, pat_off, pat_len, diagchk, apos, bpos, spdup, spflag, status_aux;
+    // every workspace buffer, for destroy and stats (one list, so neither can miss one)
+    Buf* all_bufs[24] = {&flops,   &fscan,   &binid,   &perm_sym, &perm_num, &counts, &binscratch, &binstart,
+                         &bc_len,  &pairs,   &cursors, &partial,  &status,   &bmeta,  &wlo,        &pat,
+                         &pat_off, &pat_len, &diagchk, &apos,     &bpos,     &spdup,  &spflag,     &status_aux};
     DevStatus* h_status = nullptr;  // pinned
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -117,7 +122,7 @@ struct kk_spgemm_handle_s {
     // record of the last SpAdd symbolic
     struct AddRec {
         bool valid = false;
-        int64_t m = 0, k = 0, nnzA = 0, nnzB = 0;
+        int64_t m = 0, k = 0, nnzA = 0, nnzB = 0, nnzC = 0;
         const void *arm = nullptr, *aent = nullptr, *brm = nullptr, *bent = nullptr, *crm = nullptr;
         int offt = 0;
     } addrec;
@@ -299,10 +304,7 @@ kk_status_t kk_spgemm_destroy(kk_spgemm_handle_t h) {
     if (!h) return KK_ERR_INVALID_ARG;
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
-    Buf* bufs[] = {&h->flops, &h->fscan, &h->binid, &h->perm_sym, &h->perm_num, &h->counts, &h->binscratch,
-                   &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status,
-                   &h->bmeta, &h->wlo, &h->pat, &h->pat_off, &h->pat_len};
-    for (Buf* b : bufs) release(h, *b);
+    for (Buf* b : h->all_bufs) release(h, *b);
     delete h->timer;
     if (h->h_status) cudaFreeHost(h->h_status);
     if (h->side) cudaStreamDestroy(h->side);
@@ -331,9 +333,10 @@ kk_status_t kk_spgemm_compress(kk_spgemm_handle_t h, const kk_csr_t* B, int32_t*
     if (B->nnz > 0 && !pairs) return fail(h, KK_ERR_INVALID_ARG, "pairs is NULL");
     cudaSetDevice(h->device);
     cudaStream_t s = (cudaStream_t)stream;
-    if ((st = ensure(h, h->status, sizeof(DevStatus), s)) != KK_OK) return st;
+    // a status block of its own: the symbolic state numeric reads (B flags) stays intact
+    if ((st = ensure(h, h->status_aux, sizeof(DevStatus), s)) != KK_OK) return st;
     kk::Launch L = make_launch(h, s);
-    DevStatus* dst = (DevStatus*)h->status.p;
+    DevStatus* dst = (DevStatus*)h->status_aux.p;
     kk::init_status(L, dst);
     kk::check_compress(L, B->offset_type == KK_I64, view(B), B->ncols, true, h->opts.validate != 0, len,
                        (uint2*)pairs, nullptr, dst);
@@ -349,7 +352,7 @@ kk_status_t kk_spgemm_row_flops(kk_spgemm_handle_t h, const kk_csr_t* A, const k
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t m = A->nrows;
     const bool off64 = A->offset_type == KK_I64;
-    if ((st = ensure(h, h->status, sizeof(DevStatus), s)) != KK_OK) return st;
+    if ((st = ensure(h, h->status_aux, sizeof(DevStatus), s)) != KK_OK) return st;
     if ((st = ensure(h, h->binid, (size_t)m, s)) != KK_OK) return st;
     if ((st = ensure(h, h->counts, (size_t)m * 4, s)) != KK_OK) return st;
     if ((st = ensure(h, h->partial, (size_t)kk::scan_partial_len(m) * 8, s)) != KK_OK) return st;
@@ -359,18 +362,18 @@ kk_status_t kk_spgemm_row_flops(kk_spgemm_handle_t h, const kk_csr_t* A, const k
         f = (int64_t*)h->flops.p;
     }
     kk::Launch L = make_launch(h, s);
-    DevStatus* dst = (DevStatus*)h->status.p;
+    DevStatus* dst = (DevStatus*)h->status_aux.p;
     kk::init_status(L, dst);
     kk::row_flops_bin(L, off64, view(A), view(B), B->ncols, 0, h->opts.validate != 0, nullptr, nullptr, f,
                       (uint8_t*)h->binid.p, (int32_t*)h->counts.p, nullptr, dst);
     if (flops_scan) kk::exclusive_scan(L, true, f, true, flops_scan, m, (int64_t*)h->partial.p, nullptr, nullptr);
     if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_row_flops launch")) != KK_OK) return st;
     if (total) {
-        cudaMemcpyAsync(h->h_status, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
+        DevStatus hs;
+        cudaMemcpyAsync(&hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
         if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_row_flops sync")) != KK_OK) return st;
-        if (h->opts.validate && h->h_status->bad_index)
-            return fail(h, KK_ERR_INDEX_OVERFLOW, "column index of A out of range");
-        *total = (int64_t)h->h_status->total_flops;
+        if (h->opts.validate && hs.bad_index) return fail(h, KK_ERR_INDEX_OVERFLOW, "column index of A out of range");
+        *total = (int64_t)hs.total_flops;
     }
     return KK_OK;
 }
@@ -515,9 +518,10 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     S.b_strict = hs.b_strict;
     S.num_symbolic_bins = kk::SYM_NBINS;
     S.num_numeric_bins = kk::NUM_NBINS;
-    for (int b = 0; b < 16; ++b) {
-        S.symbolic_bin_rows[b] = b < kk::NB ? hs.sym_bin_start[b + 1] - hs.sym_bin_start[b] : 0;
-        S.numeric_bin_rows[b] = b < kk::NB ? hs.num_bin_start[b + 1] - hs.num_bin_start[b] : 0;
+    static_assert(kk::NB <= KK_STATS_MAX_BINS, "stats arrays must hold every bin");
+    for (int b = 0; b < KK_STATS_MAX_BINS; ++b) {
+        S.symbolic_bin_rows[b] = b < kk::SYM_NBINS ? hs.sym_bin_start[b + 1] - hs.sym_bin_start[b] : 0;
+        S.numeric_bin_rows[b] = b < kk::NUM_NBINS ? hs.num_bin_start[b + 1] - hs.num_bin_start[b] : 0;
     }
     return KK_OK;
 }
@@ -640,10 +644,7 @@ kk_status_t kk_spgemm_stats(kk_spgemm_handle_t h, kk_spgemm_stats_t* out) {
     *out = h->stats;
     out->kernel_launches = h->launches;
     int64_t ws = 0;
-    const Buf* bufs[] = {&h->flops, &h->fscan, &h->binid, &h->perm_sym, &h->perm_num, &h->counts, &h->binscratch,
-                         &h->binstart, &h->bc_len, &h->pairs, &h->cursors, &h->partial, &h->status,
-                         &h->bmeta, &h->wlo, &h->pat, &h->pat_off, &h->pat_len};
-    for (const Buf* b : bufs) ws += (int64_t)b->bytes;
+    for (const Buf* b : h->all_bufs) ws += (int64_t)b->bytes;
     out->workspace_bytes = ws;
     return KK_OK;
 }
@@ -675,14 +676,14 @@ kk_status_t kk_spadd_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t m = A->nrows;
     const bool off64 = A->offset_type == KK_I64;
-    if ((st = ensure(h, h->status, sizeof(DevStatus), s)) != KK_OK) return st;
+    if ((st = ensure(h, h->status_aux, sizeof(DevStatus), s)) != KK_OK) return st;
     if ((st = ensure(h, h->counts, (size_t)m * 4, s)) != KK_OK) return st;
     if ((st = ensure(h, h->partial, (size_t)kk::scan_partial_len(m) * 8, s)) != KK_OK) return st;
     if ((st = ensure(h, h->apos, (size_t)A->nnz * 4, s)) != KK_OK) return st;
     if ((st = ensure(h, h->bpos, (size_t)B->nnz * 4, s)) != KK_OK) return st;
     if ((st = ensure(h, h->spdup, (size_t)m, s)) != KK_OK) return st;
     if ((st = ensure(h, h->spflag, sizeof(int), s)) != KK_OK) return st;
-    DevStatus* dst = (DevStatus*)h->status.p;
+    DevStatus* dst = (DevStatus*)h->status_aux.p;
     kk::Launch L = make_launch(h, s);
     kk::init_status(L, dst);
     cudaMemsetAsync(h->spflag.p, 0, sizeof(int), s);
@@ -690,19 +691,21 @@ kk_status_t kk_spadd_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
                        (int32_t*)h->bpos.p, (uint8_t*)h->spdup.p, (int*)h->spflag.p);
     kk::exclusive_scan(L, false, h->counts.p, off64, c_row_map, m, (int64_t*)h->partial.p, &dst->nnz_c,
                        &dst->overflow);
-    cudaMemcpyAsync(h->h_status, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
+    DevStatus hs;
+    cudaMemcpyAsync(&hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
     int too_long = 0;
     cudaMemcpyAsync(&too_long, h->spflag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
     if ((st = cuda_check(h, cudaGetLastError(), "kk_spadd_symbolic launch")) != KK_OK) return st;
     if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spadd_symbolic sync")) != KK_OK) return st;
     if (too_long)
         return fail(h, KK_ERR_UNSUPPORTED_TYPE, "SpAdd: a row has nnz(A_i) + nnz(B_i) > 256 (warp sort limit)");
-    if (h->h_status->overflow)
+    if (hs.overflow)
         return fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) = %llu exceeds int32 row offsets; use KK_I64",
-                    (unsigned long long)h->h_status->nnz_c);
-    *c_nnz = (int64_t)h->h_status->nnz_c;
+                    (unsigned long long)hs.nnz_c);
+    *c_nnz = (int64_t)hs.nnz_c;
     auto& R = h->addrec;
     R.valid = true;
+    R.nnzC = (int64_t)hs.nnz_c;
     R.m = m;
     R.k = A->ncols;
     R.nnzA = A->nnz;
@@ -726,8 +729,7 @@ kk_status_t kk_spadd_numeric(kk_spgemm_handle_t h, double alpha, const kk_csr_t*
         R.arm != A->row_map || R.aent != A->entries || R.brm != B->row_map || R.bent != B->entries ||
         R.crm != c_row_map || R.offt != (int)A->offset_type)
         return fail(h, KK_ERR_STALE_HANDLE, "spadd numeric: no matching spadd symbolic for these matrices / row map");
-    if (h->h_status->nnz_c > 0 && (!c_entries || !c_values))
-        return fail(h, KK_ERR_INVALID_ARG, "c_entries/c_values is NULL");
+    if (R.nnzC > 0 && (!c_entries || !c_values)) return fail(h, KK_ERR_INVALID_ARG, "c_entries/c_values is NULL");
     cudaSetDevice(h->device);
     cudaStream_t s = (cudaStream_t)stream;
     kk::Launch L = make_launch(h, s);

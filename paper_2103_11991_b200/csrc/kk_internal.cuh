@@ -39,8 +39,9 @@ constexpr int PAT_DENSE_WORDS = 2048;  // widest word span of a pattern with a d
 constexpr int NUM_TINY_BIN = 16;
 constexpr int NUM_NBINS = 17;
 
-// Device-side status block.  Written by the kernels, copied to pinned host memory
-// once at the end of the symbolic phase (the phase's only device->host sync).
+// Device-side status block.  Written by the kernels, copied to pinned host memory at the
+// end of the symbolic phase (the phase's second device->host sync; the first reads the
+// symbolic bin sizes after binning).
 struct DevStatus {
     unsigned long long total_flops;   // sum_i flops_i
     unsigned long long total_words;   // |B_C| (pairs written by compression)

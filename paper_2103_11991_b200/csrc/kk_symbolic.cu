@@ -1080,15 +1080,9 @@ static bool use_sym_rows() {
     return v;
 }
 
-// Window rows take a step's B_C rows in one round of shared atomic ORs (default; C2
-// sym_rows 1.13 -> 1.04 ms); KK_SYM_ATOM=0 restores one plain read-OR-write round per row
-static int sym_atom() {
-    static const int v = [] {
-        const char* s = getenv("KK_SYM_ATOM");
-        return (s && s[0] == '0') ? 0 : 1;
-    }();
-    return v;
-}
+// Window rows take a step's B_C rows in one round of shared atomic ORs (C2 sym_rows 1.13
+// -> 1.04 ms against one plain read-OR-write round per row)
+static int sym_atom() { return 1; }
 
 template <typename OffT, int W>
 static void launch_sym_rows(Launch& L, const SymArgs& a, int bin) {

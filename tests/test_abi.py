@@ -26,10 +26,32 @@ def test_opts_default():
     assert (o.sort_rows, o.compression, o.validate, o.num_streams) == (1, -1, 0, 2)
 
 
-def test_struct_layout_matches_header():
-    # kk_csr_t: 3 x int64 + 2 enums + 3 pointers = 24 + 8 + 24
-    assert ctypes.sizeof(_ffi.kk_csr_t) == 56
-    assert ctypes.sizeof(_ffi.kk_spgemm_stats_t) == 8 * 3 + 4 * 6 + 8 * 32 + 16
+def test_struct_layout_matches_header(tmp_path):
+    """The ctypes structs have the sizes and field offsets the C compiler gives the header."""
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = {"kk_csr_t": _ffi.kk_csr_t, "kk_spgemm_opts_t": _ffi.kk_spgemm_opts_t,
+               "kk_spgemm_stats_t": _ffi.kk_spgemm_stats_t, "kk_kernel_time_t": _ffi.kk_kernel_time_t}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "kk_spgemm.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'  printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines) + "\n")
+    exe = tmp_path / "layout"
+    inc = os.path.join(os.path.dirname(os.path.dirname(_ffi.__file__)), "include")
+    subprocess.run([cc, "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
 
 
 def test_create_fails_cleanly_without_gpu():

@@ -2,9 +2,9 @@
 oracle on sampled rows (the oracle computes those rows one by one; it is not run on the
 whole product) plus properties that hold at any size.
 
-Opt-in (minutes, up to ~120 GB of device memory): KK_FULLSIZE=1 pytest -m gpu tests/test_gpu_fullsize.py
+Part of the default `pytest -m gpu` run (about half a minute, up to ~120 GB of device
+memory on the 180 GB B200).
 """
-import os
 
 import numpy as np
 import pytest
@@ -14,8 +14,7 @@ from workloads import generators as g
 
 from .helpers import assert_parity
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow,
-              pytest.mark.skipif(os.environ.get("KK_FULLSIZE") != "1", reason="set KK_FULLSIZE=1")]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
 def _dev(M, ot, vt=torch.float64):

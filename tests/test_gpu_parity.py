@@ -221,9 +221,10 @@ def test_errors():
 
 
 @pytest.mark.slow
-def test_C2_full_sampled(oracle_mod):
-    """BASELINE configs[1] at full size in the bench's launch configuration: bit-exact
-    counts/columns and exact integer values on a sample of rows (boundary + random)."""
+def test_C2_full(oracle_mod):
+    """BASELINE configs[1] at full size in the bench's launch configuration (int32 offsets,
+    fp64, integer values): the whole product against the oracle -- row map and columns
+    bit-exact, values exactly equal."""
     A, B = g.config("C2", device="cuda")
     from paper_2103_11991_b200 import SpGEMM
 
@@ -233,14 +234,107 @@ def test_C2_full_sampled(oracle_mod):
     ent, val = h.numeric(Ad, Bd, rm, nnz=nnz)
     torch.cuda.synchronize()
     assert nnz == 120553784 and h.stats()["muladds"] == 704969000
-    rng = np.random.default_rng(0)
-    rows = np.concatenate([np.arange(0, 300), np.arange(A.nrows - 300, A.nrows), rng.integers(0, A.nrows, 1500)])
     Ac, Bc = A.to(device="cpu"), B.to(device="cpu")
     got = (rm.cpu().numpy().astype(np.int64), ent.cpu().numpy(), val.cpu().numpy())
-    assert_parity(oracle_mod, Ac, Bc, got, rows=rows, exact=True)
-    # properties that hold at any size: rows strictly increasing, interior row sums zero
+    h.close()
+    del ent, val
+    assert_parity(oracle_mod, Ac, Bc, got, exact=True)
     lens = np.diff(got[0])
     assert lens.max() == 125 and int((lens == 125).sum()) == 96 ** 3
+
+
+def _diag_first(M):
+    """The same matrix with each row's diagonal entry stored first (rows otherwise in
+    column order): a partly unsorted B of the kind FEM assemblies produce."""
+    rm = M.row_map.to(torch.int64)
+    ent, val = M.entries.clone(), M.values.clone()
+    for i in range(M.nrows):
+        a, b = int(rm[i]), int(rm[i + 1])
+        row = ent[a:b]
+        d = (row == i).nonzero()
+        if len(d) == 0:
+            continue
+        p = int(d[0])
+        order = torch.cat([torch.tensor([p]), torch.arange(0, p), torch.arange(p + 1, b - a)])
+        ent[a:b] = row[order]
+        val[a:b] = val[a:b][order]
+    return g.CSR(M.nrows, M.ncols, M.row_map, ent, val)
+
+
+@pytest.mark.parametrize("compression", ["auto", "on", "off"])
+@pytest.mark.parametrize("values", ["int", "random"])
+def test_unsorted_diagonal_first(oracle_mod, compression, values):
+    """27-point stencil with the diagonal stored first in every row of A and B: rows of ~27
+    entries with one out-of-order word.  Compression must not be used on an unsorted B (the
+    compressor merges adjacent equal words only), whatever the option says."""
+    A, B = g.config("C2", size=12, values=values)
+    A, B = _diag_first(A), _diag_first(B)
+    for ot in (torch.int32, torch.int64):
+        got = gpu_spgemm(A, B, offset_dtype=ot, compression=compression)
+        assert_parity(oracle_mod, A, B, got, exact=(values == "int"))
+        assert got[3]["b_sorted"] == 0 and got[3]["compression_used"] == 0
+
+
+def test_index_overflow_int32():
+    """nnz(C) = 46,341^2 = 2,147,488,281 > INT32_MAX: the outer product of a 46,341 x 1
+    column of ones and a 1 x 46,341 row of ones.  int32 offsets -> KK_ERR_INDEX_OVERFLOW
+    from the i64 scan; int64 offsets -> the exact count and a correct C."""
+    from paper_2103_11991_b200 import SpGEMM, CsrMatrix
+    from paper_2103_11991_b200._ffi import KKError, KK_ERR_INDEX_OVERFLOW
+
+    n = 46341
+    dev = "cuda"
+
+    def col_ones(ot):
+        return CsrMatrix(n, 1, torch.arange(n + 1, device=dev, dtype=ot),
+                         torch.zeros(n, dtype=torch.int32, device=dev), torch.ones(n, dtype=torch.float64, device=dev))
+
+    def row_ones(ot):
+        return CsrMatrix(1, n, torch.tensor([0, n], device=dev, dtype=ot),
+                         torch.arange(n, dtype=torch.int32, device=dev), torch.ones(n, dtype=torch.float64, device=dev))
+
+    h = SpGEMM()
+    with pytest.raises(KKError) as e:
+        h.symbolic(col_ones(torch.int32), row_ones(torch.int32))
+    assert e.value.status == KK_ERR_INDEX_OVERFLOW
+    A, B = col_ones(torch.int64), row_ones(torch.int64)
+    rm, nnz = h.symbolic(A, B)
+    assert nnz == n * n == 2147488281
+    assert torch.equal(rm, torch.arange(n + 1, device=dev, dtype=torch.int64) * n)
+    ent, val = h.numeric(A, B, rm, nnz=nnz)
+    torch.cuda.synchronize()
+    cols = torch.arange(n, dtype=torch.int32, device=dev)
+    for r in (0, 1, n // 2, n - 2, n - 1):
+        assert torch.equal(ent[r * n:(r + 1) * n], cols), r
+        assert bool((val[r * n:(r + 1) * n] == 1.0).all()), r
+    # every entry: columns cycle 0..n-1, every value is 1 (blocks of rows, no 2^31-long temp)
+    for r0 in range(0, n, 4096):
+        r1 = min(n, r0 + 4096)
+        blk = ent[r0 * n:r1 * n].view(r1 - r0, n)
+        assert bool((blk == cols).all())
+        assert bool((val[r0 * n:r1 * n] == 1.0).all())
+    h.close()
+
+
+def test_hub_long_entry_list_overflow(oracle_mod):
+    """A hub row (k_num_hub, k > 25.6K) with more than HUB_LIST = 1,024 A entries whose B rows
+    each exceed HUB_LONG = 256 entries: the CTA-walked long-entry list overflows and the
+    remaining long rows take the overflow branch."""
+    rng = np.random.default_rng(17)
+    n, k, na, nb = 1300, 120000, 1100, 300
+    # A: row 0 references B rows 0..1099, row 1 a few, row 2 empty
+    a_rows = [np.arange(na), np.sort(rng.choice(n, 40, replace=False)), np.zeros(0, dtype=np.int64)]
+    arm = np.cumsum([0] + [len(r) for r in a_rows])
+    A = g.CSR(3, n, torch.tensor(arm), torch.tensor(np.concatenate(a_rows), dtype=torch.int32),
+              torch.tensor(rng.uniform(-1, 1, arm[-1])))
+    b_rows = [np.sort(rng.choice(k, nb + (j % 7), replace=False)) for j in range(n)]
+    brm = np.cumsum([0] + [len(r) for r in b_rows])
+    B = g.CSR(n, k, torch.tensor(brm), torch.tensor(np.concatenate(b_rows), dtype=torch.int32),
+              torch.tensor(rng.uniform(-1, 1, brm[-1])))
+    for ot in (torch.int32, torch.int64):
+        got = gpu_spgemm(A, B, offset_dtype=ot)
+        assert got[3]["numeric_bin_rows"][6] > 0
+        assert_parity(oracle_mod, A, B, got)
 
 
 def _banded(m, k, per_row, band, seed, values="random"):
