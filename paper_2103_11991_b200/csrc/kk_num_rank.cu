@@ -5,6 +5,7 @@
 #include "kk_numeric.cuh"
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace kk {
 // ------------------------------------------------------------------------------------
@@ -239,32 +240,77 @@ __global__ void __launch_bounds__(256, MINB) k_num_pattern(const OffT* __restric
 }
 
 // ------------------------------------------------------------------------------------
-// a7 for pattern rows with a dense word index, lean form (k_num_rank).  The method is
-// k_num_pattern's -- rank(c) = prefix(word(c)) + popc(mask & bits below c) from the
-// pattern kept by symbolic, accum = + into a dense per-row value array (PAPER.md:178,
-// Eq. 1) -- with the instruction stream cut down:
+// a7 for pattern rows, lean form (k_num_rank).  The method is k_num_pattern's -- the
+// output position of a product is the rank of its column in the pattern kept by symbolic,
+// rank(c) = prefix(word(c)) + popc(mask & bits below c), accum = + into a dense per-row
+// value array (Eq. 1) -- with the per-product work cut down:
+//   * dense word index (rows whose words span <= PAT_NWIN words): the prologue expands the
+//     pattern into a slot table rtab[word index][bit] -> value slot, so a product's slot is
+//     two dependent byte loads (word index, then rtab) and no popcount;
+//   * value slots are the ranks scattered by slot(r) = (SLOT_MUL * r) mod M (M the smallest
+//     prime above CAP), a bijection that breaks the arithmetic progressions of stencil
+//     ranks: the 27 ranks of a 27-point B row are 9 runs of 3 at a fixed stride, which in
+//     rank order put two lanes of a half-warp on one bank pair in every 8-byte access
+//     (4.0 -> 3.2 wavefronts per access, offline bank simulation on C2 rows);
 //   * each 32-entry A chunk becomes steps, one per 32-entry segment of its B rows (empty
 //     B rows give none, a row of L entries ceil(L/32)), 16-byte records in windows of 32;
 //   * steps are branch-free: lanes past the B row's end load a valid entry of it and
-//     accumulate into a dump slot vals[CAP], so no divergent region per step;
-//   * two steps per iteration, loads two steps ahead, and both steps' rank lookups are
+//     accumulate into a dump slot vals[NS], so no divergent region per step;
+//   * two steps per iteration, loads two steps ahead, and both steps' slot lookups are
 //     issued before either read-modify-write (the lookups only read the pattern tables);
-//   * the prologue writes each rank's column into shared memory once (one popcount scan
-//     of two 16-bit halves), and the epilogue writes entries and values coalesced.
-// Needs B.nnz < 2^31 (32-bit element offsets) and strictly increasing B rows.  HASHW: the
-// word index is a hash of the pattern's words (rows whose words span > PAT_NWIN words).
-// ------------------------------------------------------------------------------------
+//   * the epilogue writes entries and values coalesced, in rank order, from the slots.
+// Needs B.nnz < 2^31 (32-bit element offsets) and strictly increasing B rows.
 // HASHW: patterns whose words span more than PAT_NWIN words (wide rows, e.g. C5): the word
-// index is a PAT_SW-slot hash of the words (winfo indexed by hash slot) instead of a dense
-// u8 index over the window.
+// index is a PAT_SW-slot hash of the words and (mask, prefix) per hash slot gives the rank
+// by popcount (an rtab per hash slot would not fit); slots = ranks.
+// ------------------------------------------------------------------------------------
+template <int CAP>
+struct RankPrime;
+template <>
+struct RankPrime<32> {
+    static constexpr int M = 37;
+};
+template <>
+struct RankPrime<64> {
+    static constexpr int M = 67;
+};
+template <>
+struct RankPrime<128> {
+    static constexpr int M = 131;
+};
+template <>
+struct RankPrime<256> {
+    static constexpr int M = 257;
+};
+template <>
+struct RankPrime<512> {
+    static constexpr int M = 521;
+};
+constexpr uint32_t SLOT_MUL = 53;
+
 template <typename ValT, int CAP, bool HASHW = false>
 struct RankLayout {
-    static constexpr size_t vals = 0;  // CAP + 1 values (slot CAP: idle lanes)
-    static constexpr size_t cols = ((size_t)(CAP + 1) * sizeof(ValT) + 15) / 16 * 16;  // CAP int32
-    static constexpr size_t rec = cols + (size_t)CAP * 4;                                // 32 x {bb, len, a}
-    static constexpr size_t winfo = rec + 32 * 16;                  // (mask, prefix) per word / hash slot
-    static constexpr size_t widx = winfo + (size_t)(HASHW ? PAT_SW : PAT_W) * 8;  // u8 index | hash keys
+    static constexpr int NS = HASHW ? CAP : RankPrime<CAP>::M;  // value slots; slot NS: idle lanes
+    using SlotT = typename std::conditional<(NS < 255), uint8_t, uint16_t>::type;
+    static constexpr size_t vals = 0;                                                  // NS + 1 values
+    static constexpr size_t cols = ((size_t)(NS + 1) * sizeof(ValT) + 15) / 16 * 16;  // column per slot
+    static constexpr size_t rec = cols + ((size_t)NS * 4 + 15) / 16 * 16;             // 32 x {bb, len, a}
+    // HASHW: (mask, prefix) per hash slot; dense: rtab[PAT_W][32] slots, then (word, mask)
+    // per word index (the Jacobi insertion's pattern check)
+    static constexpr size_t winfo = rec + 32 * 16;
+    // rtab rows are RT = 36 entries apart (32 used): the 4-byte word holding (word index wi,
+    // bit b) is 9*wi + b/4 (u8), so the rows of the ~9 words a B row touches spread over
+    // the banks instead of landing on 4 bank groups (32-entry rows: bank = 8*wi + b/4)
+    static constexpr uint32_t RT = 36;
+    static constexpr size_t pw = winfo + (HASHW ? (size_t)PAT_SW * 8 : ((size_t)PAT_W * RT * sizeof(SlotT) + 15) / 16 * 16);
+    static constexpr size_t widx = pw + (HASHW ? 0 : (size_t)PAT_W * 8);              // u8 index | hash keys
     static constexpr size_t bytes = (widx + (HASHW ? (size_t)PAT_SW * 4 : (size_t)PAT_NWIN) + 15) / 16 * 16;
+    __device__ static __forceinline__ uint32_t slot(uint32_t r) {
+        if constexpr (HASHW)
+            return r;
+        else
+            return (SLOT_MUL * r) % (uint32_t)NS;
+    }
 };
 
 template <typename OffT, typename ValT, int CAP, int MINB, bool HASHW>
@@ -278,17 +324,20 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                                                         const int* __restrict__ pat_len, const ValT* __restrict__ dinv,
                                                         double omega) {
     using LY = RankLayout<ValT, CAP, HASHW>;
+    using SlotT = typename LY::SlotT;
+    constexpr uint32_t NS = (uint32_t)LY::NS;
     extern __shared__ __align__(16) unsigned char sm_rank[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
     // all shared accesses as sm_rank + 32-bit offset (shared addressing, no generic)
     const uint32_t o_w = (uint32_t)warp * (uint32_t)LY::bytes;
     const uint32_t o_val = o_w + (uint32_t)LY::vals, o_col = o_w + (uint32_t)LY::cols;
     const uint32_t o_rec = o_w + (uint32_t)LY::rec, o_inf = o_w + (uint32_t)LY::winfo;
+    const uint32_t o_pw = o_w + (uint32_t)LY::pw;
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     const int stride = gridDim.x * warps;
     int r = r0 + blockIdx.x * warps + warp;
     if (r >= r1) return;
-    for (int t = lane; t < CAP; t += 32) *(ValT*)(sm_rank + o_val + t * (uint32_t)sizeof(ValT)) = (ValT)0;
+    for (uint32_t t = lane; t <= NS; t += 32) *(ValT*)(sm_rank + o_val + t * (uint32_t)sizeof(ValT)) = (ValT)0;
     uint32_t* wkeys = (uint32_t*)(sm_rank + o_w + (uint32_t)LY::widx);  // HASHW only
     if (HASHW)
         for (int t = lane; t < PAT_SW; t += 32) wkeys[t] = EMPTY;
@@ -301,7 +350,7 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
         const int clen = (int)(ld(crm, i + 1) - cb);
         const long long po = __ldg(pat_off + i);
         const int pl = __ldg(pat_len + i);
-        // ---- the row's pattern: (mask, prefix) per word, word index, column of each rank ----
+        // ---- the row's pattern: word index, slot table (or (mask, prefix)), column per slot ----
         const uint2 p0 = lane < pl ? __ldg(pat + po + lane) : make_uint2(0u, 0u);
         uint2 p1 = make_uint2(0u, 0u);
         if (pl > 32 && lane + 32 < pl) p1 = __ldg(pat + po + 32 + lane);
@@ -318,51 +367,55 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
         const uint32_t wb = __shfl_sync(FULL, p0.x, 0);
         const uint32_t o_idx = o_w + (uint32_t)LY::widx - wb;
         __syncwarp();
-        // word -> (mask, prefix) slot: dense u8 index, or the hash slot of the word
+        // word -> slot-table row: dense u8 index (row = word index), or the hash slot of the word
         uint32_t h0 = (uint32_t)lane, h1 = (uint32_t)lane + 32u;
         if constexpr (HASHW) {
             h0 = wt_insert(wkeys, p0.x, lane < pl);
             h1 = wt_insert(wkeys, p1.x, lane + 32 < pl);
         }
-        if (lane < pl) {
-            if constexpr (!HASHW) sm_rank[o_idx + p0.x] = (uint8_t)lane;
-            *(uint2*)(sm_rank + o_inf + h0 * 8u) = make_uint2(p0.y, (uint32_t)pre0);
-            uint32_t m = p0.y;
-            uint32_t o = o_col + (uint32_t)pre0 * 4u;
-            while (m) {
-                *(int32_t*)(sm_rank + o) = (int32_t)(p0.x * 32u + (uint32_t)(__ffs(m) - 1));
-                m &= m - 1;
-                o += 4;
+        auto expand = [&](uint2 p, uint32_t h, int pre) {
+            if constexpr (HASHW) {
+                *(uint2*)(sm_rank + o_inf + h * 8u) = make_uint2(p.y, (uint32_t)pre);
+            } else {
+                sm_rank[o_idx + p.x] = (uint8_t)h;
+                if (dinv) *(uint2*)(sm_rank + o_pw + h * 8u) = p;
             }
-        }
-        if (lane + 32 < pl) {
-            if constexpr (!HASHW) sm_rank[o_idx + p1.x] = (uint8_t)(lane + 32);
-            *(uint2*)(sm_rank + o_inf + h1 * 8u) = make_uint2(p1.y, (uint32_t)pre1);
-            uint32_t m = p1.y;
-            uint32_t o = o_col + (uint32_t)pre1 * 4u;
+            uint32_t m = p.y;
+            uint32_t rk = (uint32_t)pre;
             while (m) {
-                *(int32_t*)(sm_rank + o) = (int32_t)(p1.x * 32u + (uint32_t)(__ffs(m) - 1));
+                const uint32_t b = (uint32_t)(__ffs(m) - 1);
+                const uint32_t sl = LY::slot(rk);
+                *(int32_t*)(sm_rank + o_col + sl * 4u) = (int32_t)(p.x * 32u + b);
+                if constexpr (!HASHW) *(SlotT*)(sm_rank + o_inf + (h * LY::RT + b) * (uint32_t)sizeof(SlotT)) = (SlotT)sl;
                 m &= m - 1;
-                o += 4;
+                ++rk;
             }
-        }
+        };
+        if (lane < pl) expand(p0, h0, pre0);
+        if (lane + 32 < pl) expand(p1, h1, pre1);
         __syncwarp();
-        auto rank = [&](int col, bool valid) -> uint32_t {
-            uint32_t wi;
+        // value slot of a column of the pattern
+        auto slot_of = [&](int col, bool valid) -> uint32_t {
+            uint32_t sl;
             if constexpr (HASHW) {
                 const uint32_t w = (uint32_t)col >> 5;
-                wi = wt_slot(w);
+                uint32_t wi = wt_slot(w);
                 while (wkeys[wi] != w) wi = (wi + 1) & (PAT_SW - 1);  // present: no empty-slot test
+                const uint2 mp = *(const uint2*)(sm_rank + o_inf + wi * 8u);
+                sl = mp.y + __popc(mp.x & ~(0xffffffffu << (col & 31)));
             } else {
-                wi = sm_rank[o_idx + ((uint32_t)col >> 5)];
+                const uint32_t wi = sm_rank[o_idx + ((uint32_t)col >> 5)];
+                sl = *(const SlotT*)(sm_rank + o_inf + (wi * LY::RT + ((uint32_t)col & 31u)) * (uint32_t)sizeof(SlotT));
             }
-            const uint2 mp = *(const uint2*)(sm_rank + o_inf + wi * 8u);
-            const uint32_t rk = mp.y + __popc(mp.x & ~(0xffffffffu << (col & 31)));
-            return valid ? rk : (uint32_t)CAP;
+            return valid ? sl : NS;
         };
-        auto acc = [&](uint32_t rk, ValT prod) {
-            ValT* p = (ValT*)(sm_rank + o_val + rk * (uint32_t)sizeof(ValT));
-            *p += prod;
+        // idle lanes (past the B row's end) are predicated off: a common dump slot would sit
+        // on the bank pair of real slots and cost a wavefront in the second half-warp
+        auto acc = [&](uint32_t sl, ValT prod) {
+            if (sl < NS) {
+                ValT* q = (ValT*)(sm_rank + o_val + sl * (uint32_t)sizeof(ValT));
+                *q += prod;
+            }
         };
         // ---- products, one 32-entry A chunk at a time ----
         // A step is one 32-entry segment of a B row (a B row of L entries gives ceil(L/32)
@@ -393,7 +446,7 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                 load(0, colA, bA, aA, vA);
                 load(1, colB, bB, aB, vB);
                 for (int t = 0; t < nt; t += 2) {
-                    const uint32_t rA = rank(colA, vA), rB = rank(colB, vB);
+                    const uint32_t rA = slot_of(colA, vA), rB = slot_of(colB, vB);
                     const ValT pA = aA * bA, pB = aB * bB;
                     if (t + 2 < nt) {
                         load(t + 2, colA, bA, aA, vA);
@@ -444,43 +497,52 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
         if (dinv) {
             // Jacobi-fused row: C(i,:) = B(i,:) - omega D^-1(i) E(i,:).
             // E(i,:) is scaled once per entry by the row's scalar, then B(i,:) is added at
-            // its ranks (its columns lie in E's pattern when A(i,i) is stored).
+            // its slots (its columns lie in E's pattern when A(i,i) is stored).
             const ValT sc = (ValT)(-omega * (double)__ldg(dinv + i));
-            for (int t = lane; t < clen; t += 32) *(ValT*)(sm_rank + o_val + (uint32_t)t * (uint32_t)sizeof(ValT)) *= sc;
+            for (int t = lane; t < clen; t += 32) {
+                ValT* q = (ValT*)(sm_rank + o_val + LY::slot((uint32_t)t) * (uint32_t)sizeof(ValT));
+                *q *= sc;
+            }
             __syncwarp();
             const int bs = (int)ld(brm, i), bl = (int)(ld(brm, i + 1) - bs);
             for (int q0 = 0; q0 < bl; q0 += 32) {
                 const bool valid = q0 + lane < bl;
                 const int q = bs + min(q0 + lane, bl - 1);
                 const int col = __ldg(bent + q);
-                // a word outside the dense index's range is not in the pattern
-                bool inpat = HASHW || ((uint32_t)col >> 5) - wb < (uint32_t)PAT_NWIN;
+                const uint32_t w = (uint32_t)col >> 5;
+                // a column outside the pattern (A(i,i) not stored) must not land on a slot
+                bool inpat;
                 if constexpr (HASHW) {
-                    // the word must be present before probing (no empty-slot test in rank())
-                    const uint32_t w = (uint32_t)col >> 5;
+                    // the word must be present before probing (no empty-slot test in slot_of)
                     uint32_t wi = wt_slot(w);
                     while (wkeys[wi] != w && wkeys[wi] != EMPTY) wi = (wi + 1) & (PAT_SW - 1);
-                    inpat = wkeys[wi] == w;
+                    inpat = wkeys[wi] == w && ((*(const uint2*)(sm_rank + o_inf + wi * 8u)).x >> (col & 31)) & 1u;
+                } else {
+                    // the dense index may hold a stale entry: check the indexed word itself
+                    inpat = w - wb < (uint32_t)PAT_NWIN;
+                    if (inpat) {
+                        const uint32_t wi = sm_rank[o_idx + w];
+                        const uint2 pwm = *(const uint2*)(sm_rank + o_pw + (wi & 63u) * 8u);
+                        inpat = wi < (uint32_t)pl && pwm.x == w && ((pwm.y >> (col & 31)) & 1u);
+                    }
                 }
-                uint32_t rk = rank(inpat ? col : (int)(wb * 32u), valid && inpat);
-                // a column outside the pattern (A(i,i) not stored) must not land on another rank
-                if (rk < (uint32_t)CAP && *(const int32_t*)(sm_rank + o_col + rk * 4u) != col) rk = CAP;
-                acc(rk, __ldg(bval + q));
+                acc(slot_of(inpat ? col : 0, valid && inpat), __ldg(bval + q));
                 __syncwarp();
             }
         }
-        // ---- entries and values, coalesced; reset ----
+        // ---- entries and values in rank order, coalesced; reset ----
         if (HASHW) {
             if (lane < pl) wkeys[h0] = EMPTY;
             if (lane + 32 < pl) wkeys[h1] = EMPTY;
         }
         for (int t = lane; t < clen; t += 32) {
+            const uint32_t sl = LY::slot((uint32_t)t);
             // C is written once and not read again here: streaming (evict-first) stores keep
             // L2 for B's rows, which neighbouring rows of C read again
-            __stcs(cent + cb + t, *(const int32_t*)(sm_rank + o_col + (uint32_t)t * 4u));
-            ValT* p = (ValT*)(sm_rank + o_val + (uint32_t)t * (uint32_t)sizeof(ValT));
-            __stcs(cval + cb + t, *p);
-            *p = (ValT)0;
+            __stcs(cent + cb + t, *(const int32_t*)(sm_rank + o_col + sl * 4u));
+            ValT* q = (ValT*)(sm_rank + o_val + sl * (uint32_t)sizeof(ValT));
+            __stcs(cval + cb + t, *q);
+            *q = (ValT)0;
         }
         __syncwarp();
         if (inext < 0) break;

@@ -52,7 +52,7 @@ def _run_case(name):
             rm, nnz = h.symbolic(Ad, Bd)
             ent, val = h.numeric(Ad, Bd, rm, nnz=nnz)
             torch.cuda.synchronize()
-            names |= {k["name"] for k in h.kernel_times()}
+            names |= {k[0] for k in h.kernel_times()}
             got = (rm.cpu().numpy().astype(np.int64), ent.cpu().numpy(), val.cpu().double().numpy())
             assert_parity(oracle, A, B, got, value_dtype=vt)
             h.close()
@@ -67,7 +67,7 @@ def test_fallback_kernels(case):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     names = set(json.loads(r.stdout.strip().splitlines()[-1]))
     assert not any(n.startswith("num_rank") or n.startswith("sym_rows") for n in names), names
-    if case in ("C2", "C5", "banded", "wide"):
+    if case in ("C2", "C5", "wide"):
         assert any(n.startswith("num_pattern") for n in names), names
     if case in ("C2", "banded"):
         assert any(n.startswith("sym_window") for n in names), names
