@@ -104,11 +104,12 @@ struct kk_spgemm_handle_s {
     long long launches = 0;
     // workspace
     Buf flops, fscan, binid, perm_sym, perm_num, counts, binscratch, binstart, bc_len, pairs, cursors, partial,
-        status, bmeta, wlo, pat, pat_off, pat_len, diagchk, apos, bpos, spdup, spflag, status_aux;
+        status, bmeta, wlo, pat, pat_off, pat_len, diagchk, apos, bpos, spdup, spflag, status_aux, workctr;
     // every workspace buffer, for destroy and stats (one list, so neither can miss one)
-    Buf* all_bufs[24] = {&flops,   &fscan,   &binid,   &perm_sym, &perm_num, &counts, &binscratch, &binstart,
+    Buf* all_bufs[25] = {&flops,   &fscan,   &binid,   &perm_sym, &perm_num, &counts, &binscratch, &binstart,
                          &bc_len,  &pairs,   &cursors, &partial,  &status,   &bmeta,  &wlo,        &pat,
-                         &pat_off, &pat_len, &diagchk, &apos,     &bpos,     &spdup,  &spflag,     &status_aux};
+                         &pat_off, &pat_len, &diagchk, &apos,     &bpos,     &spdup,  &spflag,     &status_aux,
+                         &workctr};
     DevStatus* h_status = nullptr;  // pinned
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -545,6 +546,9 @@ static kk_status_t numeric_impl(kk_spgemm_handle_t h, const kk_csr_t* A, const k
     na.f64 = A->value_type == KK_F64;
     na.sort = h->opts.sort_rows != 0;
     na.strict = h->stats.b_strict != 0;
+    na.sorted = h->stats.b_sorted != 0;
+    if ((st = ensure(h, h->workctr, 16, s)) != KK_OK) return st;
+    na.work_ctr = (int*)h->workctr.p;
     na.wlo = (const int32_t*)h->wlo.p;
     na.pat = (const uint2*)h->pat.p;
     na.pat_off = (const long long*)h->pat_off.p;

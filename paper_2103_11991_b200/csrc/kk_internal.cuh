@@ -142,6 +142,8 @@ void symbolic_bins(Launch& L, const SymArgs& a, cudaStream_t dense_stream);
 struct NumArgs {
     bool off64, f64, sort;
     bool strict;                 // every B row strictly increasing (host copy of the a4 flag)
+    bool sorted;                 // every B row non-decreasing (host copy of the a4 flag)
+    int* work_ctr = nullptr;     // device scratch: dynamic row counters of the cluster tier
     MatView A, B;
     int64_t k;
     const void* c_row_map;

@@ -431,154 +431,6 @@ static void launch_num_strict(Launch& L, const NumArgs& a, int bin) {
 }
 
 
-// ------------------------------------------------------------------------------------
-// a7 for long rows (nnz(C_i) > 512) when B has at most ~1.4M columns: a CTA owns a row and
-// the row's whole column bit vector (k bits) plus the popcount prefix of every group of 4
-// words in shared memory.  (1) the bit vector of the row's pattern (accum = OR, as the
-// symbolic dense tier); (2) one pass over it writes the sorted column indices of C(i,:)
-// and the group prefixes; (3) each product finds its rank in the row (group prefix +
-// popcounts of <= 3 preceding words + the bits below it) and is added to C's value at that
-// position in global memory (fp64/fp32 reduction at L2, fire-and-forget).  This is the
-// paper's dense accumulator turned into "bit vector in shared memory,
-// scalar array = the output row itself", so no column windows are walked.
-// ------------------------------------------------------------------------------------
-constexpr int HUB_THREADS = 512;
-constexpr int HUB_WARPS = HUB_THREADS / 32;
-
-__host__ __device__ constexpr int64_t hub_words(int64_t k) { return ((k + 127) / 128) * 4; }  // multiple of 4
-constexpr int HUB_LONG = 256;     // B rows longer than this are walked by the whole CTA
-constexpr int HUB_LIST = 1024;    // capacity of the per-row list of such A entries
-
-// shared layout: bm[NW] | gp[NW/4] (padded to 8 bytes) | wtot[HUB_WARPS] (int64) |
-//                list[HUB_LIST] (int32) | nlist
-__host__ __device__ constexpr int64_t hub_gp_words(int64_t k) { return (hub_words(k) / 4 + 1) & ~1ll; }
-__host__ __device__ constexpr size_t hub_smem(int64_t k) {
-    return (size_t)(hub_words(k) + hub_gp_words(k)) * 4 + (size_t)HUB_WARPS * 8 + (size_t)HUB_LIST * 4 + 16;
-}
-
-template <typename OffT, typename ValT>
-__global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
-                                                             const ValT* __restrict__ aval, const OffT* __restrict__ brm,
-                                                             const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
-                                                             const OffT* __restrict__ crm, int32_t* __restrict__ cent,
-                                                             ValT* __restrict__ cval, const int32_t* __restrict__ perm,
-                                                             const int* __restrict__ bin_start, int bin, int64_t k) {
-    extern __shared__ __align__(16) uint32_t sm_hub[];
-    const int64_t NW = hub_words(k);
-    uint32_t* bm = sm_hub;
-    uint32_t* gp = bm + NW;
-    long long* wtot = (long long*)(gp + hub_gp_words(k));
-    int* list = (int*)(wtot + HUB_WARPS);
-    int* nlist = list + HUB_LIST;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
-    if (r0 + (int)blockIdx.x >= r1) return;
-    const int64_t per = (NW / 4 + HUB_WARPS - 1) / HUB_WARPS * 4;  // words per warp (multiple of 4)
-    for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
-        const int i = perm[r];
-        const int64_t s = ld(arm, i), e = ld(arm, i + 1);
-        const int64_t cb = ld(crm, i);
-        const int64_t clen = ld(crm, i + 1) - cb;
-        for (int64_t t = threadIdx.x; t < NW / 4; t += HUB_THREADS) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
-        if (threadIdx.x == 0) *nlist = 0;
-        __syncthreads();
-        // (1) pattern.  Warps take the A entries whose B rows are short; longer B rows are
-        // listed and then walked by the whole CTA, one at a time (a hub B row must not
-        // leave one warp working while the others wait at the barrier).
-        for (int64_t p = s + warp; p < e; p += HUB_WARPS) {
-            const int j = __ldg(aent + p);
-            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
-            if (be - bs > HUB_LONG) {
-                int slot = 0;
-                if (lane == 0) slot = atomicAdd(nlist, 1);
-                slot = __shfl_sync(FULL, slot, 0);
-                if (slot < HUB_LIST) {
-                    if (lane == 0) list[slot] = (int)(p - s);
-                    continue;
-                }
-            }
-            for (int64_t q = bs + lane; q < be; q += 32) {
-                const int c = __ldg(bent + q);
-                atomicOr(&bm[c >> 5], 1u << (c & 31));
-            }
-        }
-        __syncthreads();
-        const int nl = min(*nlist, HUB_LIST);
-        for (int l = 0; l < nl; ++l) {
-            const int j = __ldg(aent + s + list[l]);
-            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
-            for (int64_t q = bs + threadIdx.x; q < be; q += HUB_THREADS) {
-                const int c = __ldg(bent + q);
-                atomicOr(&bm[c >> 5], 1u << (c & 31));
-            }
-        }
-        __syncthreads();
-        // (2) per-warp word ranges: totals, then prefixes + sorted entries in one pass
-        const int64_t w0 = (int64_t)warp * per, w1 = min(NW, w0 + per);
-        long long tot = 0;
-        for (int64_t w = w0 + lane; w < w1; w += 32) tot += __popc(bm[w]);
-        tot = warp_sum(tot);
-        if (lane == 0) wtot[warp] = tot;
-        __syncthreads();
-        long long base = 0;
-        for (int w = 0; w < warp; ++w) base += wtot[w];
-        for (int64_t c0 = w0; c0 < w1; c0 += 32) {
-            const int64_t w = c0 + lane;
-            const uint32_t word = w < w1 ? bm[w] : 0u;
-            const int n = __popc(word);
-            int x = n;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int y = __shfl_up_sync(FULL, x, d);
-                if (lane >= d) x += y;
-            }
-            long long pos = base + x - n;
-            if (w < w1 && (w & 3) == 0) gp[w >> 2] = (uint32_t)pos;
-            uint32_t m = word;
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                if (pos < clen) cent[cb + pos] = (int32_t)(w * 32 + b);
-                ++pos;
-            }
-            base += __shfl_sync(FULL, x, 31);
-        }
-        for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) cval[cb + t] = (ValT)0;
-        __syncthreads();
-        // (3) values: rank lookup, reduction into C(i, rank) (same split of the work)
-        auto add = [&](int c, ValT prod) {
-            const int w = c >> 5;
-            uint32_t rk = gp[w >> 2];
-            const int g0 = w & ~3;
-            if (g0 + 0 < w) rk += __popc(bm[g0 + 0]);
-            if (g0 + 1 < w) rk += __popc(bm[g0 + 1]);
-            if (g0 + 2 < w) rk += __popc(bm[g0 + 2]);
-            rk += __popc(bm[w] & ((1u << (c & 31)) - 1u));
-            if ((int64_t)rk < clen) atomicAdd(&cval[cb + rk], prod);
-        };
-        for (int64_t p = s + warp; p < e; p += HUB_WARPS) {
-            const int j = __ldg(aent + p);
-            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
-            if (be - bs > HUB_LONG && nl > 0) {
-                // listed above (unless the list overflowed: then it is not in the list)
-                bool listed = false;
-                for (int l = lane; l < nl; l += 32) listed |= list[l] == (int)(p - s);
-                if (__any_sync(FULL, listed)) continue;
-            }
-            const ValT a = __ldg(aval + p);
-            for (int64_t q = bs + lane; q < be; q += 32) add(__ldg(bent + q), a * __ldg(bval + q));
-        }
-        for (int l = 0; l < nl; ++l) {
-            const int64_t p = s + list[l];
-            const int j = __ldg(aent + p);
-            const ValT a = __ldg(aval + p);
-            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
-            for (int64_t q = bs + threadIdx.x; q < be; q += HUB_THREADS) add(__ldg(bent + q), a * __ldg(bval + q));
-        }
-        __syncthreads();
-    }
-}
-
 template <typename OffT, typename ValT, int S, bool SORT>
 static void launch_num_warp(Launch& L, const NumArgs& a, int bin) {
     const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
@@ -657,19 +509,9 @@ static void launch_num_tiny(Launch& L, const NumArgs& a) {
 template <typename OffT, typename ValT, bool SORT>
 static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_stream) {
     const int drows = a.host_bin_start[NUM_DENSE_BIN + 1] - a.host_bin_start[NUM_DENSE_BIN];
-    const size_t hsm = hub_smem(a.k);
-    if (drows > 0 && a.k > 25600 && hsm <= 220 * 1024) {
-        // long rows, one column window would not do: bit vector over all of k (k_num_hub)
-        auto kern = k_num_hub<OffT, ValT>;
-        KCfg c = kernel_cfg(kern, HUB_THREADS, hsm, L.num_sms);
-        const int grid = (int)std::min<int64_t>(drows, c.grid_cap);
-        cudaStream_t s = dense_stream ? dense_stream : L.stream;
-        L.begin("num_hub", s);
-        kern<<<grid, HUB_THREADS, hsm, s>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
-                                            (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
-                                            (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
-                                            a.bin_start, NUM_DENSE_BIN, a.k);
-        L.end(s);
+    cudaStream_t ds = dense_stream ? dense_stream : L.stream;
+    if (drows > 0 && launch_hub_bins(L, a, ds)) {
+        // long rows over a wide k: CTA bit vector / cluster column slices (kk_num_hub.cu)
     } else if (drows > 0) {
         const int threads = 256;
         const size_t budget = 200 * 1024;

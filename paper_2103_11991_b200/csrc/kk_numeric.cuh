@@ -136,4 +136,8 @@ __device__ __forceinline__ void row_products(int64_t s, int64_t e, int jn, ValT 
 // NUM_PATH_BIN0..), kk_num_rank.cu
 void launch_pattern_bins(Launch& L, const NumArgs& a);
 
+// a7 for the dense bin (nnz(C_i) > 512) when k is wide enough for a column bit vector
+// (kk_num_hub.cu); false: not applicable, the caller runs the windowed dense tier
+bool launch_hub_bins(Launch& L, const NumArgs& a, cudaStream_t s);
+
 }  // namespace kk

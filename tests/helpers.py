@@ -27,6 +27,8 @@ def gpu_spgemm(A, B, value_dtype=torch.float64, offset_dtype=torch.int64, **opts
     ent, val = h.numeric(Ad, Bd, rm, nnz=nnz)
     torch.cuda.synchronize()
     st = h.stats()
+    if opts.get("timing"):
+        st["kernels"] = [k[0] for k in h.kernel_times()]
     h.close()
     return rm.cpu().numpy().astype(np.int64), ent.cpu().numpy(), val.cpu().to(torch.float64).numpy(), st
 

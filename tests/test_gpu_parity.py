@@ -418,3 +418,25 @@ def test_wide_pattern_hashed_word_table(oracle_mod, vt):
     assert_parity(oracle_mod, A, B, got, value_dtype=vt)
     st = got[3]
     assert sum(st["numeric_bin_rows"][12:16]) > 0, "expected rows in the hashed-pattern bins"
+
+
+def test_cluster_tier_windows(oracle_mod):
+    """Rows far above one CTA's value array on a wide k (k = 1M): the cluster tier (column
+    slices across the CTAs of a thread-block cluster, slice offsets through distributed
+    shared memory), slices with several rank windows, B-row segments long enough to be
+    walked by the whole CTA, and more of them than its list holds (CL_LIST = 512)."""
+    rng = np.random.default_rng(23)
+    k, nb, per = 1_000_000, 700, 20000
+    b_rows = [np.sort(rng.choice(k, per - (j % 13), replace=False)) for j in range(nb)]
+    brm = np.cumsum([0] + [len(r) for r in b_rows])
+    B = g.CSR(nb, k, torch.tensor(brm), torch.tensor(np.concatenate(b_rows), dtype=torch.int32),
+              torch.tensor(rng.uniform(-1, 1, brm[-1])))
+    a_rows = [np.arange(600), np.sort(rng.choice(nb, 50, replace=False)), np.sort(rng.choice(nb, 10, replace=False)),
+              np.array([3, 500, 699]), np.array([7])]
+    arm = np.cumsum([0] + [len(r) for r in a_rows])
+    A = g.CSR(len(a_rows), nb, torch.tensor(arm), torch.tensor(np.concatenate(a_rows), dtype=torch.int32),
+              torch.tensor(rng.uniform(-1, 1, arm[-1])))
+    for vt in (torch.float64, torch.float32):
+        got = gpu_spgemm(A, B, value_dtype=vt, offset_dtype=torch.int64, timing=True)
+        assert "num_cluster" in got[3]["kernels"] and "num_hub" in got[3]["kernels"], got[3]["kernels"]
+        assert_parity(oracle_mod, A, B, got, value_dtype=vt)
