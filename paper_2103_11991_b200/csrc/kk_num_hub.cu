@@ -12,6 +12,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace kk {
 namespace cg = cooperative_groups;
@@ -39,6 +40,89 @@ constexpr int HUB_LIST = 1024; // capacity of the per-row list of such A entries
 __host__ __device__ constexpr int64_t hub_gp_words(int64_t k) { return (hub_words(k) / 4 + 1) & ~1ll; }
 __host__ __device__ constexpr size_t hub_smem(int64_t k) {
     return (size_t)(hub_words(k) + hub_gp_words(k)) * 4 + (size_t)HUB_WARPS * 8 + (size_t)HUB_LIST * 4 + 16;
+}
+
+// The products of the A entries [s, e): each warp takes batches of 32 A entries (one
+// load chain for the batch: column, value, B-row bounds per lane; batches handed out by a
+// shared counter), then walks their B rows one after the other with 4 entries per lane in
+// flight (otherwise the hub kernels are bound by load latency: one dependent chain per A
+// entry per warp).  B rows longer than HUB_LONG are appended to the CTA's list and walked
+// by all threads afterwards (a hub B row must not leave one warp working while the others
+// wait at the barrier); when the list is full the warp walks the row itself.
+// f(col, a * b) per product (b = 1 when VALS is false: the pattern pass loads no values).
+template <int U, bool VALS, typename ValT, typename F>
+__device__ __forceinline__ void hub_segment(const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                            int64_t b0, int64_t len, int tid, int nthr, ValT a, F f) {
+    for (int64_t x0 = tid; x0 < len; x0 += (int64_t)nthr * U) {
+        int c[U];
+        ValT v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t x = x0 + (int64_t)u * nthr;
+            const bool ok = x < len;
+            c[u] = ok ? __ldg(bent + b0 + x) : -1;
+            v[u] = (VALS && ok) ? __ldg(bval + b0 + x) : (ValT)1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (c[u] >= 0) f(c[u], a * v[u]);
+    }
+}
+
+// nlist[0]: list length, nlist[1]: batch counter (both zero on entry)
+template <bool VALS, typename OffT, typename ValT, typename F>
+__device__ __forceinline__ void hub_walk(int64_t s, int64_t e, const int32_t* __restrict__ aent,
+                                         const ValT* __restrict__ aval, const OffT* __restrict__ brm,
+                                         const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
+                                         int* list, int* nlist, F f) {
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        int b = 0;
+        if (lane == 0) b = atomicAdd(nlist + 1, 1);
+        const int64_t p0 = s + (int64_t)__shfl_sync(FULL, b, 0) * 32;
+        if (p0 >= e) break;
+        const int64_t p = p0 + lane;
+        int64_t bs = 0, bl = 0;
+        ValT a = (ValT)0;
+        if (p < e) {
+            const int j = __ldg(aent + p);
+            if (VALS) a = __ldg(aval + p);
+            bs = ld(brm, j);
+            bl = ld(brm, j + 1) - bs;
+        }
+        // long B rows to the CTA list (one atomic per warp for the batch)
+        const bool lng = bl > HUB_LONG;
+        const unsigned lb = __ballot_sync(FULL, lng);
+        bool listed = false;
+        if (lb) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(nlist, __popc(lb));
+            base = __shfl_sync(FULL, base, 0);
+            const int slot = base + __popc(lb & lanemask_lt());
+            if (lng && slot < HUB_LIST) {
+                list[slot] = (int)(p - s);
+                listed = true;
+            }
+        }
+        const unsigned skip = __ballot_sync(FULL, listed);
+        const int n = (int)min((int64_t)32, e - p0);
+        for (int t = 0; t < n; ++t) {
+            if ((skip >> t) & 1u) continue;
+            const int64_t tb = __shfl_sync(FULL, bs, t);
+            const int64_t tl = __shfl_sync(FULL, bl, t);
+            const ValT ta = __shfl_sync(FULL, a, t);
+            hub_segment<4, VALS>(bent, bval, tb, tl, lane, 32, ta, f);
+        }
+    }
+    __syncthreads();
+    const int nl = min(*nlist, HUB_LIST);
+    for (int l = 0; l < nl; ++l) {
+        const int64_t p = s + list[l];
+        const int j = __ldg(aent + p);
+        const ValT a = VALS ? __ldg(aval + p) : (ValT)0;
+        const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+        hub_segment<4, VALS>(bent, bval, bs, be - bs, (int)threadIdx.x, HUB_THREADS, a, f);
+    }
 }
 
 template <typename OffT, typename ValT>
@@ -69,66 +153,50 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
         const bool inshared = clen <= (int64_t)vcap;
         if (!inshared && big) continue;  // the cluster tier's row
         for (int64_t t = threadIdx.x; t < NW / 4; t += HUB_THREADS) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
-        if (threadIdx.x == 0) *nlist = 0;
+        if (threadIdx.x == 0) nlist[0] = nlist[1] = 0;
         __syncthreads();
-        // (1) pattern.  Warps take the A entries whose B rows are short; longer B rows are
-        // listed and then walked by the whole CTA, one at a time (a hub B row must not
-        // leave one warp working while the others wait at the barrier).
-        for (int64_t p = s + warp; p < e; p += HUB_WARPS) {
-            const int j = __ldg(aent + p);
-            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
-            if (be - bs > HUB_LONG) {
-                int slot = 0;
-                if (lane == 0) slot = atomicAdd(nlist, 1);
-                slot = __shfl_sync(FULL, slot, 0);
-                if (slot < HUB_LIST) {
-                    if (lane == 0) list[slot] = (int)(p - s);
-                    continue;
-                }
-            }
-            for (int64_t q = bs + lane; q < be; q += 32) {
-                const int c = __ldg(bent + q);
-                atomicOr(&bm[c >> 5], 1u << (c & 31));
-            }
-        }
+        // (1) pattern (accum = OR)
+        hub_walk<false>(s, e, aent, aval, brm, bent, bval, list, nlist,
+                        [&](int c, ValT) { atomicOr(&bm[c >> 5], 1u << (c & 31)); });
         __syncthreads();
-        const int nl = min(*nlist, HUB_LIST);
-        for (int l = 0; l < nl; ++l) {
-            const int j = __ldg(aent + s + list[l]);
-            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
-            for (int64_t q = bs + threadIdx.x; q < be; q += HUB_THREADS) {
-                const int c = __ldg(bent + q);
-                atomicOr(&bm[c >> 5], 1u << (c & 31));
-            }
-        }
-        __syncthreads();
-        // (2) per-warp word ranges: totals, then prefixes + sorted entries in one pass
-        const int64_t w0 = (int64_t)warp * per, w1 = min(NW, w0 + per);
+        // (2) per-warp ranges of 4-word groups: totals, then group prefixes + sorted entries in
+        // one pass, a group per lane; chunks of 32 empty groups are skipped (their prefixes
+        // are never read: no product falls in an empty group)
+        const uint4* bm4 = (const uint4*)bm;
+        const int64_t g0 = (int64_t)warp * (per / 4), g1 = min(NW / 4, g0 + per / 4);
         long long tot = 0;
-        for (int64_t w = w0 + lane; w < w1; w += 32) tot += __popc(bm[w]);
+        for (int64_t g = g0 + lane; g < g1; g += 32) {
+            const uint4 v = bm4[g];
+            tot += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+        }
         tot = warp_sum(tot);
         if (lane == 0) wtot[warp] = tot;
         __syncthreads();
         long long base = 0;
         for (int w = 0; w < warp; ++w) base += wtot[w];
-        for (int64_t c0 = w0; c0 < w1; c0 += 32) {
-            const int64_t w = c0 + lane;
-            const uint32_t word = w < w1 ? bm[w] : 0u;
-            const int n = __popc(word);
+        for (int64_t c0 = g0; c0 < g1; c0 += 32) {
+            const int64_t g = c0 + lane;
+            const uint4 v = g < g1 ? bm4[g] : make_uint4(0u, 0u, 0u, 0u);
+            const int n = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+            if (__ballot_sync(FULL, n != 0) == 0u) continue;
             int x = n;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const int y = __shfl_up_sync(FULL, x, d);
                 if (lane >= d) x += y;
             }
-            long long pos = base + x - n;
-            if (w < w1 && (w & 3) == 0) gp[w >> 2] = (uint32_t)pos;
-            uint32_t m = word;
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                if (pos < clen) cent[cb + pos] = (int32_t)(w * 32 + b);
-                ++pos;
+            long long pp = base + x - n;
+            if (g < g1) gp[g] = (uint32_t)pp;
+            const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint32_t m = wv[u];
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (pp < clen) __stcs(cent + cb + pp, (int32_t)((g * 4 + u) * 32 + b));
+                    ++pp;
+                }
             }
             base += __shfl_sync(FULL, x, 31);
         }
@@ -136,15 +204,16 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
             for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) svals[t] = (ValT)0;
         else
             for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) cval[cb + t] = (ValT)0;
+        if (threadIdx.x == 0) nlist[0] = nlist[1] = 0;
         __syncthreads();
-        // (3) values: rank lookup, accumulation at the rank (same split of the work)
-        auto add = [&](int c, ValT prod) {
+        // (3) values: rank lookup, accumulation at the rank
+        hub_walk<true>(s, e, aent, aval, brm, bent, bval, list, nlist, [&](int c, ValT prod) {
             const int w = c >> 5;
             uint32_t rk = gp[w >> 2];
-            const int g0 = w & ~3;
-            if (g0 + 0 < w) rk += __popc(bm[g0 + 0]);
-            if (g0 + 1 < w) rk += __popc(bm[g0 + 1]);
-            if (g0 + 2 < w) rk += __popc(bm[g0 + 2]);
+            const int gw = w & ~3;
+            if (gw + 0 < w) rk += __popc(bm[gw + 0]);
+            if (gw + 1 < w) rk += __popc(bm[gw + 1]);
+            if (gw + 2 < w) rk += __popc(bm[gw + 2]);
             rk += __popc(bm[w] & ((1u << (c & 31)) - 1u));
             if ((int64_t)rk < clen) {
                 if (inshared)
@@ -152,26 +221,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
                 else
                     atomicAdd(&cval[cb + rk], prod);
             }
-        };
-        for (int64_t p = s + warp; p < e; p += HUB_WARPS) {
-            const int j = __ldg(aent + p);
-            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
-            if (be - bs > HUB_LONG && nl > 0) {
-                // listed above (unless the list overflowed: then it is not in the list)
-                bool listed = false;
-                for (int l = lane; l < nl; l += 32) listed |= list[l] == (int)(p - s);
-                if (__any_sync(FULL, listed)) continue;
-            }
-            const ValT a = __ldg(aval + p);
-            for (int64_t q = bs + lane; q < be; q += 32) add(__ldg(bent + q), a * __ldg(bval + q));
-        }
-        for (int l = 0; l < nl; ++l) {
-            const int64_t p = s + list[l];
-            const int j = __ldg(aent + p);
-            const ValT a = __ldg(aval + p);
-            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
-            for (int64_t q = bs + threadIdx.x; q < be; q += HUB_THREADS) add(__ldg(bent + q), a * __ldg(bval + q));
-        }
+        });
         __syncthreads();
         if (inshared) {
             for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) __stcs(cval + cb + t, svals[t]);
@@ -443,6 +493,16 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
     cluster.sync();
 }
 
+// the cluster tier for rows above one CTA's value array: KK_HUB_CLUSTER=1 (measured slower
+// than L2 reductions on C4; kept for the A/B and its parity test)
+static bool use_cluster() {
+    static const bool v = [] {
+        const char* e = getenv("KK_HUB_CLUSTER");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 template <typename OffT, typename ValT>
 static bool hub_bins_t(Launch& L, const NumArgs& a, cudaStream_t s) {
     const size_t hsm = hub_smem(a.k);
@@ -456,7 +516,7 @@ static bool hub_bins_t(Launch& L, const NumArgs& a, cudaStream_t s) {
     // (b) the cluster tier for the longer rows: sorted B, slice bit vector + value window fit
     const size_t cfix = cl_fixed_smem(a.k);
     const int cvcap = cfix + 4096 * sizeof(ValT) <= SMEM_MAX ? (int)((SMEM_MAX - cfix) / sizeof(ValT)) - 64 : 0;
-    const bool cluster = a.sorted && a.work_ctr != nullptr && cvcap >= 4096;
+    const bool cluster = use_cluster() && a.sorted && a.work_ctr != nullptr && cvcap >= 4096;
     {
         auto kern = k_num_hub<OffT, ValT>;
         KCfg c = kernel_cfg(kern, HUB_THREADS, hsm_v, L.num_sms);
@@ -492,7 +552,7 @@ static bool hub_bins_t(Launch& L, const NumArgs& a, cudaStream_t s) {
         nclusters = std::min(nclusters, drows);
         cfg.gridDim = dim3((unsigned)(nclusters * CL_SIZE), 1, 1);
         cudaMemsetAsync(a.work_ctr, 0, sizeof(int), s);
-        L.begin("num_cluster", s);
+        L.begin(kname("num_cluster", nclusters), s);
         cudaLaunchKernelEx(&cfg, kern, (const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                            (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values, (const OffT*)a.c_row_map,
                            a.c_entries, (ValT*)a.c_values, a.perm, a.bin_start, (int)NUM_DENSE_BIN, a.k,
