@@ -304,15 +304,24 @@ def run_ours(args):
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N>1 must be launched with torchrun (one rank per GPU)")
+    # BENCH_SHARE_DEVICE=1 / BENCH_BACKEND=gloo: every rank on cuda:0 over gloo -- only for
+    # the single-GPU test of the N>1 path (tests/test_gpu_multi.py); never a measurement
+    if os.environ.get("BENCH_SHARE_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     vdt = torch.float64 if args.dtype == "f64" else torch.float32
     odt = offset_dtype_for(args.config)
+    vwork = None
 
     # ---- workload (generated on the device: inputs resident in HBM) ----
     t_bcast = None
@@ -329,18 +338,41 @@ def run_ours(args):
         A, B = mats[0], mats[1]
         r0, r1 = 0, A.nrows
     else:
-        if args.config in ("C3", "C3J"):
-            raise SystemExit(f"{args.config} is benchmarked on one GPU")
-        from paper_2103_11991_b200.parallel import broadcast_csr, flop_balanced_cuts, halo_exchange_b, slice_rows
+        if args.config == "C3J":
+            raise SystemExit("C3J is benchmarked on one GPU")
+        from paper_2103_11991_b200.parallel import (broadcast_csr, flop_balanced_cuts, galerkin_slab_cuts,
+                                                    halo_exchange_b, shift_columns, slice_rows)
 
-        if args.halo:
+        align = 3 if args.config == "C5" else 1  # whole 3-dof nodes
+        vwork = None
+        if args.config == "C3":
+            # z-slab partition: P broadcast from rank 0; A and R row blocks of
+            # whole aggregate planes, so R_p * T_p needs no second exchange
+            A_f, P_f, R_f = make_workload(args.config, args.size, args.values, dev)
+            n = round(A_f.nrows ** (1.0 / 3.0))
+            fc, cc = galerkin_slab_cuts(n, 3, world)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            P = broadcast_csr(conv(P_f) if rank == 0 else None, src=0, device=dev)
+            e1.record()
+            torch.cuda.synchronize()
+            t_bcast = e0.elapsed_time(e1)
+            r0, r1 = fc[rank], fc[rank + 1]
+            A = conv(slice_rows(A_f, r0, r1))
+            R_p = conv(shift_columns(slice_rows(R_f, cc[rank], cc[rank + 1]), r0, r1 - r0))
+            mats = [A, P, R_p]
+            B = P
+            del A_f, R_f
+        elif args.halo:
             # every rank holds its row block of B (here: generated whole, then sliced -- the
             # input of a row-distributed solver) and fetches the rows its A block needs
             full = conv(make_workload(args.config, args.size, args.values, dev)[1])
             hf = SpGEMM(device=dev)
             _, F, _ = hf.row_flops(full, full, scan=True, total=False)
             hf.close()
-            cuts = flop_balanced_cuts(F.cpu().numpy(), world)
+            cuts = flop_balanced_cuts(F.cpu().numpy(), world, align)
             r0, r1 = cuts[rank], cuts[rank + 1]
             A = slice_rows(full, r0, r1)
             B_loc = slice_rows(full, r0, r1)
@@ -364,16 +396,16 @@ def run_ours(args):
             dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            B = broadcast_csr(B0, src=0, device=dev)
+            # the values' broadcast stays in flight while the row split and the first symbolic
+            # phase (pattern only) run; the first numeric phase waits for it
+            B, vwork = broadcast_csr(B0, src=0, device=dev, async_values=True)
             e1.record()
-            torch.cuda.synchronize()
-            t_bcast = e0.elapsed_time(e1)
             # A*A: A is B (a separate copy on every rank would only double memory; row block
             # of the broadcast matrix, SURVEY §8e "A needs no extra traffic")
             hf = SpGEMM(device=dev)
             _, F, _ = hf.row_flops(B, B, scan=True, total=False)
             hf.close()
-            cuts = flop_balanced_cuts(F.cpu().numpy(), world)
+            cuts = flop_balanced_cuts(F.cpu().numpy(), world, align)
             r0, r1 = cuts[rank], cuts[rank + 1]
             A = slice_rows(B, r0, r1)
             mats = [A, B]
@@ -397,9 +429,14 @@ def run_ours(args):
 
     # the step's products: A*B, or for C3 T = A*P then Ac = R*T (T stays in HBM)
     prods = [Product(A, B, jac)]
+    if world > 1 and vwork is not None:
+        vwork.wait()  # B's values (in flight during the row split and the first symbolic phase)
+        torch.cuda.synchronize()
+        t_bcast = e0.elapsed_time(e1)  # the blocking part: header, row map, entries
     if args.config == "C3":
         prods.append(Product(mats[2], prods[0].C()))
-    nnz_all = torch.zeros(world, dtype=torch.int64, device=dev)
+    if world > 1:
+        from paper_2103_11991_b200.parallel import allgather_row_map_total
 
     def step(ev=None):
         for k, pr in enumerate(prods):
@@ -407,8 +444,8 @@ def run_ours(args):
                 ev[2 * k].record(stream)
             _, n = pr.h.symbolic(pr.X, pr.Y, c_row_map=pr.crm)
             if world > 1:
-                mine = torch.tensor([n], dtype=torch.int64, device=dev)
-                dist.all_gather_into_tensor(nnz_all, mine)
+                # nnz(C_p) straight from the row map the scan kernel wrote (no host tensor)
+                allgather_row_map_total(pr.crm)
             if ev is not None:
                 ev[2 * k + 1].record(stream)
             if pr.jacobi is not None:
@@ -590,8 +627,11 @@ def run_ours(args):
                "config": {"workload": f"{args.config}: {WORKLOADS[args.config]}", "values": args.values,
                           "offsets": "int32" if odt == torch.int32 else "int64",
                           "l2": "inputs (A, B) and output C each exceed the 126 MB L2; no flush",
-                          "parallelism": f"row-sharded x{world}" + (", B broadcast (NCCL), nnz all-gather"
-                                                                    if world > 1 else ""),
+                          "parallelism": f"row-sharded x{world}" + (
+                              (", z-slabs, P broadcast (NCCL), nnz all-gather" if args.config == "C3" else
+                               ", B halo exchange (NCCL), nnz all-gather" if args.halo else
+                               ", B broadcast (NCCL, values overlapped with symbolic), nnz all-gather")
+                              if world > 1 else ""),
                           "nnz_A": int(A.nnz) if world == 1 else int(nnzA_all), "nnz_C": int(nnz_all_c),
                           "multiply_adds": int(muladds_all)},
                "hbm_gbs": round(hbm_gbs, 1), "hbm_frac": round(hbm_gbs / peak, 4),

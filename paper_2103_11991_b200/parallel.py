@@ -22,10 +22,11 @@ from .spgemm import CsrMatrix, SpGEMM
 _DT = [torch.int32, torch.int64, torch.float32, torch.float64]
 
 
-def flop_balanced_cuts(F: Sequence[int], world: int) -> List[int]:
+def flop_balanced_cuts(F: Sequence[int], world: int, align: int = 1) -> List[int]:
     """Split points r_0=0 <= r_1 <= ... <= r_P=m of rows, from the exclusive prefix F
     (length m+1) of per-row multiply-adds: r_p is the first row whose prefix reaches
-    p*F[m]/P."""
+    p*F[m]/P, rounded to a multiple of `align` (whole 3-dof nodes of the
+    block stencil C5: align=3)."""
     import numpy as np
 
     F = np.asarray(F, dtype=np.int64)
@@ -33,7 +34,10 @@ def flop_balanced_cuts(F: Sequence[int], world: int) -> List[int]:
     total = int(F[m]) if m >= 0 else 0
     cuts = [0]
     for p in range(1, world):
-        cuts.append(int(np.searchsorted(F, (total * p) // world, side="left")))
+        c = int(np.searchsorted(F, (total * p) // world, side="left"))
+        if align > 1:
+            c = int(round(c / align)) * align
+        cuts.append(c)
     cuts.append(max(m, 0))
     out = [min(max(c, 0), max(m, 0)) for c in cuts]
     for i in range(1, len(out)):
@@ -50,6 +54,20 @@ def global_offsets(nnz_per_rank: Sequence[int]) -> List[int]:
     return out
 
 
+def galerkin_slab_cuts(n: int, agg: int, world: int) -> Tuple[List[int], List[int]]:
+    """z-slab partition of the C3 Galerkin product on an n^3 grid with agg^3 aggregates
+    (SURVEY §8e "C3 at P > 1"): slab p holds whole aggregate planes, i.e. fine z-planes
+    [agg*z_p, agg*z_{p+1}) and coarse z-planes [z_p, z_{p+1}).  With lexicographic
+    numbering (z slowest) both are contiguous row ranges: fine rows [n*n*agg*z_p, ...) of A
+    and T, coarse rows [nc*nc*z_p, ...) of R and Ac.  R's row block p references only fine
+    rows of slab p, so R_p * T_p needs no second exchange.  Returns (fine_cuts, coarse_cuts)."""
+    nc = (n + agg - 1) // agg
+    zc = [(nc * p) // world for p in range(world + 1)]
+    fine = [min(n, agg * z) * n * n for z in zc]
+    coarse = [z * nc * nc for z in zc]
+    return fine, coarse
+
+
 def slice_rows(M: CsrMatrix, r0: int, r1: int) -> CsrMatrix:
     """Rows [r0, r1) of M as a CSR matrix of its own (row map rebased to 0; entries and
     values are views, no copy)."""
@@ -61,9 +79,29 @@ def slice_rows(M: CsrMatrix, r0: int, r1: int) -> CsrMatrix:
     return CsrMatrix(r1 - r0, M.ncols, sub_rm, M.entries[s:e], vals)
 
 
-def broadcast_csr(M: Optional[CsrMatrix], src: int = 0, device=None, group=None) -> CsrMatrix:
+def shift_columns(M: CsrMatrix, c0: int, ncols: int) -> CsrMatrix:
+    """The same rows with column indices shifted by -c0 into [0, ncols) (a row block whose
+    columns all lie in [c0, c0 + ncols), e.g. R_p of the slab-partitioned Galerkin product)."""
+    return CsrMatrix(M.nrows, ncols, M.row_map, (M.entries - c0).to(torch.int32), M.values)
+
+
+def _bcast(t: torch.Tensor, src: int, group, async_op: bool = False):
+    """Broadcast in place.  NCCL takes device tensors; gloo (CPU tests, or several ranks
+    sharing one GPU in the single-GPU tests) is staged through host memory."""
+    if dist.get_backend(group) == "nccl" or t.device.type == "cpu":
+        return dist.broadcast(t, src, group=group, async_op=async_op)
+    h = t.cpu()
+    dist.broadcast(h, src, group=group)
+    t.copy_(h)
+    return None
+
+
+def broadcast_csr(M: Optional[CsrMatrix], src: int = 0, device=None, group=None, async_values: bool = False):
     """Replicate a CSR matrix from rank `src` to every rank: a small header broadcast,
-    then row map + entries (the pattern, so symbolic could start), then values."""
+    then row map + entries (the pattern: symbolic can start once they have arrived), then
+    the values.  async_values=True returns (M, work) with the values' broadcast still in
+    flight (NCCL, its own stream): the caller overlaps it with the symbolic phase, which
+    reads only the pattern, and waits on `work` before the numeric phase."""
     rank = dist.get_rank(group)
     dev = torch.device(device) if device is not None else (
         M.row_map.device if M is not None else torch.device("cpu"))
@@ -72,7 +110,7 @@ def broadcast_csr(M: Optional[CsrMatrix], src: int = 0, device=None, group=None)
         hdr[0], hdr[1], hdr[2] = M.nrows, M.ncols, M.nnz
         hdr[3] = _DT.index(M.row_map.dtype)
         hdr[4] = _DT.index(M.values.dtype) if M.values is not None else -1
-    dist.broadcast(hdr, src, group=group)
+    _bcast(hdr, src, group)
     nrows, ncols, nnz, od, vd = (int(x) for x in hdr[:5].tolist())
     if rank == src:
         rm, ent = M.row_map.to(dev).contiguous(), M.entries.to(dev).contiguous()
@@ -81,16 +119,33 @@ def broadcast_csr(M: Optional[CsrMatrix], src: int = 0, device=None, group=None)
         rm = torch.empty(nrows + 1, dtype=_DT[od], device=dev)
         ent = torch.empty(nnz, dtype=torch.int32, device=dev)
         val = torch.empty(nnz, dtype=_DT[vd], device=dev) if vd >= 0 else None
-    dist.broadcast(rm, src, group=group)
+    _bcast(rm, src, group)
+    work = None
     if nnz:
-        dist.broadcast(ent, src, group=group)
+        _bcast(ent, src, group)
         if val is not None:
-            dist.broadcast(val, src, group=group)
-    return CsrMatrix(nrows, ncols, rm, ent, val)
+            work = _bcast(val, src, group, async_op=async_values)
+    out = CsrMatrix(nrows, ncols, rm, ent, val)
+    return (out, work) if async_values else out
+
+
+def allgather_row_map_total(c_row_map: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather nnz(C_p) = c_row_map[m_p] straight from the device row map the symbolic
+    scan kernel wrote (the all-gather's send buffer is that last entry: no host round trip
+    and no host-built tensor).  Returns the per-rank counts as an int64 device tensor."""
+    world = dist.get_world_size(group)
+    mine = c_row_map[-1:].to(torch.int64)
+    if dist.get_backend(group) == "nccl":
+        allv = torch.empty(world, dtype=torch.int64, device=c_row_map.device)
+        dist.all_gather_into_tensor(allv, mine, group=group)
+        return allv
+    parts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(parts, mine.cpu(), group=group)
+    return torch.cat(parts).to(c_row_map.device)
 
 
 def allgather_nnz(nnz_local: int, device, group=None) -> List[int]:
-    """All-gather one int64 nnz(C_p) per rank."""
+    """All-gather one int64 nnz(C_p) per rank (host values)."""
     world = dist.get_world_size(group)
     mine = torch.tensor([int(nnz_local)], dtype=torch.int64, device=device)
     if dist.get_backend(group) == "nccl":
@@ -208,10 +263,15 @@ class ShardedSpGEMM:
         self.group = group
         self.h = SpGEMM(device=device, **opts)
 
-    def __call__(self, A_local: CsrMatrix, B: CsrMatrix) -> Tuple[CsrMatrix, int, int]:
+    def __call__(self, A_local: CsrMatrix, B: CsrMatrix, values_work=None) -> Tuple[CsrMatrix, int, int]:
+        """values_work: the in-flight broadcast of B's values (broadcast_csr(...,
+        async_values=True)); the symbolic phase reads only B's pattern, so the wait is placed
+        just before the numeric phase."""
         rm, nnz = self.h.symbolic(A_local, B)
-        counts = allgather_nnz(nnz, rm.device, self.group)
+        counts = allgather_row_map_total(rm, self.group).tolist()
         offs = global_offsets(counts)
+        if values_work is not None:
+            values_work.wait()
         ent, val = self.h.numeric(A_local, B, rm, nnz=nnz)
         rank = dist.get_rank(self.group)
         return CsrMatrix(A_local.nrows, B.ncols, rm, ent, val), offs[rank], sum(counts)

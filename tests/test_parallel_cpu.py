@@ -169,3 +169,35 @@ def test_gloo_halo_exchange(oracle_mod, world):
         assert np.array_equal(np.asarray(ent, dtype=np.int32), ent_full[s:e])
         assert np.array_equal(np.asarray(val), val_full[s:e])
         assert fetched == want_fetched and nneed < n
+
+
+def test_flop_balanced_cuts_align():
+    from paper_2103_11991_b200.parallel import flop_balanced_cuts
+
+    A, B = g.config("C5", size=5)
+    rm = A.row_map.numpy()
+    f = np.array([int(B.row_map[int(j) + 1] - B.row_map[int(j)]) for j in A.entries.numpy()])
+    per_row = np.add.reduceat(f, rm[:-1]) if len(f) else np.zeros(A.nrows, dtype=np.int64)
+    F = np.concatenate([[0], np.cumsum(per_row)])
+    for world in (2, 3, 4, 8):
+        c = flop_balanced_cuts(F, world, align=3)
+        assert c[0] == 0 and c[-1] == A.nrows and c == sorted(c)
+        assert all(x % 3 == 0 for x in c), c
+
+
+@pytest.mark.parametrize("n,world", [(12, 2), (13, 3), (128, 8), (30, 4)])
+def test_galerkin_slab_cuts(n, world):
+    """Slab p's coarse rows (R's row block) reference only fine rows of slab p, so R_p * T_p
+    needs no exchange."""
+    from paper_2103_11991_b200.parallel import galerkin_slab_cuts
+
+    fc, cc = galerkin_slab_cuts(n, 3, world)
+    nc = (n + 2) // 3
+    assert fc[0] == 0 and fc[-1] == n ** 3 and cc[0] == 0 and cc[-1] == nc ** 3
+    if n <= 30:
+        _, _, R = g.config("C3", size=n)
+        rrm, rent = R.row_map.numpy(), R.entries.numpy()
+        for p in range(world):
+            s, e = int(rrm[cc[p]]), int(rrm[cc[p + 1]])
+            cols = rent[s:e]
+            assert cols.size == 0 or (cols.min() >= fc[p] and cols.max() < fc[p + 1])
