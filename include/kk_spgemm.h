@@ -190,6 +190,24 @@ kk_status_t kk_spadd_numeric(kk_spgemm_handle_t handle, double alpha, const kk_c
                              const kk_csr_t* B, const void* c_row_map, int32_t* c_entries, void* c_values,
                              void* stream);
 
+/* C = A*B with A, B and C in HOST memory: the paper's protocol run end to
+ * end over host buffers.  A, B: CSR whose row_map / entries / values are HOST pointers
+ * (pinned memory, e.g. cudaHostAlloc, lets the copies run asynchronously; pageable memory
+ * works but serialises them).  B is copied to the device once; A is processed in `blocks`
+ * contiguous row blocks (<= 0: 8 when A has >= 65,536 rows, else 1), each block's host->device
+ * copy, symbolic + numeric phases and device->host copy of its rows of C overlapped with the
+ * neighbouring blocks' on three streams (row blocks are independent products, Eq. 1 at
+ * PAPER.md:160-163).  Outputs:
+ *   c_row_map: HOST, A.nrows+1 of A.offset_type, caller-allocated, filled with C's row map;
+ *   *c_nnz: nnz(C);
+ *   *c_entries, *c_values: HOST (pinned) arrays of nnz(C) column indices / values owned by the
+ *     handle, valid until the next kk_spgemm_multiply_host or kk_spgemm_destroy.
+ * Errors as kk_spgemm_symbolic / numeric; KK_ERR_INDEX_OVERFLOW when nnz(C) does not fit
+ * int32 offsets.  Synchronises `stream` (returns when C is on the host). */
+kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t handle, const kk_csr_t* A, const kk_csr_t* B,
+                                    void* c_row_map, int64_t* c_nnz, int32_t** c_entries, void** c_values,
+                                    int blocks, void* stream);
+
 /* Per-kernel device times (opts.timing = 1).  One record per kernel (or fixed group of
  * launches, e.g. the three launches of a scan), accumulated since the last
  * kk_spgemm_timing_reset: number of launches, total and maximum duration in ms, from

@@ -84,11 +84,13 @@ def load() -> ctypes.CDLL:
         lib.kk_spadd_numeric.argtypes = [H, ctypes.c_double, P(kk_csr_t), ctypes.c_double, P(kk_csr_t), _vp, _vp,
                                          _vp, _vp]
         lib.kk_spgemm_stats.argtypes = [H, P(kk_spgemm_stats_t)]
+        lib.kk_spgemm_multiply_host.argtypes = [H, P(kk_csr_t), P(kk_csr_t), _vp, P(_i64),
+                                                P(ctypes.POINTER(ctypes.c_int32)), P(_vp), ctypes.c_int, _vp]
         lib.kk_spgemm_kernel_times.argtypes = [H, P(kk_kernel_time_t), P(ctypes.c_int)]
         lib.kk_spgemm_timing_reset.argtypes = [H]
         for fn in ("kk_spgemm_create", "kk_spgemm_destroy", "kk_spgemm_row_flops", "kk_spgemm_compress",
                    "kk_spgemm_symbolic", "kk_spgemm_numeric", "kk_spgemm_jacobi_numeric", "kk_spgemm_stats",
-                   "kk_spadd_symbolic", "kk_spadd_numeric",
+                   "kk_spadd_symbolic", "kk_spadd_numeric", "kk_spgemm_multiply_host",
                    "kk_spgemm_kernel_times",
                    "kk_spgemm_timing_reset"):
             getattr(lib, fn).restype = ctypes.c_int
@@ -189,6 +191,17 @@ def kk_spgemm_stats(h) -> dict:
     d["symbolic_bin_rows"] = list(s.symbolic_bin_rows)
     d["numeric_bin_rows"] = list(s.numeric_bin_rows)
     return d
+
+
+def kk_spgemm_multiply_host(h, A: kk_csr_t, B: kk_csr_t, c_row_map_ptr: int, blocks: int, stream: int):
+    """-> (nnz, entries address, values address): host arrays owned by the handle."""
+    nnz = _i64(0)
+    ent = ctypes.POINTER(ctypes.c_int32)()
+    val = _vp()
+    _check(h, load().kk_spgemm_multiply_host(h, ctypes.byref(A), ctypes.byref(B), c_row_map_ptr or None,
+                                             ctypes.byref(nnz), ctypes.byref(ent), ctypes.byref(val), int(blocks),
+                                             stream or None))
+    return int(nnz.value), ctypes.cast(ent, _vp).value or 0, val.value or 0
 
 
 def kk_spgemm_kernel_times(h) -> list:

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/kk_spgemm.h"
@@ -130,6 +131,18 @@ struct kk_spgemm_handle_s {
     int host_num_bin_start[kk::NB + 1] = {0};
     kk_spgemm_stats_t stats;
     kk::KTimer* timer = nullptr;
+    // kk_spgemm_multiply_host: streams, events, device staging (B; two slots of A blocks and
+    // C blocks), pinned host staging (rebased row maps; C's entries and values, grow-only)
+    struct HostPath {
+        cudaStream_t s_in = nullptr, s_out = nullptr;
+        Buf brm, bent, bval, arm[2], aent[2], aval[2], crm[2], cent[2], cval[2];
+        void* h_reb = nullptr;
+        size_t h_reb_bytes = 0;
+        void* h_cent = nullptr;
+        size_t h_cent_bytes = 0;
+        void* h_cval = nullptr;
+        size_t h_cval_bytes = 0;
+    } hp;
 };
 
 static kk_status_t fail(kk_spgemm_handle_t h, kk_status_t s, const char* fmt, ...) {
@@ -306,6 +319,17 @@ kk_status_t kk_spgemm_destroy(kk_spgemm_handle_t h) {
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     for (Buf* b : h->all_bufs) release(h, *b);
+    {
+        auto& P = h->hp;
+        Buf* hb[] = {&P.brm, &P.bent, &P.bval, &P.arm[0], &P.arm[1], &P.aent[0], &P.aent[1], &P.aval[0],
+                     &P.aval[1], &P.crm[0], &P.crm[1], &P.cent[0], &P.cent[1], &P.cval[0], &P.cval[1]};
+        for (Buf* b : hb) release(h, *b);
+        if (P.h_reb) cudaFreeHost(P.h_reb);
+        if (P.h_cent) cudaFreeHost(P.h_cent);
+        if (P.h_cval) cudaFreeHost(P.h_cval);
+        if (P.s_in) cudaStreamDestroy(P.s_in);
+        if (P.s_out) cudaStreamDestroy(P.s_out);
+    }
     delete h->timer;
     if (h->h_status) cudaFreeHost(h->h_status);
     if (h->side) cudaStreamDestroy(h->side);
@@ -649,7 +673,193 @@ kk_status_t kk_spgemm_stats(kk_spgemm_handle_t h, kk_spgemm_stats_t* out) {
     out->kernel_launches = h->launches;
     int64_t ws = 0;
     for (const Buf* b : h->all_bufs) ws += (int64_t)b->bytes;
+    {
+        const auto& P = h->hp;
+        const Buf* hb[] = {&P.brm, &P.bent, &P.bval, &P.arm[0], &P.arm[1], &P.aent[0], &P.aent[1], &P.aval[0],
+                           &P.aval[1], &P.crm[0], &P.crm[1], &P.cent[0], &P.cent[1], &P.cval[0], &P.cval[1]};
+        for (const Buf* b : hb) ws += (int64_t)b->bytes;
+    }
     out->workspace_bytes = ws;
+    return KK_OK;
+}
+
+// ---- C = A*B from host memory (PAPER.md:169-174 on host buffers) -------------------------
+// B is copied to the device once; A runs in `blocks` contiguous row blocks, each an
+// independent product (Eq. 1): block q's host->device copy (stream s_in),
+// its symbolic + numeric phases (the caller's stream) and the device->host copy of its rows
+// of C (stream s_out) overlap the neighbouring blocks' (two staging slots, events between
+// the streams).  The global row map is the blocks' row maps shifted by the nnz of the
+// blocks before them, assembled on the host.
+static kk_status_t ensure_host(kk_spgemm_handle_t h, void** p, size_t* have, size_t need, bool keep, size_t used) {
+    if (*have >= need) return KK_OK;
+    const size_t bytes = need + need / 4 + 256;
+    void* q = nullptr;
+    if (cudaHostAlloc(&q, bytes, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(h, KK_ERR_OUT_OF_MEMORY, "pinned host allocation of %zu bytes failed", bytes);
+    }
+    if (keep && *p && used) memcpy(q, *p, used);
+    if (*p) cudaFreeHost(*p);
+    *p = q;
+    *have = bytes;
+    return KK_OK;
+}
+
+extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B,
+                                              void* c_row_map, int64_t* c_nnz, int32_t** c_entries, void** c_values,
+                                              int blocks, void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    kk_status_t st;
+    if ((st = check_pair(h, A, B, true)) != KK_OK) return st;
+    if (!c_row_map || !c_nnz || !c_entries || !c_values) return fail(h, KK_ERR_INVALID_ARG, "NULL output pointer");
+    cudaSetDevice(h->device);
+    auto& P = h->hp;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!P.s_in) {
+        cudaStreamCreateWithFlags(&P.s_in, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&P.s_out, cudaStreamNonBlocking);
+    }
+    const int64_t m = A->nrows;
+    const size_t osz = A->offset_type == KK_I64 ? 8 : 4, vsz = A->value_type == KK_F64 ? 8 : 4;
+    auto rmv = [&](const void* rm, int64_t i) -> int64_t {
+        return osz == 8 ? ((const int64_t*)rm)[i] : (int64_t)((const int32_t*)rm)[i];
+    };
+    if (blocks <= 0) blocks = m >= 65536 ? 8 : 1;
+    blocks = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, std::max<int64_t>(m, 1)));
+    std::vector<int64_t> cuts(blocks + 1);
+    for (int q = 0; q <= blocks; ++q) cuts[q] = m * q / blocks;
+    // B once (every block reads all of it)
+    if ((st = ensure(h, P.brm, (B->nrows + 1) * osz, s)) != KK_OK) return st;
+    if ((st = ensure(h, P.bent, B->nnz * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, P.bval, B->nnz * vsz, s)) != KK_OK) return st;
+    cudaStreamSynchronize(s);  // the workspace may have been (re)allocated on s
+    cudaEvent_t ev_b;
+    cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
+    cudaMemcpyAsync(P.brm.p, B->row_map, (B->nrows + 1) * osz, cudaMemcpyHostToDevice, P.s_in);
+    cudaMemcpyAsync(P.bent.p, B->entries, B->nnz * 4, cudaMemcpyHostToDevice, P.s_in);
+    cudaMemcpyAsync(P.bval.p, B->values, B->nnz * vsz, cudaMemcpyHostToDevice, P.s_in);
+    cudaEventRecord(ev_b, P.s_in);
+    kk_csr_t Bd = *B;
+    Bd.row_map = P.brm.p;
+    Bd.entries = (const int32_t*)P.bent.p;
+    Bd.values = P.bval.p;
+    // the blocks' row maps rebased to 0, in pinned staging (block q at offset q + cuts[q])
+    if ((st = ensure_host(h, &P.h_reb, &P.h_reb_bytes, (m + blocks) * osz, false, 0)) != KK_OK) return st;
+    for (int q = 0; q < blocks; ++q) {
+        const int64_t r0 = cuts[q], r1 = cuts[q + 1], base = rmv(A->row_map, r0);
+        for (int64_t r = r0; r <= r1; ++r) {
+            const int64_t v = rmv(A->row_map, r) - base;
+            if (osz == 8)
+                ((int64_t*)P.h_reb)[q + r] = v;
+            else
+                ((int32_t*)P.h_reb)[q + r] = (int32_t)v;
+        }
+    }
+    // staging slots: sized for the largest block's A arrays
+    int64_t max_rows = 0, max_nnz = 0;
+    for (int q = 0; q < blocks; ++q) {
+        max_rows = std::max<int64_t>(max_rows, cuts[q + 1] - cuts[q]);
+        max_nnz = std::max<int64_t>(max_nnz, rmv(A->row_map, cuts[q + 1]) - rmv(A->row_map, cuts[q]));
+    }
+    for (int sl = 0; sl < 2; ++sl) {
+        if ((st = ensure(h, P.arm[sl], (max_rows + 1) * osz, s)) != KK_OK) return st;
+        if ((st = ensure(h, P.aent[sl], max_nnz * 4, s)) != KK_OK) return st;
+        if ((st = ensure(h, P.aval[sl], max_nnz * vsz, s)) != KK_OK) return st;
+        if ((st = ensure(h, P.crm[sl], (max_rows + 1) * osz, s)) != KK_OK) return st;
+    }
+    cudaStreamSynchronize(s);
+    std::vector<cudaEvent_t> ev_in(blocks), ev_c(blocks), ev_out(blocks);
+    for (int q = 0; q < blocks; ++q) {
+        cudaEventCreateWithFlags(&ev_in[q], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_c[q], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_out[q], cudaEventDisableTiming);
+    }
+    std::vector<kk_csr_t> Ab(blocks);
+    auto load_block = [&](int q) {
+        const int sl = q % 2;
+        const int64_t r0 = cuts[q], r1 = cuts[q + 1];
+        const int64_t e0 = rmv(A->row_map, r0), e1 = rmv(A->row_map, r1);
+        if (q >= 2) cudaStreamWaitEvent(P.s_in, ev_c[q - 2], 0);  // slot free once block q-2 is computed
+        cudaMemcpyAsync(P.arm[sl].p, (const char*)P.h_reb + (q + r0) * osz, (r1 - r0 + 1) * osz,
+                        cudaMemcpyHostToDevice, P.s_in);
+        cudaMemcpyAsync(P.aent[sl].p, A->entries + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, P.s_in);
+        cudaMemcpyAsync(P.aval[sl].p, (const char*)A->values + e0 * vsz, (e1 - e0) * vsz, cudaMemcpyHostToDevice,
+                        P.s_in);
+        cudaEventRecord(ev_in[q], P.s_in);
+        kk_csr_t a = *A;
+        a.nrows = r1 - r0;
+        a.nnz = e1 - e0;
+        a.row_map = P.arm[sl].p;
+        a.entries = (const int32_t*)P.aent[sl].p;
+        a.values = P.aval[sl].p;
+        Ab[q] = a;
+    };
+    for (int q = 0; q < std::min(2, blocks); ++q) load_block(q);
+    std::vector<int64_t> nnz_off(blocks + 1, 0);
+    st = KK_OK;
+    for (int q = 0; q < blocks && st == KK_OK; ++q) {
+        const int sl = q % 2;
+        const int64_t r0 = cuts[q], r1 = cuts[q + 1];
+        cudaStreamWaitEvent(s, ev_in[q], 0);
+        cudaStreamWaitEvent(s, ev_b, 0);
+        if (q >= 2) cudaStreamWaitEvent(s, ev_out[q - 2], 0);  // C slot drained to the host
+        int64_t nnz = 0;
+        if ((st = kk_spgemm_symbolic(h, &Ab[q], &Bd, P.crm[sl].p, &nnz, s)) != KK_OK) break;
+        if ((st = ensure(h, P.cent[sl], nnz * 4, s)) != KK_OK) break;
+        if ((st = ensure(h, P.cval[sl], nnz * vsz, s)) != KK_OK) break;
+        if ((st = kk_spgemm_numeric(h, &Ab[q], &Bd, P.crm[sl].p, (int32_t*)P.cent[sl].p, P.cval[sl].p, s)) != KK_OK)
+            break;
+        cudaEventRecord(ev_c[q], s);
+        nnz_off[q + 1] = nnz_off[q] + nnz;
+        // host output capacity (grows on a larger product: earlier blocks are kept)
+        if (P.h_cent_bytes < (size_t)nnz_off[q + 1] * 4 || P.h_cval_bytes < (size_t)nnz_off[q + 1] * vsz) {
+            cudaStreamSynchronize(P.s_out);
+            if ((st = ensure_host(h, &P.h_cent, &P.h_cent_bytes, nnz_off[q + 1] * 4, true, nnz_off[q] * 4)) != KK_OK)
+                break;
+            if ((st = ensure_host(h, &P.h_cval, &P.h_cval_bytes, nnz_off[q + 1] * vsz, true, nnz_off[q] * vsz)) !=
+                KK_OK)
+                break;
+        }
+        cudaStreamWaitEvent(P.s_out, ev_c[q], 0);
+        // rows r0+1..r1 of the row map (entry r0 is the previous block's end, fixed below)
+        cudaMemcpyAsync((char*)c_row_map + (r0 + 1) * osz, (const char*)P.crm[sl].p + osz, (r1 - r0) * osz,
+                        cudaMemcpyDeviceToHost, P.s_out);
+        cudaMemcpyAsync((char*)P.h_cent + nnz_off[q] * 4, P.cent[sl].p, nnz * 4, cudaMemcpyDeviceToHost, P.s_out);
+        cudaMemcpyAsync((char*)P.h_cval + nnz_off[q] * vsz, P.cval[sl].p, nnz * vsz, cudaMemcpyDeviceToHost,
+                        P.s_out);
+        cudaEventRecord(ev_out[q], P.s_out);
+        if (q + 2 < blocks) load_block(q + 2);
+    }
+    cudaStreamSynchronize(P.s_in);
+    cudaStreamSynchronize(P.s_out);
+    cudaStreamSynchronize(s);
+    for (int q = 0; q < blocks; ++q) {
+        cudaEventDestroy(ev_in[q]);
+        cudaEventDestroy(ev_c[q]);
+        cudaEventDestroy(ev_out[q]);
+    }
+    cudaEventDestroy(ev_b);
+    if (st != KK_OK) return st;
+    if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_multiply_host")) != KK_OK) return st;
+    // global row map: block q's local offsets + the nnz of the blocks before it
+    if (osz == 4 && nnz_off[blocks] > INT32_MAX)
+        return fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) = %lld exceeds int32 row offsets; use KK_I64",
+                    (long long)nnz_off[blocks]);
+    for (int q = 0; q < blocks; ++q) {
+        for (int64_t r = cuts[q] + 1; r <= cuts[q + 1]; ++r) {
+            if (osz == 8)
+                ((int64_t*)c_row_map)[r] += nnz_off[q];
+            else
+                ((int32_t*)c_row_map)[r] += (int32_t)nnz_off[q];
+        }
+    }
+    if (osz == 8)
+        ((int64_t*)c_row_map)[0] = 0;
+    else
+        ((int32_t*)c_row_map)[0] = 0;
+    *c_nnz = nnz_off[blocks];
+    *c_entries = (int32_t*)P.h_cent;
+    *c_values = P.h_cval;
     return KK_OK;
 }
 

@@ -14,6 +14,8 @@ or, following the paper's two-phase protocol:
 """
 from __future__ import annotations
 
+import ctypes
+
 from dataclasses import dataclass
 from typing import Optional
 
@@ -190,125 +192,36 @@ class SpGEMM:
 
     # -- end to end from host memory ------------------------------------------------------
     def multiply_host(self, A, B, stream=None, blocks: Optional[int] = None) -> "CsrMatrix":
-        """C = A*B for CSR operands in (pinned) HOST memory, C returned in pinned HOST memory.
+        """C = A*B for CSR operands in (pinned) HOST memory, C returned in HOST memory, through
+        the C ABI's kk_spgemm_multiply_host (B copied once; A in `blocks` row blocks whose
+        copies in both PCIe directions overlap the kernels; the global row map assembled in
+        the library).  C's entries and values are the handle's pinned buffers: valid until
+        the next call on this handle (copy them to keep them)."""
+        import numpy as np
 
-        B is copied to the device once; A is processed in `blocks` contiguous row blocks
-        (default 8 when A has >= 64K rows): block b's host->device copy, its symbolic and
-        numeric phases and the device->host copy of its rows of C run on three streams, so
-        the copies of neighbouring blocks (both PCIe directions) overlap the kernels.  Row
-        blocks are independent products (Eq. 1); the host assembles the
-        global row map from the blocks' row maps and nnz.  Device and pinned staging buffers
-        are cached on the handle.  The result is valid until the next call on this handle."""
         A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
-        dev = self.device
-        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        for M in (A, B):
+            for t in (M.row_map, M.entries, M.values):
+                if t.device.type != "cpu":
+                    raise ValueError("multiply_host takes host (CPU) tensors")
+        a, b = _kk_csr(A, True), _kk_csr(B, True)
         cache = self.__dict__.setdefault("_host_cache", {})
-        m = A.nrows
-        if blocks is None:
-            blocks = 8 if m >= 65536 else 1
-        blocks = max(1, min(int(blocks), max(m, 1)))
-        if "s_in" not in cache:
-            cache["s_in"] = torch.cuda.Stream(dev)
-            cache["s_out"] = torch.cuda.Stream(dev)
-        s_in, s_out = cache["s_in"], cache["s_out"]
-
-        def dbuf(key, n, dtype):
-            t = cache.get(key)
-            if t is None or t.numel() < n or t.dtype != dtype:
-                t = torch.empty(max(n, 1), dtype=dtype, device=dev)
-                cache[key] = t
-            return t[:n]
-
-        def hbuf(key, n, dtype):
-            t = cache.get(key)
-            if t is None or t.numel() < n or t.dtype != dtype:
-                t = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
-                cache[key] = t
-            return t[:n]
-
-        def h2d(key, t):
-            d = dbuf(key, t.numel(), t.dtype)
-            d.copy_(t, non_blocking=True)
-            return d
-
-        # B once (every block reads all of it)
-        ev_b = torch.cuda.Event()
-        with torch.cuda.stream(s_in):
-            Bd = CsrMatrix(B.nrows, B.ncols, h2d("brm", B.row_map), h2d("bent", B.entries), h2d("bval", B.values))
-            ev_b.record(s_in)
-        # A's row blocks; their row maps rebased to 0 in a pinned staging buffer
-        rm = A.row_map
-        cuts = [m * q // blocks for q in range(blocks + 1)]
-        reb = hbuf("a_rm_reb", m + blocks, rm.dtype)
-        roffs = []
-        for q in range(blocks):
-            r0, r1 = cuts[q], cuts[q + 1]
-            o = q + r0
-            torch.sub(rm[r0:r1 + 1], rm[r0], out=reb[o:o + r1 - r0 + 1])
-            roffs.append(o)
-        ev_in = [torch.cuda.Event() for _ in range(blocks)]
-        ev_c = [torch.cuda.Event() for _ in range(blocks)]
-        ev_out = [torch.cuda.Event() for _ in range(blocks)]
-
-        def load_block(q):
-            r0, r1 = cuts[q], cuts[q + 1]
-            e0, e1 = int(rm[r0]), int(rm[r1])
-            sl = q % 2
-            with torch.cuda.stream(s_in):
-                if q >= 2:
-                    s_in.wait_event(ev_c[q - 2])
-                Ab = CsrMatrix(r1 - r0, A.ncols, h2d(f"arm{sl}", reb[roffs[q]:roffs[q] + r1 - r0 + 1]),
-                               h2d(f"aent{sl}", A.entries[e0:e1]), h2d(f"aval{sl}", A.values[e0:e1]))
-                ev_in[q].record(s_in)
-            return Ab
-
-        h_rm = hbuf("h_crm", m + 1, rm.dtype)
-        pending = [load_block(q) for q in range(min(2, blocks))]
-        nnz_off = [0] * (blocks + 1)
-        for q in range(blocks):
-            r0, r1 = cuts[q], cuts[q + 1]
-            Ab = pending[q]
-            sl = q % 2
-            st.wait_event(ev_in[q])
-            st.wait_event(ev_b)
-            if q >= 2:
-                st.wait_event(ev_out[q - 2])
-            crm = dbuf(f"crm{sl}", r1 - r0 + 1, rm.dtype)
-            crm, nnz = self.symbolic(Ab, Bd, c_row_map=crm, stream=st)
-            cent = dbuf(f"cent{sl}", nnz, torch.int32)
-            cval = dbuf(f"cval{sl}", nnz, A.values.dtype)
-            self.numeric(Ab, Bd, crm, nnz=nnz, c_entries=cent, c_values=cval, stream=st)
-            ev_c[q].record(st)
-            nnz_off[q + 1] = nnz_off[q] + nnz
-            # host output capacity (grows only on a first, larger call: earlier blocks are kept)
-            for key, dt in (("h_cent", torch.int32), ("h_cval", A.values.dtype)):
-                t = cache.get(key)
-                if t is None or t.numel() < nnz_off[q + 1] or t.dtype != dt:
-                    s_out.synchronize()
-                    nt = torch.empty(max(int(nnz_off[q + 1] * 1.25), 1), dtype=dt, pin_memory=True)
-                    if t is not None and t.dtype == dt and nnz_off[q]:
-                        nt[:nnz_off[q]].copy_(t[:nnz_off[q]])
-                    cache[key] = nt
-            h_ent, h_val = cache["h_cent"], cache["h_cval"]
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_c[q])
-                h_rm[r0:r1 + 1].copy_(crm, non_blocking=True)
-                h_ent[nnz_off[q]:nnz_off[q + 1]].copy_(cent, non_blocking=True)
-                h_val[nnz_off[q]:nnz_off[q + 1]].copy_(cval, non_blocking=True)
-                ev_out[q].record(s_out)
-            if q + 2 < blocks:
-                pending.append(load_block(q + 2))
-        s_out.synchronize()
-        # global row map: block q's local offsets + the nnz of the blocks before it (block
-        # q+1's copy overwrote the shared boundary entry with its local 0; restored here)
-        for q in range(blocks):
-            r0, r1 = cuts[q], cuts[q + 1]
-            if nnz_off[q]:
-                h_rm[r0 + 1:r1 + 1] += nnz_off[q]
-            h_rm[r0] = nnz_off[q]
-        h_rm[m] = nnz_off[blocks]
-        tot = nnz_off[blocks]
-        return CsrMatrix(m, B.ncols, h_rm, cache["h_cent"][:tot], cache["h_cval"][:tot])
+        rm = cache.get("h_crm")
+        if rm is None or rm.numel() < A.nrows + 1 or rm.dtype != A.row_map.dtype:
+            rm = torch.empty(A.nrows + 1, dtype=A.row_map.dtype, pin_memory=True)
+            cache["h_crm"] = rm
+        rm = rm[:A.nrows + 1]
+        nnz, pe, pv = _ffi.kk_spgemm_multiply_host(self._h, a, b, rm.data_ptr(), blocks or 0,
+                                                   _stream_ptr(self.device, stream))
+        vt = np.float64 if A.values.dtype == torch.float64 else np.float32
+        if nnz:
+            ent = torch.from_numpy(np.ctypeslib.as_array((ctypes.c_int32 * nnz).from_address(pe)))
+            val = torch.from_numpy(np.frombuffer((ctypes.c_char * (nnz * np.dtype(vt).itemsize)).from_address(pv),
+                                                 dtype=vt))
+        else:
+            ent = torch.zeros(0, dtype=torch.int32)
+            val = torch.zeros(0, dtype=A.values.dtype)
+        return CsrMatrix(A.nrows, B.ncols, rm, ent, val)
 
     # -- individual steps ----------------------------------------------------------------
     def row_flops(self, A, B, scan: bool = True, total: bool = True, stream=None):
