@@ -50,10 +50,12 @@ _OFF = {torch.int32: _ffi.KK_I32, torch.int64: _ffi.KK_I64}
 _VAL = {torch.float32: _ffi.KK_F32, torch.float64: _ffi.KK_F64}
 
 
-def _kk_csr(M: CsrMatrix, need_values: bool) -> _ffi.kk_csr_t:
+def _kk_csr(M: CsrMatrix, need_values: bool, host: bool = False) -> _ffi.kk_csr_t:
+    """kk_csr_t of M: device tensors, or host tensors for kk_spgemm_multiply_host (host=True;
+    the library copies them to the device -- there is no CPU compute path)."""
     for name, t in (("row_map", M.row_map), ("entries", M.entries)):
-        if not t.is_cuda:
-            raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+        if t.is_cuda == host:
+            raise ValueError(f"{name} must be a {'host' if host else 'CUDA'} tensor")
         if not t.is_contiguous():
             raise ValueError(f"{name} must be contiguous")
     if M.row_map.dtype not in _OFF:
@@ -68,8 +70,8 @@ def _kk_csr(M: CsrMatrix, need_values: bool) -> _ffi.kk_csr_t:
     c.row_map = M.row_map.data_ptr()
     c.entries = M.entries.data_ptr() if M.entries.numel() else None
     if M.values is not None:
-        if not M.values.is_cuda or not M.values.is_contiguous() or M.values.dtype not in _VAL:
-            raise TypeError("values must be a contiguous CUDA float32/float64 tensor")
+        if M.values.is_cuda == host or not M.values.is_contiguous() or M.values.dtype not in _VAL:
+            raise TypeError(f"values must be a contiguous {'host' if host else 'CUDA'} float32/float64 tensor")
         c.value_type = _VAL[M.values.dtype]
         c.values = M.values.data_ptr() if M.values.numel() else None
     else:
@@ -200,11 +202,7 @@ class SpGEMM:
         import numpy as np
 
         A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
-        for M in (A, B):
-            for t in (M.row_map, M.entries, M.values):
-                if t.device.type != "cpu":
-                    raise ValueError("multiply_host takes host (CPU) tensors")
-        a, b = _kk_csr(A, True), _kk_csr(B, True)
+        a, b = _kk_csr(A, True, host=True), _kk_csr(B, True, host=True)
         cache = self.__dict__.setdefault("_host_cache", {})
         rm = cache.get("h_crm")
         if rm is None or rm.numel() < A.nrows + 1 or rm.dtype != A.row_map.dtype:
