@@ -89,6 +89,13 @@ typedef struct {
                           (sorted (word, mask) pairs, <= 64 words) in the handle, and numeric
                           accumulates those rows by rank lookup; 0: numeric re-derives every
                           row.  Costs up to 48 * 8 bytes of workspace per row of A. */
+    int deterministic; /* 1: bitwise-reproducible values from run to run (the handle-selected
+                          variant of PAPER.md:708-712): the tiers that would add products into
+                          a shared or global accumulator with atomics (long rows, short-B-row
+                          warp tables) add them in A-entry order instead.  Needs strictly
+                          increasing B rows (then every other tier is order-fixed already);
+                          otherwise kk_spgemm_symbolic returns KK_ERR_UNSUPPORTED_TYPE.
+                          Default 0 (long rows are slower in this mode). */
     kk_alloc_fn alloc;
     kk_free_fn free;
     void* alloc_ctx;

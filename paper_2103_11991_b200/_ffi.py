@@ -35,7 +35,8 @@ FREE_FN = ctypes.CFUNCTYPE(None, _vp, ctypes.c_size_t, _vp, _vp)
 class kk_spgemm_opts_t(ctypes.Structure):
     _fields_ = [("sort_rows", ctypes.c_int), ("compression", ctypes.c_int), ("validate", ctypes.c_int),
                 ("num_streams", ctypes.c_int), ("timing", ctypes.c_int),
-                ("patterns", ctypes.c_int), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", _vp)]
+                ("patterns", ctypes.c_int), ("deterministic", ctypes.c_int), ("alloc", ALLOC_FN), ("free", FREE_FN),
+                ("alloc_ctx", _vp)]
 
 
 class kk_spgemm_stats_t(ctypes.Structure):

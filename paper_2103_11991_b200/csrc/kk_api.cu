@@ -517,6 +517,9 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     if (hs.overflow)
         return fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) = %llu exceeds int32 row offsets; use KK_I64",
                     (unsigned long long)hs.nnz_c);
+    if (h->opts.deterministic && !hs.b_strict && A->nrows > 0 && B->nnz > 0)
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE,
+                    "deterministic mode needs strictly increasing B rows (sorted, no duplicate columns)");
     *c_nnz = (int64_t)hs.nnz_c;
     // record for numeric
     h->rec.valid = true;
@@ -571,6 +574,7 @@ static kk_status_t numeric_impl(kk_spgemm_handle_t h, const kk_csr_t* A, const k
     na.sort = h->opts.sort_rows != 0;
     na.strict = h->stats.b_strict != 0;
     na.sorted = h->stats.b_sorted != 0;
+    na.det = h->opts.deterministic != 0;
     if ((st = ensure(h, h->workctr, 16, s)) != KK_OK) return st;
     na.work_ctr = (int*)h->workctr.p;
     na.wlo = (const int32_t*)h->wlo.p;
@@ -589,6 +593,8 @@ static kk_status_t numeric_impl(kk_spgemm_handle_t h, const kk_csr_t* A, const k
     na.cursors = (int32_t*)h->cursors.p;
     na.st = (const DevStatus*)h->status.p;
     na.logG = pick_logG(B->nrows > 0 ? (double)B->nnz / (double)B->nrows : 1.0);
+    // deterministic: one B row per warp step in the warp tables (plain adds, step order)
+    if (na.det) na.logG = 5;
     na.dinv = dinv;
     na.omega = omega;
     cudaStream_t side = nullptr;

@@ -143,6 +143,7 @@ struct NumArgs {
     bool off64, f64, sort;
     bool strict;                 // every B row strictly increasing (host copy of the a4 flag)
     bool sorted;                 // every B row non-decreasing (host copy of the a4 flag)
+    bool det = false;            // opts.deterministic: products added in A-entry order
     int* work_ctr = nullptr;     // device scratch: dynamic row counters of the cluster tier
     MatView A, B;
     int64_t k;

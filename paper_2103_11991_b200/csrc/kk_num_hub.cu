@@ -69,13 +69,26 @@ __device__ __forceinline__ void hub_segment(const int32_t* __restrict__ bent, co
     }
 }
 
-// nlist[0]: list length, nlist[1]: batch counter (both zero on entry)
+// nlist[0]: list length, nlist[1]: batch counter (both zero on entry).  ordered: the A
+// entries one at a time by the whole CTA, in order, a barrier after each (deterministic mode:
+// with strictly increasing B rows the products of one A entry have distinct columns, so
+// f may add without atomics and every output sums its products in A order).
 template <bool VALS, typename OffT, typename ValT, typename F>
 __device__ __forceinline__ void hub_walk(int64_t s, int64_t e, const int32_t* __restrict__ aent,
                                          const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                          const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
-                                         int* list, int* nlist, F f) {
+                                         int* list, int* nlist, F f, bool ordered = false) {
     const int lane = threadIdx.x & 31;
+    if (ordered) {
+        for (int64_t p = s; p < e; ++p) {
+            const int j = __ldg(aent + p);
+            const ValT a = VALS ? __ldg(aval + p) : (ValT)0;
+            const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+            hub_segment<4, VALS>(bent, bval, bs, be - bs, (int)threadIdx.x, HUB_THREADS, a, f);
+            __syncthreads();
+        }
+        return;
+    }
     while (true) {
         int b = 0;
         if (lane == 0) b = atomicAdd(nlist + 1, 1);
@@ -132,7 +145,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
                                                              const OffT* __restrict__ crm, int32_t* __restrict__ cent,
                                                              ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                              const int* __restrict__ bin_start, int bin, int64_t k,
-                                                             int vcap, int big) {
+                                                             int vcap, int big, int det) {
     extern __shared__ __align__(16) uint32_t sm_hub[];
     const int64_t NW = hub_words(k);
     uint32_t* bm = sm_hub;
@@ -216,12 +229,18 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
             if (gw + 2 < w) rk += __popc(bm[gw + 2]);
             rk += __popc(bm[w] & ((1u << (c & 31)) - 1u));
             if ((int64_t)rk < clen) {
-                if (inshared)
+                if (det) {
+                    if (inshared)
+                        svals[rk] += prod;
+                    else
+                        cval[cb + rk] += prod;
+                } else if (inshared) {
                     atomicAdd(&svals[rk], prod);
-                else
+                } else {
                     atomicAdd(&cval[cb + rk], prod);
+                }
             }
-        });
+        }, det != 0);
         __syncthreads();
         if (inshared) {
             for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) __stcs(cval + cb + t, svals[t]);
@@ -516,7 +535,7 @@ static bool hub_bins_t(Launch& L, const NumArgs& a, cudaStream_t s) {
     // (b) the cluster tier for the longer rows: sorted B, slice bit vector + value window fit
     const size_t cfix = cl_fixed_smem(a.k);
     const int cvcap = cfix + 4096 * sizeof(ValT) <= SMEM_MAX ? (int)((SMEM_MAX - cfix) / sizeof(ValT)) - 64 : 0;
-    const bool cluster = use_cluster() && a.sorted && a.work_ctr != nullptr && cvcap >= 4096;
+    const bool cluster = use_cluster() && !a.det && a.sorted && a.work_ctr != nullptr && cvcap >= 4096;
     {
         auto kern = k_num_hub<OffT, ValT>;
         KCfg c = kernel_cfg(kern, HUB_THREADS, hsm_v, L.num_sms);
@@ -525,7 +544,8 @@ static bool hub_bins_t(Launch& L, const NumArgs& a, cudaStream_t s) {
         kern<<<grid, HUB_THREADS, hsm_v, s>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                               (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                               (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
-                                              a.bin_start, NUM_DENSE_BIN, a.k, vcap, cluster ? 1 : 0);
+                                              a.bin_start, NUM_DENSE_BIN, a.k, vcap, cluster ? 1 : 0,
+                                              a.det ? 1 : 0);
         L.end(s);
     }
     if (cluster) {

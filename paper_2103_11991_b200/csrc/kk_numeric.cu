@@ -69,7 +69,11 @@ __global__ void __launch_bounds__(256, 1) k_num_warp(const OffT* __restrict__ ar
             for (int64_t q = bs + lane; q < be; q += 32) {
                 bool fresh;
                 const uint32_t h = probe_claim<S>(keys, (uint32_t)__ldg(bent + q), &fresh);
-                atomicAdd(&vals[h], __ldg(bval + q));
+                if (plain)  // strictly increasing B(i,:): distinct keys in a step
+                    vals[h] += __ldg(bval + q);
+                else
+                    atomicAdd(&vals[h], __ldg(bval + q));
+                if (plain) __syncwarp();
             }
             __syncwarp();
         }
@@ -134,7 +138,8 @@ __global__ void __launch_bounds__(256) k_num_dense(const OffT* __restrict__ arm,
                                                    const OffT* __restrict__ crm, int32_t* __restrict__ cent,
                                                    ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                    const int* __restrict__ bin_start, int bin, int64_t k, int W,
-                                                   int32_t* __restrict__ cursors, const DevStatus* __restrict__ st) {
+                                                   int32_t* __restrict__ cursors, const DevStatus* __restrict__ st,
+                                                   int det) {
     extern __shared__ __align__(16) unsigned char sm_dense[];
     ValT* win = (ValT*)sm_dense;
     uint32_t* bmp = (uint32_t*)(win + W);
@@ -155,16 +160,29 @@ __global__ void __launch_bounds__(256) k_num_dense(const OffT* __restrict__ arm,
         for (int64_t lo = 0; lo < k; lo += W) {
             const int64_t hi = min(k, lo + (int64_t)W);
             const bool single = (lo == 0 && hi == k);
-            for (int64_t p = s + warp; p < e; p += warps) {
+            // deterministic: A entries one at a time by the whole CTA, in order (strict B: the
+            // entries of one B row have distinct columns, so plain adds); else warp per entry
+            const int pw = det ? 0 : warp, pstep = det ? 1 : warps;
+            for (int64_t p = s + pw; p < e; p += pstep) {
                 const int j = __ldg(aent + p);
                 const ValT a = __ldg(aval + p);
                 const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
                 auto ins = [&](int64_t q, int64_t c) {
                     const int x = (int)(c - lo);
-                    atomicAdd(&win[x], a * __ldg(bval + q));
+                    if (det)
+                        win[x] += a * __ldg(bval + q);
+                    else
+                        atomicAdd(&win[x], a * __ldg(bval + q));
                     atomicOr(&bmp[x >> 5], 1u << (x & 31));
                 };
-                if (single) {
+                if (det) {
+                    // the whole CTA on this B row (entries past the window are skipped)
+                    for (int64_t q = bs + threadIdx.x; q < be; q += blockDim.x) {
+                        const int64_t c = __ldg(bent + q);
+                        if (c >= lo && c < hi) ins(q, c);
+                    }
+                    __syncthreads();
+                } else if (single) {
                     for (int64_t q = bs + lane; q < be; q += 32) ins(q, __ldg(bent + q));
                 } else if (sorted) {
                     const int64_t q0 = bs + (lo == 0 ? 0 : cursors[p]);
@@ -527,7 +545,7 @@ static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_strea
         kern<<<grid, threads, smem, s>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                          (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                          (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm, a.bin_start,
-                                         NUM_DENSE_BIN, a.k, (int)W, a.cursors, a.st);
+                                         NUM_DENSE_BIN, a.k, (int)W, a.cursors, a.st, a.det ? 1 : 0);
         L.end(s);
     }
     launch_num_tiny<OffT, ValT>(L, a);

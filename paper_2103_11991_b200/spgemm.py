@@ -91,7 +91,7 @@ class SpGEMM:
     """Kernel handle: options + the symbolic state reused by numeric."""
 
     def __init__(self, device=None, sort_rows: bool = True, compression="auto", validate: bool = False,
-                 num_streams: int = 2, timing: bool = False, patterns: bool = True):
+                 num_streams: int = 2, timing: bool = False, patterns: bool = True, deterministic: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2103_11991_b200 needs a CUDA device (there is no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
@@ -102,6 +102,7 @@ class SpGEMM:
         o.validate = int(bool(validate))
         o.num_streams = int(num_streams)
         o.timing = int(bool(timing))
+        o.deterministic = int(bool(deterministic))
         o.patterns = int(bool(patterns))
         self._h = _ffi.kk_spgemm_create(self.device.index, o)
 

@@ -440,3 +440,33 @@ def test_cluster_tier_windows(oracle_mod):
         got = gpu_spgemm(A, B, value_dtype=vt, offset_dtype=torch.int64, timing=True)
         assert "num_hub" in got[3]["kernels"], got[3]["kernels"]
         assert_parity(oracle_mod, A, B, got, value_dtype=vt)
+
+
+@pytest.mark.parametrize("kind", ["hub", "dense_window", "short_b_rows", "C2"])
+def test_deterministic_mode(oracle_mod, kind):
+    """opts.deterministic (handle-selected variant): random values, tiers
+    that add with atomics by default; two runs are bitwise equal and within the parity bound."""
+    if kind == "hub":
+        A, B = _long_rows(31)  # k = 200K: the CTA bit-vector tier
+    elif kind == "dense_window":
+        A = g.random_csr(24, 300, 100, seed=41, empty_row_frac=0.0)
+        B = g.random_csr(300, 20000, 300, seed=42, empty_row_frac=0.0)  # k <= 25.6K: windowed
+    elif kind == "short_b_rows":
+        A = g.random_csr(400, 300, 40, seed=43)
+        B = g.random_csr(300, 500, 2, seed=44)  # ~1 entry per B row: sub-warp groups otherwise
+    else:
+        A, B = g.config("C2", size=14, values="random")
+    runs = [gpu_spgemm(A, B, deterministic=True) for _ in range(2)]
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+    assert np.array_equal(runs[0][2].view(np.int64), runs[1][2].view(np.int64)), "values differ between runs"
+    assert_parity(oracle_mod, A, B, runs[0])
+
+
+def test_deterministic_needs_strict_b():
+    from paper_2103_11991_b200._ffi import KKError, KK_ERR_UNSUPPORTED_TYPE
+
+    A = g.random_csr(30, 25, 10, seed=51, sorted_rows=False)
+    B = g.random_csr(25, 45, 10, seed=52, sorted_rows=False, duplicates=True)
+    with pytest.raises(KKError) as e:
+        gpu_spgemm(A, B, deterministic=True)
+    assert e.value.status == KK_ERR_UNSUPPORTED_TYPE
