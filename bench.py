@@ -230,12 +230,36 @@ def time_oracle_once(oracle, As, Bh):
     return time.perf_counter() - t0
 
 
+def host_info():
+    """CPU model (lscpu), logical CPUs usable by this process, host RAM."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    ram = None
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal:"):
+                    ram = round(int(line.split()[1]) / 1024 ** 2, 1)
+                    break
+    except Exception:
+        pass
+    return {"cpu_model": model, "cpus_usable": len(os.sched_getaffinity(0)), "host_ram_gib": ram}
+
+
 def cpu_baseline(A, B, seconds, rows):
+    """The oracle as it stands on the host: all usable cores (the reported value) and one
+    thread (OMP=1, the plain oracle; a fifth of the time budget), SURVEY §8d."""
     import oracle
 
     oracle.build()
     cores = len(os.sched_getaffinity(0))
-    oracle.set_num_threads(cores)
     from workloads import generators as g
 
     def host(M):
@@ -245,14 +269,24 @@ def cpu_baseline(A, B, seconds, rows):
     Bh = host(B)
     As, r0 = oracle_sample(host(A), rows)
     f, muladds = oracle.row_flops(As, Bh)
-    tot, reps = 0.0, 0
-    while reps < 1 or (tot < seconds and reps < 50):
-        tot += time_oracle_once(oracle, As, Bh)
-        reps += 1
-    value = 2.0 * muladds * reps / tot / 1e9
-    return {"value": round(value, 3), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+
+    def timed(threads, budget):
+        oracle.set_num_threads(threads)
+        tot, reps = 0.0, 0
+        while reps < 1 or (tot < budget and reps < 50):
+            tot += time_oracle_once(oracle, As, Bh)
+            reps += 1
+        return 2.0 * muladds * reps / tot / 1e9, reps, tot
+
+    value, reps, tot = timed(cores, seconds)
+    used = oracle.num_threads()
+    v1, reps1, tot1 = timed(1, seconds / 5)
+    oracle.set_num_threads(cores)
+    return {"value": round(value, 3), "unit": UNIT, "cores": used, "kind": "oracle",
             "sample": f"rows [{r0}, {r0 + As.nrows}) of A ({As.nrows} of {A.nrows} rows, {muladds} multiply-adds) "
-                      f"x full B, symbolic+numeric, {reps} reps in {tot:.2f} s, OpenMP threads={oracle.num_threads()}"}
+                      f"x full B, symbolic+numeric, {reps} reps in {tot:.2f} s, OpenMP threads={used}",
+            "one_thread": {"value": round(v1, 3), "reps": reps1, "seconds": round(tot1, 2)},
+            "host": host_info()}
 
 
 def run_reference(args):
@@ -285,7 +319,7 @@ def run_reference(args):
                       "offsets": "int32" if offset_dtype_for(args.config) == torch.int32 else "int64"},
            "impl": "reference",
            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-                            "sample": sample},
+                            "sample": sample, "host": host_info()},
            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/kk_spgemm.h"
 #include "kk_internal.cuh"
 
@@ -143,6 +145,13 @@ struct kk_spgemm_handle_s {
         void* h_cval = nullptr;
         size_t h_cval_bytes = 0;
     } hp;
+};
+
+// NVTX ranges around the entry points and the symbolic steps (visible in nsys / ncu range
+// filters; header-only NVTX v3, no-ops without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 
 static kk_status_t fail(kk_spgemm_handle_t h, kk_status_t s, const char* fmt, ...) {
@@ -351,6 +360,7 @@ static kk::Launch make_launch(kk_spgemm_handle_t h, cudaStream_t s) {
 
 kk_status_t kk_spgemm_compress(kk_spgemm_handle_t h, const kk_csr_t* B, int32_t* len, uint64_t* pairs,
                                void* stream) {
+    NvtxRange nvtx_("kk_spgemm_compress");
     if (!h) return KK_ERR_INVALID_ARG;
     kk_status_t st;
     if ((st = check_csr(h, B, "B", false)) != KK_OK) return st;
@@ -370,6 +380,7 @@ kk_status_t kk_spgemm_compress(kk_spgemm_handle_t h, const kk_csr_t* B, int32_t*
 
 kk_status_t kk_spgemm_row_flops(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, int64_t* flops,
                                 int64_t* flops_scan, int64_t* total, void* stream) {
+    NvtxRange nvtx_("kk_spgemm_row_flops");
     if (!h) return KK_ERR_INVALID_ARG;
     kk_status_t st;
     if ((st = check_pair(h, A, B, false)) != KK_OK) return st;
@@ -405,6 +416,7 @@ kk_status_t kk_spgemm_row_flops(kk_spgemm_handle_t h, const kk_csr_t* A, const k
 
 kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, void* c_row_map,
                                int64_t* c_nnz, void* stream) {
+    NvtxRange nvtx_("kk_spgemm_symbolic");
     if (!h) return KK_ERR_INVALID_ARG;
     h->rec.valid = false;
     kk_status_t st;
@@ -449,6 +461,7 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     const MatView Av = view(A), Bv = view(B);
 
     kk::init_status(L, dst);
+    nvtxRangePushA("a4 compress + a1 flops + a2 scan + a3 bins");
     // a4: sortedness flags (+ B_C unless compression is off)
     kk::check_compress(L, off64, Bv, k, comp_mode != 0, h->opts.validate != 0, (int32_t*)h->bc_len.p,
                        (uint2*)h->pairs.p, (int4*)h->bmeta.p, dst);
@@ -463,7 +476,9 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     // the symbolic bin sizes on the host (one sync): empty bins are not launched and grids
     // are sized to their bins
     cudaMemcpyAsync(h->h_status->sym_bin_start, sym_start, sizeof(int) * (kk::NB + 1), cudaMemcpyDeviceToHost, s);
+    nvtxRangePop();
     if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_symbolic bins")) != KK_OK) return st;
+    NvtxRange nvtx_a5("a5 symbolic bins + a6 row map");
     // a5: symbolic kernels per bin (dense bin on the side stream)
     kk::SymArgs sa;
     sa.off64 = off64;
@@ -556,6 +571,7 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
 
 static kk_status_t numeric_impl(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, const void* c_row_map,
                                 int32_t* c_entries, void* c_values, void* stream, const void* dinv, double omega) {
+    NvtxRange nvtx_(dinv ? "kk_spgemm_jacobi_numeric" : "kk_spgemm_numeric");
     if (!h) return KK_ERR_INVALID_ARG;
     kk_status_t st;
     if ((st = check_pair(h, A, B, true)) != KK_OK) return st;
@@ -714,6 +730,7 @@ static kk_status_t ensure_host(kk_spgemm_handle_t h, void** p, size_t* have, siz
 extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B,
                                               void* c_row_map, int64_t* c_nnz, int32_t** c_entries, void** c_values,
                                               int blocks, void* stream) {
+    NvtxRange nvtx_("kk_spgemm_multiply_host");
     if (!h) return KK_ERR_INVALID_ARG;
     kk_status_t st;
     if ((st = check_pair(h, A, B, true)) != KK_OK) return st;
@@ -886,6 +903,7 @@ static kk_status_t check_add_pair(kk_spgemm_handle_t h, const kk_csr_t* A, const
 
 kk_status_t kk_spadd_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_csr_t* B, void* c_row_map,
                               int64_t* c_nnz, void* stream) {
+    NvtxRange nvtx_("kk_spadd_symbolic");
     if (!h) return KK_ERR_INVALID_ARG;
     h->addrec.valid = false;
     kk_status_t st;
@@ -941,6 +959,7 @@ kk_status_t kk_spadd_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
 
 kk_status_t kk_spadd_numeric(kk_spgemm_handle_t h, double alpha, const kk_csr_t* A, double beta, const kk_csr_t* B,
                              const void* c_row_map, int32_t* c_entries, void* c_values, void* stream) {
+    NvtxRange nvtx_("kk_spadd_numeric");
     if (!h) return KK_ERR_INVALID_ARG;
     kk_status_t st;
     if ((st = check_add_pair(h, A, B, true)) != KK_OK) return st;
