@@ -22,7 +22,10 @@ LIB = os.path.join(PKG, "libkk_spgemm.so")
 BUILD = os.path.join(PKG, "_build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+# -fmad=false: every product is rounded before it is added (a*b then +, like the oracle's
+# -ffp-contract=off), whichever tier a row lands in -- the tier of a row can depend on the
+# pattern pool's fill order, and the deterministic mode needs the same arithmetic in all
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-I" + os.path.join(ROOT, "include")]
 
 
