@@ -946,7 +946,48 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
                     act = actn;
                 }
             };
-            if (maxbl <= 8)
+            if (COMP && !HT && atom && maxbl <= 32) {
+                // the chunk's B_C rows back to back, 32 pairs per step: one round of atomic ORs
+                // per step (lanes of different rows sharing a word are ordered by the atomics),
+                // no lanes idle past the end of short rows.  Row of flat pair f: the rows that
+                // start in the step's window are one OR-reduction of their start bits; a lane's
+                // row is the count of those at or below it (rows are non-empty, so starts are
+                // distinct).  Pairs are loaded one step ahead.
+                int pex = lane < ntr ? rec[lane].y : 0;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int y = __shfl_up_sync(FULL, pex, d);
+                    if (lane >= d) pex += y;
+                }
+                const int T = __shfl_sync(FULL, pex, 31);
+                pex -= lane < ntr ? rec[lane].y : 0;  // exclusive prefix: first pair of row lane
+                int cur = -1;
+                auto fetch = [&](int f0, uint2& p, bool& act) {
+                    const unsigned M = __reduce_or_sync(
+                        FULL, (lane < ntr && pex >= f0 && pex < f0 + 32) ? 1u << (pex - f0) : 0u);
+                    const int t = min(max(cur + __popc(M & lanemask_le()), 0), ntr - 1);
+                    cur += __popc(M);
+                    const int2 rr = rec[t];
+                    const int f = f0 + lane;
+                    act = f < T;
+                    const int off = min(f - __shfl_sync(FULL, pex, t), rr.y - 1);
+                    p = pair_at(rr.x + max(off, 0));
+                };
+                uint2 p;
+                bool act;
+                fetch(0, p, act);
+                for (int f0 = 0; f0 < T; f0 += 32) {
+                    uint2 pn = p;
+                    bool actn = false;
+                    if (f0 + 32 < T) fetch(f0 + 32, pn, actn);
+                    uint32_t tag = 0;
+                    const uint32_t old = rmw(p.x, p.y, act, false, tag);
+                    __syncwarp();
+                    post(tag, p.y, old, act);
+                    p = pn;
+                    act = actn;
+                }
+            } else if (maxbl <= 8)
                 run(std::integral_constant<int, 4>{});
             else if (maxbl <= 10)
                 run(std::integral_constant<int, 3>{});
