@@ -144,6 +144,9 @@ struct NumArgs {
     bool strict;                 // every B row strictly increasing (host copy of the a4 flag)
     bool sorted;                 // every B row non-decreasing (host copy of the a4 flag)
     bool det = false;            // opts.deterministic: products added in A-entry order
+    // 1-D linear texture objects over B.entries / B.values (0: none; the pattern tier then
+    // loads B with LDG)
+    unsigned long long tex_ent = 0, tex_val = 0;
     int* work_ctr = nullptr;     // device scratch: dynamic row counters of the cluster tier
     MatView A, B;
     int64_t k;

@@ -313,7 +313,7 @@ struct RankLayout {
     }
 };
 
-template <typename OffT, typename ValT, int CAP, int MINB, bool HASHW>
+template <typename OffT, typename ValT, int CAP, int MINB, bool HASHW, bool TEX = false>
 __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                         const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                                         const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                                                         const int* __restrict__ bin_start, int bin,
                                                         const uint2* __restrict__ pat, const long long* __restrict__ pat_off,
                                                         const int* __restrict__ pat_len, const ValT* __restrict__ dinv,
-                                                        double omega) {
+                                                        double omega, cudaTextureObject_t tb, cudaTextureObject_t tv) {
     using LY = RankLayout<ValT, CAP, HASHW>;
     using SlotT = typename LY::SlotT;
     constexpr uint32_t NS = (uint32_t)LY::NS;
@@ -436,8 +436,19 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                     const int4 rr = *(const int4*)(sm_rank + o_rec + (uint32_t)min(t, nt - 1) * 16u);
                     valid = t < nt && lane < rr.y;
                     const int q = rr.x + min(lane, rr.y - 1);
-                    col = __ldg(bent + q);
-                    bv = __ldg(bval + q);
+                    if constexpr (TEX) {
+                        // B through the texture pipe (its wavefronts are not the LSU's)
+                        col = tex1Dfetch<int>(tb, q);
+                        if constexpr (sizeof(ValT) == 8) {
+                            const int2 v = tex1Dfetch<int2>(tv, q);
+                            bv = (ValT)__hiloint2double(v.y, v.x);
+                        } else {
+                            bv = (ValT)tex1Dfetch<float>(tv, q);
+                        }
+                    } else {
+                        col = __ldg(bent + q);
+                        bv = __ldg(bval + q);
+                    }
                     a = (ValT)__hiloint2double(rr.w, rr.z);
                 };
                 int colA, colB;
@@ -566,7 +577,12 @@ static void launch_num_rank(Launch& L, const NumArgs& a, int bin) {
     if (rows <= 0) return;
     const int warps = 8;
     const size_t smem = (size_t)warps * RankLayout<ValT, CAP, HASHW>::bytes;
-    auto kern = k_num_rank<OffT, ValT, CAP, 4, HASHW>;
+    // B's entries and values through the texture pipe when the handle made texture objects
+    // for them (C2: num_rank 1.97 -> 1.88 ms; the kernel is bound by the LSU's L1 data
+    // wavefronts, and texture fetches are the TEX pipe's)
+    const cudaTextureObject_t tb = a.tex_ent, tv = a.tex_val;
+    const bool tex = tb != 0 && tv != 0;
+    auto kern = tex ? k_num_rank<OffT, ValT, CAP, 4, HASHW, true> : k_num_rank<OffT, ValT, CAP, 4, HASHW, false>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (rows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
@@ -574,7 +590,8 @@ static void launch_num_rank(Launch& L, const NumArgs& a, int bin) {
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                                (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                                (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
-                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len, (const ValT*)a.dinv, a.omega);
+                                               a.bin_start, bin, a.pat, a.pat_off, a.pat_len, (const ValT*)a.dinv, a.omega,
+                                               tb, tv);
     L.end(L.stream);
 }
 
