@@ -170,9 +170,9 @@ kk_status_t kk_spgemm_numeric(kk_spgemm_handle_t handle, const kk_csr_t* A, cons
  * Preconditions: A square (A.nrows == A.ncols == B.nrows, else KK_ERR_DIM_MISMATCH);
  * every row of A stores its diagonal entry -- checked only when
  * opts.validate = 1 (KK_ERR_INVALID_ARG); without it, entries of B(i,:) outside E(i,:)'s
- * pattern are dropped.  Rows with nnz(C_i) > 512 (the dense tiers) are not supported yet:
- * KK_ERR_UNSUPPORTED_TYPE.  Per row the kernel forms -omega * dinv[i] once, scales E(i,:)
- * by it and inserts B(i,:) into the accumulator (the paper's fusion).
+ * pattern are dropped.  Every tier has the fused form, the long-row (dense) tiers included:
+ * per row the kernel forms -omega * dinv[i] once, scales E(i,:) by it and inserts B(i,:)
+ * into the accumulator (the paper's fusion).
  * Asynchronous on `stream` (the validate check synchronises it). */
 kk_status_t kk_spgemm_jacobi_numeric(kk_spgemm_handle_t handle, double omega, const void* dinv, const kk_csr_t* A,
                                      const kk_csr_t* B, const void* c_row_map, int32_t* c_entries, void* c_values,
@@ -183,8 +183,10 @@ kk_status_t kk_spgemm_jacobi_numeric(kk_spgemm_handle_t handle, double omega, co
  * A.nrows+1 of A.offset_type, caller-allocated), returns nnz(C) in *c_nnz (host), and keeps
  * in the handle the scatter position of every entry of A and B in its row of C (the
  * paper's Apos / Bpos).  Rows may be unsorted and unmerged (duplicate columns inside A or
- * B are merged into one entry of C); C's pattern is the structural union.  Rows with
- * nnz(A_i) + nnz(B_i) > 256 return KK_ERR_UNSUPPORTED_TYPE.  Synchronises `stream`. */
+ * B are merged into one entry of C); C's pattern is the structural union.  A warp owns a row
+ * of nnz(A_i) + nnz(B_i) <= 256 (register bitonic sort / merge), a CTA a longer row (shared-
+ * memory bitonic sort); rows with nnz(A_i) + nnz(B_i) > 16384 return
+ * KK_ERR_UNSUPPORTED_TYPE.  Synchronises `stream`. */
 kk_status_t kk_spadd_symbolic(kk_spgemm_handle_t handle, const kk_csr_t* A, const kk_csr_t* B, void* c_row_map,
                               int64_t* c_nnz, void* stream);
 

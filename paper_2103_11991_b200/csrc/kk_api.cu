@@ -674,10 +674,6 @@ static kk_status_t numeric_impl(kk_spgemm_handle_t h, const kk_csr_t* A, const k
     cudaStream_t side = nullptr;
     const bool dense = h->host_num_bin_start[kk::NUM_DENSE_BIN + 1] > h->host_num_bin_start[kk::NUM_DENSE_BIN];
     if (dinv) {
-        if (dense)
-            return fail(h, KK_ERR_UNSUPPORTED_TYPE,
-                        "jacobi numeric: %d rows with nnz(C_i) > 512 need the dense tiers, which have no Jacobi form yet",
-                        h->host_num_bin_start[kk::NUM_DENSE_BIN + 1] - h->host_num_bin_start[kk::NUM_DENSE_BIN]);
         if (h->opts.validate) {
             int missing = 0;
             if ((st = ensure(h, h->diagchk, sizeof(int), s)) != KK_OK) return st;
@@ -994,7 +990,7 @@ kk_status_t kk_spadd_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
     if ((st = cuda_check(h, cudaGetLastError(), "kk_spadd_symbolic launch")) != KK_OK) return st;
     if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spadd_symbolic sync")) != KK_OK) return st;
     if (too_long)
-        return fail(h, KK_ERR_UNSUPPORTED_TYPE, "SpAdd: a row has nnz(A_i) + nnz(B_i) > 256 (warp sort limit)");
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE, "SpAdd: a row has nnz(A_i) + nnz(B_i) > 16384 (the CTA tier's shared-memory sort)");
     if (hs.overflow)
         return fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) = %llu exceeds int32 row offsets; use KK_I64",
                     (unsigned long long)hs.nnz_c);

@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
                                                              const OffT* __restrict__ crm, int32_t* __restrict__ cent,
                                                              ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                              const int* __restrict__ bin_start, int bin, int64_t k,
-                                                             int vcap, int big, int det) {
+                                                             int vcap, int big, int det,
+                                                             const ValT* __restrict__ dinv, double omega) {
     extern __shared__ __align__(16) uint32_t sm_hub[];
     const int64_t NW = hub_words(k);
     uint32_t* bm = sm_hub;
@@ -242,6 +243,42 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
             }
         }, det != 0);
         __syncthreads();
+        if (dinv) {
+            // Jacobi-fused row: C(i,:) = B(i,:) - omega D^-1(i) E(i,:): E(i,:)
+            // scaled once by the row's scalar, then B(i,:) added at its ranks (its columns lie
+            // in E's pattern when A(i,i) is stored; others are dropped)
+            const ValT sc = (ValT)(-omega * (double)__ldg(dinv + i));
+            if (inshared)
+                for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) svals[t] *= sc;
+            else
+                for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) cval[cb + t] *= sc;
+            __syncthreads();
+            const int64_t bs = ld(brm, i), be = ld(brm, i + 1);
+            for (int64_t q = bs + threadIdx.x; q < be; q += HUB_THREADS) {
+                const int c = __ldg(bent + q);
+                if (c < 0 || (int64_t)c >= k || !((bm[c >> 5] >> (c & 31)) & 1u)) continue;
+                const int w = c >> 5;
+                uint32_t rk = gp[w >> 2];
+                const int gw = w & ~3;
+                if (gw + 0 < w) rk += __popc(bm[gw + 0]);
+                if (gw + 1 < w) rk += __popc(bm[gw + 1]);
+                if (gw + 2 < w) rk += __popc(bm[gw + 2]);
+                rk += __popc(bm[w] & ((1u << (c & 31)) - 1u));
+                if ((int64_t)rk >= clen) continue;
+                const ValT b = __ldg(bval + q);
+                if (det) {  // strictly increasing B(i,:): distinct ranks
+                    if (inshared)
+                        svals[rk] += b;
+                    else
+                        cval[cb + rk] += b;
+                } else if (inshared) {
+                    atomicAdd(&svals[rk], b);
+                } else {
+                    atomicAdd(&cval[cb + rk], b);
+                }
+            }
+            __syncthreads();
+        }
         if (inshared) {
             for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) __stcs(cval + cb + t, svals[t]);
             __syncthreads();
@@ -535,7 +572,7 @@ static bool hub_bins_t(Launch& L, const NumArgs& a, cudaStream_t s) {
     // (b) the cluster tier for the longer rows: sorted B, slice bit vector + value window fit
     const size_t cfix = cl_fixed_smem(a.k);
     const int cvcap = cfix + 4096 * sizeof(ValT) <= SMEM_MAX ? (int)((SMEM_MAX - cfix) / sizeof(ValT)) - 64 : 0;
-    const bool cluster = use_cluster() && !a.det && a.sorted && a.work_ctr != nullptr && cvcap >= 4096;
+    const bool cluster = use_cluster() && !a.det && a.dinv == nullptr && a.sorted && a.work_ctr != nullptr && cvcap >= 4096;
     {
         auto kern = k_num_hub<OffT, ValT>;
         KCfg c = kernel_cfg(kern, HUB_THREADS, hsm_v, L.num_sms);
@@ -545,7 +582,7 @@ static bool hub_bins_t(Launch& L, const NumArgs& a, cudaStream_t s) {
                                               (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                               (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
                                               a.bin_start, NUM_DENSE_BIN, a.k, vcap, cluster ? 1 : 0,
-                                              a.det ? 1 : 0);
+                                              a.det ? 1 : 0, (const ValT*)a.dinv, a.omega);
         L.end(s);
     }
     if (cluster) {

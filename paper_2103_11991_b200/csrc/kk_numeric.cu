@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) k_num_dense(const OffT* __restrict__ arm,
                                                    ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                    const int* __restrict__ bin_start, int bin, int64_t k, int W,
                                                    int32_t* __restrict__ cursors, const DevStatus* __restrict__ st,
-                                                   int det) {
+                                                   int det, const ValT* __restrict__ dinv, double omega) {
     extern __shared__ __align__(16) unsigned char sm_dense[];
     ValT* win = (ValT*)sm_dense;
     uint32_t* bmp = (uint32_t*)(win + W);
@@ -197,6 +197,26 @@ __global__ void __launch_bounds__(256) k_num_dense(const OffT* __restrict__ arm,
                 }
             }
             __syncthreads();
+            if (dinv) {
+                // Jacobi-fused row: the window's E(i,:) values scaled by the
+                // row's scalar, then the entries of B(i,:) in the window added where E has an
+                // entry (A(i,i) stored; others dropped)
+                const ValT sc = (ValT)(-omega * (double)__ldg(dinv + i));
+                for (int t = threadIdx.x; t < (int)(hi - lo); t += blockDim.x) win[t] *= sc;
+                __syncthreads();
+                const int64_t bs = ld(brm, i), be = ld(brm, i + 1);
+                for (int64_t q = bs + threadIdx.x; q < be; q += blockDim.x) {
+                    const int64_t c = __ldg(bent + q);
+                    if (c < lo || c >= hi) continue;
+                    const int x = (int)(c - lo);
+                    if (!((bmp[x >> 5] >> (x & 31)) & 1u)) continue;
+                    if (det)
+                        win[x] += __ldg(bval + q);
+                    else
+                        atomicAdd(&win[x], __ldg(bval + q));
+                }
+                __syncthreads();
+            }
             // compaction in column order: warp w owns words [w0, w1)
             const int nw = (int)((hi - lo + 31) >> 5);
             const int w0 = (int)((int64_t)warp * nw / warps), w1 = (int)((int64_t)(warp + 1) * nw / warps);
@@ -545,7 +565,8 @@ static void numeric_bins_t(Launch& L, const NumArgs& a, cudaStream_t dense_strea
         kern<<<grid, threads, smem, s>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                          (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                          (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm, a.bin_start,
-                                         NUM_DENSE_BIN, a.k, (int)W, a.cursors, a.st, a.det ? 1 : 0);
+                                         NUM_DENSE_BIN, a.k, (int)W, a.cursors, a.st, a.det ? 1 : 0,
+                                         (const ValT*)a.dinv, a.omega);
         L.end(s);
     }
     launch_num_tiny<OffT, ValT>(L, a);

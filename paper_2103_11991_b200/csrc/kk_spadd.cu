@@ -16,7 +16,10 @@
 namespace kk {
 
 constexpr int SPADD_MAXE = 8;                   // keys per lane
-constexpr int SPADD_MAXROW = 32 * SPADD_MAXE;   // nnz(A_i) + nnz(B_i) limit
+constexpr int SPADD_MAXROW = 32 * SPADD_MAXE;   // nnz(A_i) + nnz(B_i) of the warp tier
+// longer rows: a CTA per row, keys sorted in shared memory (block bitonic sort)
+constexpr int SPADD_CTA_THREADS = 1024;
+constexpr int SPADD_LONG_MAX = 16384;           // nnz(A_i) + nnz(B_i) limit of the CTA tier
 
 // warp bitonic sort of 32*E 64-bit keys, E per lane (element e = lane*E + r)
 template <int E>
@@ -100,8 +103,7 @@ __global__ void __launch_bounds__(256) k_spadd_symbolic(int64_t m, const OffT* _
         const int n = na + nb;
         // rows are taken by the smallest E that holds them
         if (n > 32 * E || (E > 1 && n <= 16 * E)) {
-            if (E == SPADD_MAXE && n > 32 * E && lane == 0) atomicExch(too_long, 1);
-            continue;
+            continue;  // longer than the warp tier: k_spadd_symbolic_long
         }
         // A's keys ascending from position 0, B's from the end backwards, padding between:
         // with sorted rows this is a bitonic sequence and the merge alone sorts it
@@ -232,6 +234,138 @@ __global__ void __launch_bounds__(256) k_spadd_numeric(int64_t m, ValT alpha, co
     }
 }
 
+// Rows with SPADD_MAXROW < nnz(A_i) + nnz(B_i) <= SPADD_LONG_MAX: a CTA owns the row (Alg. 1,
+// PAPER.md:269-300, with the team sort as a block bitonic sort of 64-bit keys
+// col << 32 | matrix << 31 | index in shared memory); heads of equal-column runs, their
+// block-wide scan, Apos / Bpos and the count as in the warp tier.  Longer rows set too_long.
+template <typename OffT>
+__global__ void __launch_bounds__(SPADD_CTA_THREADS) k_spadd_symbolic_long(
+    int64_t m, const OffT* __restrict__ arm, const int32_t* __restrict__ aent, const OffT* __restrict__ brm,
+    const int32_t* __restrict__ bent, int32_t* __restrict__ counts, int32_t* __restrict__ apos,
+    int32_t* __restrict__ bpos, uint8_t* __restrict__ dup, int* __restrict__ too_long) {
+    extern __shared__ __align__(16) unsigned long long sk[];  // SPADD_LONG_MAX keys
+    __shared__ int wsum[SPADD_CTA_THREADS / 32];
+    __shared__ int sdup;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+        const int64_t sa = ld(arm, i), sb = ld(brm, i);
+        const int64_t na = ld(arm, i + 1) - sa, nb = ld(brm, i + 1) - sb;
+        const int64_t n = na + nb;
+        if (n <= SPADD_MAXROW) continue;
+        if (n > SPADD_LONG_MAX) {
+            if (tid == 0) atomicExch(too_long, 1);
+            continue;
+        }
+        int P = 1;
+        while (P < n) P <<= 1;
+        for (int e = tid; e < P; e += SPADD_CTA_THREADS) {
+            unsigned long long key = ~0ull;
+            if (e < na)
+                key = ((unsigned long long)(uint32_t)__ldg(aent + sa + e) << 32) | (unsigned long long)e;
+            else if (e < n)
+                key = ((unsigned long long)(uint32_t)__ldg(bent + sb + (e - na)) << 32) | (1ull << 31) |
+                      (unsigned long long)(e - na);
+            sk[e] = key;
+        }
+        if (tid == 0) sdup = 0;
+        __syncthreads();
+        for (int k = 2; k <= P; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int e = tid; e < P; e += SPADD_CTA_THREADS) {
+                    const int pr = e ^ j;
+                    if (pr > e) {
+                        const unsigned long long x = sk[e], y = sk[pr];
+                        const bool up = (e & k) == 0;
+                        if (up ? (x > y) : (x < y)) {
+                            sk[e] = y;
+                            sk[pr] = x;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // heads, their exclusive block scan (elements in contiguous chunks per thread)
+        const int per = (P + SPADD_CTA_THREADS - 1) / SPADD_CTA_THREADS;
+        const int e0 = tid * per, e1 = min(e0 + per, (int)n);
+        int cnt = 0;
+        bool dp = false;
+        for (int e = e0; e < e1; ++e) {
+            const unsigned long long v = sk[e];
+            const bool h = e == 0 || (sk[e - 1] >> 32) != (v >> 32);
+            dp |= e > 0 && (sk[e - 1] >> 31) == (v >> 31);
+            cnt += h;
+        }
+        int x = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(FULL, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        if (dp) sdup = 1;
+        __syncthreads();
+        int base = 0, total = 0;
+        for (int w = 0; w < SPADD_CTA_THREADS / 32; ++w) {
+            if (w < warp) base += wsum[w];
+            total += wsum[w];
+        }
+        int pos = base + x - cnt - 1;
+        for (int e = e0; e < e1; ++e) {
+            const unsigned long long v = sk[e];
+            pos += (e == 0 || (sk[e - 1] >> 32) != (v >> 32)) ? 1 : 0;
+            const int idx = (int)(v & 0x7fffffffull);
+            if (v & (1ull << 31))
+                bpos[sb + idx] = pos;
+            else
+                apos[sa + idx] = pos;
+        }
+        if (tid == 0) {
+            counts[i] = total;
+            dup[i] = sdup ? 1 : 0;
+        }
+        __syncthreads();
+    }
+}
+
+// Numeric for the CTA-tier rows: scatter straight into C's row in global memory (columns
+// stored, values zeroed, then alpha*a and beta*b added; fp64/fp32 reductions when the row
+// has unmerged input, plain adds otherwise -- A's positions, then B's, are distinct)
+template <typename OffT, typename ValT>
+__global__ void __launch_bounds__(256) k_spadd_numeric_long(
+    int64_t m, ValT alpha, const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+    const ValT* __restrict__ aval, ValT beta, const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
+    const ValT* __restrict__ bval, const OffT* __restrict__ crm, int32_t* __restrict__ cent, ValT* __restrict__ cval,
+    const int32_t* __restrict__ apos, const int32_t* __restrict__ bpos, const uint8_t* __restrict__ dup) {
+    for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+        const int64_t cb = ld(crm, i), cn = ld(crm, i + 1) - cb;
+        if (cn <= SPADD_MAXROW) continue;  // the warp tier's row
+        const int64_t sa = ld(arm, i), sb = ld(brm, i);
+        const int64_t na = ld(arm, i + 1) - sa, nb = ld(brm, i + 1) - sb;
+        if (na + nb > SPADD_LONG_MAX) continue;
+        const bool plain = dup[i] == 0;
+        for (int64_t t = threadIdx.x; t < cn; t += blockDim.x) cval[cb + t] = (ValT)0;
+        __syncthreads();
+        for (int side = 0; side < 2; ++side) {
+            const int64_t nn = side ? nb : na, s0 = side ? sb : sa;
+            const int32_t* en = side ? bent : aent;
+            const ValT* va = side ? bval : aval;
+            const int32_t* ps = side ? bpos : apos;
+            const ValT sc_ = side ? beta : alpha;
+            for (int64_t q = threadIdx.x; q < nn; q += blockDim.x) {
+                const int p = __ldg(ps + s0 + q);
+                cent[cb + p] = __ldg(en + s0 + q);
+                const ValT w = sc_ * __ldg(va + s0 + q);
+                if (plain)
+                    cval[cb + p] += w;
+                else
+                    atomicAdd(&cval[cb + p], w);
+            }
+            __syncthreads();
+        }
+    }
+}
+
 template <typename OffT>
 static void spadd_symbolic_t(Launch& L, int64_t m, const MatView& A, const MatView& B, int32_t* counts,
                              int32_t* apos, int32_t* bpos, uint8_t* dup, int* too_long) {
@@ -246,7 +380,14 @@ static void spadd_symbolic_t(Launch& L, int64_t m, const MatView& A, const MatVi
                                                               B.entries, counts, apos, bpos, dup, too_long);
     k_spadd_symbolic<OffT, 8><<<grid, threads, 0, L.stream>>>(m, (const OffT*)A.row_map, A.entries, (const OffT*)B.row_map,
                                                               B.entries, counts, apos, bpos, dup, too_long);
-    L.end(L.stream, 4);
+    {
+        const size_t smem = (size_t)SPADD_LONG_MAX * 8;
+        auto kern = k_spadd_symbolic_long<OffT>;
+        KCfg c = kernel_cfg(kern, SPADD_CTA_THREADS, smem, L.num_sms);
+        kern<<<std::min<int64_t>(m, c.grid_cap), SPADD_CTA_THREADS, smem, L.stream>>>(
+            m, (const OffT*)A.row_map, A.entries, (const OffT*)B.row_map, B.entries, counts, apos, bpos, dup, too_long);
+    }
+    L.end(L.stream, 5);
 }
 
 void spadd_symbolic(Launch& L, bool off64, int64_t m, const MatView& A, const MatView& B, int32_t* counts,
@@ -268,7 +409,10 @@ static void spadd_numeric_t(Launch& L, int64_t m, double alpha, const MatView& A
     k_spadd_numeric<OffT, ValT><<<grid, threads, 0, L.stream>>>(
         m, (ValT)alpha, (const OffT*)A.row_map, A.entries, (const ValT*)A.values, (ValT)beta, (const OffT*)B.row_map,
         B.entries, (const ValT*)B.values, (const OffT*)crm, cent, (ValT*)cval, apos, bpos, dup);
-    L.end(L.stream);
+    k_spadd_numeric_long<OffT, ValT><<<(int)std::min<int64_t>(m, (int64_t)L.num_sms * 8), 256, 0, L.stream>>>(
+        m, (ValT)alpha, (const OffT*)A.row_map, A.entries, (const ValT*)A.values, (ValT)beta, (const OffT*)B.row_map,
+        B.entries, (const ValT*)B.values, (const OffT*)crm, cent, (ValT*)cval, apos, bpos, dup);
+    L.end(L.stream, 2);
 }
 
 void spadd_numeric(Launch& L, bool off64, bool f64, int64_t m, double alpha, const MatView& A, double beta,

@@ -110,3 +110,17 @@ def test_jacobi_errors():
     with pytest.raises(KKError, match="A\\(i,i\\)"):
         h.jacobi(0.5, torch.ones(30, dtype=torch.float64, device="cuda"), A, B)
     h.close()
+
+
+@pytest.mark.parametrize("k", [200000, 20000])
+@pytest.mark.parametrize("det", [False, True])
+def test_jacobi_long_rows(oracle_mod, k, det):
+    """Rows with nnz(C_i) > 512: the fused form in the long-row tiers -- the CTA bit-vector
+    tier (k = 200K, values in shared memory or, above its capacity, at L2) and the windowed
+    dense tier (k = 20K); deterministic mode too."""
+    m = 300
+    A = _square_with_diag(m, 60, 7)
+    B = g.random_csr(m, k, 300, seed=8, empty_row_frac=0.0)
+    dinv = 1.0 / (2.0 + np.arange(m) % 7)
+    got = _run(A, B, dinv, 2.0 / 3.0, deterministic=det)
+    _check(oracle_mod, A, B, dinv, 2.0 / 3.0, got)

@@ -68,7 +68,18 @@ def test_spadd_symbolic_reuse_and_errors(oracle_mod):
         _check(oracle_mod, al, A, be, B, (rm.cpu().numpy().astype(np.int64), ent.cpu().numpy(), val.cpu().numpy()))
     with pytest.raises(KKError):  # shape mismatch
         h.spadd_symbolic(Ad, to_device(g.random_csr(200, 151, 3, seed=7), "cuda"))
-    with pytest.raises(KKError):  # a row over the 256-key sort limit
-        L = to_device(g.random_csr(10, 1000, 200, seed=8, empty_row_frac=0.0), "cuda")
+    with pytest.raises(KKError):  # a row over the CTA tier's 16,384-key sort
+        L = to_device(g.random_csr(3, 40000, 9000, seed=8, empty_row_frac=0.0), "cuda")
         h.spadd_symbolic(L, L)
     h.close()
+
+
+@pytest.mark.parametrize("kw", [{}, dict(sorted_rows=False), dict(sorted_rows=False, duplicates=True)])
+@pytest.mark.parametrize("vt", [torch.float64, torch.float32])
+def test_spadd_long_rows(oracle_mod, kw, vt):
+    """Rows with nnz(A_i) + nnz(B_i) > 256 (the CTA tier: shared-memory bitonic sort), mixed
+    with short rows (warp tier), sorted, unsorted and unmerged."""
+    A = g.random_csr(60, 30000, 3000, seed=61, **kw)
+    B = g.random_csr(60, 30000, 5000, seed=62, **kw)
+    got = _run(0.75, A, -1.5, B, vt=vt)
+    _check(oracle_mod, 0.75, A, -1.5, B, got, vt=vt)
