@@ -69,7 +69,10 @@ def test_spadd_symbolic_reuse_and_errors(oracle_mod):
     with pytest.raises(KKError):  # shape mismatch
         h.spadd_symbolic(Ad, to_device(g.random_csr(200, 151, 3, seed=7), "cuda"))
     with pytest.raises(KKError):  # a row over the CTA tier's 16,384-key sort
-        L = to_device(g.random_csr(3, 40000, 9000, seed=8, empty_row_frac=0.0), "cuda")
+        n = 9000  # one row of 9,000 entries: A + A has 18,000 keys
+        row = g.CSR(1, 40000, torch.tensor([0, n]), torch.arange(0, 4 * n, 4, dtype=torch.int32),
+                    torch.ones(n, dtype=torch.float64))
+        L = to_device(row, "cuda")
         h.spadd_symbolic(L, L)
     h.close()
 
