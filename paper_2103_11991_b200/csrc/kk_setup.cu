@@ -137,8 +137,18 @@ __global__ void __launch_bounds__(256) k_check_compress(int64_t n, int64_t k, co
             } else {
                 int prev = INT_MIN, cw = -1, outn = 0;
                 unsigned cm = 0;
+                // entries in batches of 8 loaded ahead: the walk is bound by load latency
+                // otherwise (ncu: 86 % long-scoreboard stalls)
+                int cb8[8];
                 for (int64_t q = s; q < e; ++q) {
-                    const int col = __ldg(bent + q);
+                    if (((q - s) & 7) == 0) {
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) cb8[u] = q + u < e ? __ldg(bent + q + u) : 0;
+                    }
+                    int col = cb8[0];
+#pragma unroll
+                    for (int u = 1; u < 8; ++u)
+                        if (((q - s) & 7) == u) col = cb8[u];
                     fl.unsorted |= col < prev;
                     fl.nonstrict |= col <= prev;
                     fl.bad |= (col < 0) || ((int64_t)col >= k);
@@ -298,7 +308,17 @@ __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t
             if (e - s > LANE_ROW_MAX) {
                 long_row = true;
             } else {
-                for (int64_t p = s; p < e; ++p) flop_entry(__ldg(aent + p), n, validate, brm, bc_len, bmeta, comp, acc);
+                // 4 A entries (and their B-row records) in flight per lane: the walk is
+                // bound by load latency otherwise (ncu: 72 % long-scoreboard stalls)
+                int64_t p = s;
+                for (; p + 4 <= e; p += 4) {
+                    int jj[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) jj[u] = __ldg(aent + p + u);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) flop_entry(jj[u], n, validate, brm, bc_len, bmeta, comp, acc);
+                }
+                for (; p < e; ++p) flop_entry(__ldg(aent + p), n, validate, brm, bc_len, bmeta, comp, acc);
             }
         }
         unsigned lr = __ballot_sync(FULL, long_row);
