@@ -28,7 +28,7 @@ namespace cg = cooperative_groups;
 // then written out coalesced.  Rows above vcap: skipped when the cluster tier takes them
 // (big = 1), else added into C's values in global memory (fp64/fp32 reduction at L2).
 // ------------------------------------------------------------------------------------
-constexpr int HUB_THREADS = 512;
+constexpr int HUB_THREADS = 1024;
 constexpr int HUB_WARPS = HUB_THREADS / 32;
 
 __host__ __device__ constexpr int64_t hub_words(int64_t k) { return ((k + 127) / 128) * 4; }  // multiple of 4
