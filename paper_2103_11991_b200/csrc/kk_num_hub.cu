@@ -124,7 +124,7 @@ __device__ __forceinline__ void hub_walk(int64_t s, int64_t e, const int32_t* __
             const int64_t tb = __shfl_sync(FULL, bs, t);
             const int64_t tl = __shfl_sync(FULL, bl, t);
             const ValT ta = __shfl_sync(FULL, a, t);
-            hub_segment<4, VALS>(bent, bval, tb, tl, lane, 32, ta, f);
+            hub_segment<8, VALS>(bent, bval, tb, tl, lane, 32, ta, f);
         }
     }
     __syncthreads();
