@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) k_sym_warp(const OffT* __restrict__ arm, 
 // accumulator in one CTA's shared memory, over windows of `wbits`
 // columns when k is larger.  Sorted B rows are resumed from per-entry cursors.
 template <typename OffT>
-__global__ void __launch_bounds__(512) k_sym_dense(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
+__global__ void __launch_bounds__(1024) k_sym_dense(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                    const OffT* __restrict__ brm, const int32_t* __restrict__ bent,
                                                    const int32_t* __restrict__ bc_len,
                                                    const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
@@ -108,7 +108,59 @@ __global__ void __launch_bounds__(512) k_sym_dense(const OffT* __restrict__ arm,
             const int64_t low = lo >> 5, hiw = (hi + 31) >> 5;
             if (threadIdx.x == 0) *nlist = 0;
             __syncthreads();
-            for (int64_t p = s + warp; p < e; p += warps) {
+            if (single) {
+                // one window over all of k: batches of 32 A entries per warp (one load chain per
+                // batch), their B(_C) rows walked with 8 entries per lane in flight; long rows to
+                // the CTA list (the walk is bound by load latency otherwise)
+                for (int64_t p0 = s + (int64_t)warp * 32; p0 < e; p0 += (int64_t)warps * 32) {
+                    const int64_t p = p0 + lane;
+                    int64_t bs = 0, len = 0;
+                    if (p < e) {
+                        const int j = __ldg(aent + p);
+                        bs = ld(brm, j);
+                        len = comp ? __ldg(bc_len + j) : ld(brm, j + 1) - bs;
+                    }
+                    const bool lng = len > LONG;
+                    const unsigned lb = __ballot_sync(FULL, lng);
+                    bool listed = false;
+                    if (lb) {
+                        int base = 0;
+                        if (lane == 0) base = atomicAdd(nlist, __popc(lb));
+                        base = __shfl_sync(FULL, base, 0);
+                        const int slot = base + __popc(lb & lanemask_lt());
+                        if (lng && slot < LIST) {
+                            list[slot] = (int)(p - s);
+                            listed = true;
+                        }
+                    }
+                    const unsigned skip = __ballot_sync(FULL, listed);
+                    const int n = (int)min((int64_t)32, e - p0);
+                    for (int t = 0; t < n; ++t) {
+                        if ((skip >> t) & 1u) continue;
+                        const int64_t tb = __shfl_sync(FULL, bs, t);
+                        const int64_t tl = __shfl_sync(FULL, len, t);
+                        for (int64_t x0 = lane; x0 < tl; x0 += 32 * 8) {
+                            if (comp) {
+                                uint2 pr[8];
+#pragma unroll
+                                for (int u = 0; u < 8; ++u)
+                                    pr[u] = x0 + 32 * u < tl ? __ldg(pairs + tb + x0 + 32 * u) : make_uint2(0u, 0u);
+#pragma unroll
+                                for (int u = 0; u < 8; ++u)
+                                    if (pr[u].y) atomicOr(&bmp[pr[u].x], pr[u].y);
+                            } else {
+                                int c[8];
+#pragma unroll
+                                for (int u = 0; u < 8; ++u) c[u] = x0 + 32 * u < tl ? __ldg(bent + tb + x0 + 32 * u) : -1;
+#pragma unroll
+                                for (int u = 0; u < 8; ++u)
+                                    if (c[u] >= 0) atomicOr(&bmp[c[u] >> 5], 1u << (c[u] & 31));
+                            }
+                        }
+                    }
+                }
+            }
+            for (int64_t p = s + warp; p < e && !single; p += warps) {
                 const int j = __ldg(aent + p);
                 const int64_t bs = ld(brm, j);
                 if (single) {
@@ -1280,7 +1332,7 @@ static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stre
     // dense rows first (heaviest), on their own stream when given
     const int64_t hdense = host_rows(a, SYM_DENSE_BIN);
     if (hdense != 0) {
-        const int threads = 512;
+        const int threads = 1024;
         int64_t wbits = 200 * 1024 * 8;  // 200 KB bit vector
         const int64_t k32 = ((a.k + 31) / 32) * 32;
         if (k32 < wbits) wbits = k32 > 0 ? k32 : 32;
