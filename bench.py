@@ -47,6 +47,7 @@ WORKLOADS = {
     "C4": "A*A RMAT scale 20, edge factor 16, directed (1,048,576 rows)",
     "C5": "A*A 3D 27-point block stencil, 3 dof/node, 160^3 (12,288,000 rows)",
     "C3J": "Jacobi-fused (I - w D^-1 A) P: 3D 7-point Laplacian 128^3, 3x3x3 aggregation P, w = 2/3 (NEXT-1)",
+    "C3F": "fused Galerkin R*A*P in one pass (NEXT-4): 3D 7-point Laplacian 128^3, 3x3x3 aggregation P, R = P^T",
 }
 
 
@@ -85,7 +86,7 @@ def make_workload(cfg, size, values, device):
     """(A, B) for the A*B configs; (A, P, R) for C3."""
     from workloads import generators as g
 
-    return g.config(cfg, size=size, values=values, device=device)
+    return g.config("C3" if cfg == "C3F" else cfg, size=size, values=values, device=device)
 
 
 def nbytes(t):
@@ -372,8 +373,8 @@ def run_ours(args):
         A, B = mats[0], mats[1]
         r0, r1 = 0, A.nrows
     else:
-        if args.config == "C3J":
-            raise SystemExit("C3J is benchmarked on one GPU")
+        if args.config in ("C3J", "C3F"):
+            raise SystemExit(f"{args.config} is benchmarked on one GPU")
         from paper_2103_11991_b200.parallel import (broadcast_csr, flop_balanced_cuts, galerkin_slab_cuts,
                                                     halo_exchange_b, shift_columns, slice_rows)
 
@@ -461,8 +462,33 @@ def run_ours(args):
         def C(self):
             return CsrMatrix(self.X.nrows, self.Y.ncols, self.crm, self.cent[:self.nnz], self.cval[:self.nnz])
 
+    class RapProduct:
+        """The fused triple product Ac = R*A*P of C3F (one symbolic + one numeric call)."""
+
+        def __init__(self, R, A_, P):
+            self.R, self.A, self.P = R, A_, P
+            self.X, self.Y, self.jacobi, self.rap = R, P, None, True
+            self.h = SpGEMM(device=dev, timing=True, num_streams=args.streams)
+            self.crm = torch.empty(R.nrows + 1, dtype=odt, device=dev)
+            _, n = self.h.rap_symbolic(R, A_, P, c_row_map=self.crm)
+            self.cent = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+            self.cval = torch.empty(max(n, 1), dtype=vdt, device=dev)
+            self.nnz = n
+            # the work of the product it replaces (T = A*P, Ac = R*T), for a comparable GFLOP/s
+            h2 = SpGEMM(device=dev)
+            T = h2(A_, P)
+            self.muladds = h2.stats()["muladds"]
+            h3 = SpGEMM(device=dev)
+            h3.symbolic(R, T)
+            self.muladds += h3.stats()["muladds"]
+            h2.close()
+            h3.close()
+
     # the step's products: A*B, or for C3 T = A*P then Ac = R*T (T stays in HBM)
-    prods = [Product(A, B, jac)]
+    if args.config == "C3F":
+        prods = [RapProduct(mats[2], A, B)]
+    else:
+        prods = [Product(A, B, jac)]
     if world > 1 and vwork is not None:
         vwork.wait()  # B's values (in flight during the row split and the first symbolic phase)
         torch.cuda.synchronize()
@@ -476,6 +502,12 @@ def run_ours(args):
         for k, pr in enumerate(prods):
             if ev is not None:
                 ev[2 * k].record(stream)
+            if getattr(pr, "rap", False):
+                _, n = pr.h.rap_symbolic(pr.R, pr.A, pr.P, c_row_map=pr.crm)
+                if ev is not None:
+                    ev[2 * k + 1].record(stream)
+                pr.h.rap_numeric(pr.R, pr.A, pr.P, pr.crm, n, c_entries=pr.cent[:n], c_values=pr.cval[:n])
+                continue
             _, n = pr.h.symbolic(pr.X, pr.Y, c_row_map=pr.crm)
             if world > 1:
                 # nnz(C_p) straight from the row map the scan kernel wrote (no host tensor)
@@ -496,6 +528,9 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     sts = [pr.h.stats() for pr in prods]
+    for pr, st in zip(prods, sts):
+        if getattr(pr, "rap", False):  # the fused product reports the work of R*(A*P)
+            st["muladds"], st["nnz_c"] = pr.muladds, pr.nnz
     muladds = sum(st["muladds"] for st in sts)
     nnz = sts[-1]["nnz_c"]
     for pr in prods:
@@ -549,6 +584,11 @@ def run_ours(args):
     sym_b = num_b = 0
     for pr, st in zip(prods, sts):
         sb, nb = alg_bytes(pr.X, pr.Y, pr.crm, st["nnz_c"], val_size)
+        if getattr(pr, "rap", False):  # + A, read by both phases
+            off = pr.crm.element_size()
+            a_pat = (pr.A.nrows + 1) * off + pr.A.nnz * 4
+            sb += a_pat
+            nb += a_pat + pr.A.nnz * val_size
         sym_b += sb
         num_b += nb
     if dist is not None:
@@ -589,8 +629,9 @@ def run_ours(args):
         nnz * (4 + val_size) + (prods[-1].X.nrows + 1) * 8
     if args.no_e2e:
         e2e = None
-    elif jac is not None:
-        e2e = {"value": None, "unit": UNIT, "skipped": "C3J: the host-buffer path covers the plain product only"}
+    elif jac is not None or args.config == "C3F":
+        e2e = {"value": None, "unit": UNIT,
+               "skipped": f"{args.config}: the host-buffer path covers the plain product only"}
     elif host_bytes > 48e9:
         e2e = {"value": None, "unit": UNIT, "skipped": f"inputs + C = {host_bytes / 1e9:.0f} GB of pinned host memory"}
     else:
@@ -653,6 +694,8 @@ def run_ours(args):
             cpu["sample"] = "first product T = A*P only: " + cpu["sample"]
         if args.config == "C3J":
             cpu["sample"] = "plain E = A*P (the oracle's usual product): " + cpu["sample"]
+        if args.config == "C3F":
+            cpu["sample"] = "first product T = A*P only: " + cpu["sample"]
 
     if rank == 0:
         out = {"metric": METRIC, "value": round(gflops, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,

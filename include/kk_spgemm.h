@@ -199,6 +199,22 @@ kk_status_t kk_spadd_numeric(kk_spgemm_handle_t handle, double alpha, const kk_c
                              const kk_csr_t* B, const void* c_row_map, int32_t* c_entries, void* c_values,
                              void* stream);
 
+/* Fused Galerkin triple product Ac = R * A * P (multigrid coarse operator, the SpGEMM use the
+ * paper motivates at PAPER.md:152, 200), in one pass without forming A*P:
+ * Ac(I,c) = sum_{i in R(I,:)} R(I,i) sum_{j in A(i,:)} A(i,j) P(j,c).  R: mc x m, A: m x n,
+ * P: n x nc (else KK_ERR_DIM_MISMATCH), device CSR of one offset type and one value type.
+ * kk_spgemm_rap_symbolic fills c_row_map (device, mc+1 of R.offset_type, caller-allocated)
+ * and returns nnz(Ac) in *c_nnz (host; synchronises `stream`); rows of Ac with more than 256
+ * distinct columns return KK_ERR_UNSUPPORTED_TYPE (compute them as two products).
+ * kk_spgemm_rap_numeric writes Ac's sorted column indices and values (device, caller-
+ * allocated, nnz(Ac)) for the matrices and row map of the last rap symbolic on this handle
+ * (else KK_ERR_STALE_HANDLE); values of R, A, P may change between calls.  Asynchronous. */
+kk_status_t kk_spgemm_rap_symbolic(kk_spgemm_handle_t handle, const kk_csr_t* R, const kk_csr_t* A,
+                                   const kk_csr_t* P, void* c_row_map, int64_t* c_nnz, void* stream);
+kk_status_t kk_spgemm_rap_numeric(kk_spgemm_handle_t handle, const kk_csr_t* R, const kk_csr_t* A,
+                                  const kk_csr_t* P, const void* c_row_map, int32_t* c_entries, void* c_values,
+                                  void* stream);
+
 /* C = A*B with A, B and C in HOST memory: the paper's protocol run end to
  * end over host buffers.  A, B: CSR whose row_map / entries / values are HOST pointers
  * (pinned memory, e.g. cudaHostAlloc, lets the copies run asynchronously; pageable memory

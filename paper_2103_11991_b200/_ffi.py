@@ -87,11 +87,14 @@ def load() -> ctypes.CDLL:
         lib.kk_spgemm_stats.argtypes = [H, P(kk_spgemm_stats_t)]
         lib.kk_spgemm_multiply_host.argtypes = [H, P(kk_csr_t), P(kk_csr_t), _vp, P(_i64),
                                                 P(ctypes.POINTER(ctypes.c_int32)), P(_vp), ctypes.c_int, _vp]
+        lib.kk_spgemm_rap_symbolic.argtypes = [H, P(kk_csr_t), P(kk_csr_t), P(kk_csr_t), _vp, P(_i64), _vp]
+        lib.kk_spgemm_rap_numeric.argtypes = [H, P(kk_csr_t), P(kk_csr_t), P(kk_csr_t), _vp, _vp, _vp, _vp]
         lib.kk_spgemm_kernel_times.argtypes = [H, P(kk_kernel_time_t), P(ctypes.c_int)]
         lib.kk_spgemm_timing_reset.argtypes = [H]
         for fn in ("kk_spgemm_create", "kk_spgemm_destroy", "kk_spgemm_row_flops", "kk_spgemm_compress",
                    "kk_spgemm_symbolic", "kk_spgemm_numeric", "kk_spgemm_jacobi_numeric", "kk_spgemm_stats",
                    "kk_spadd_symbolic", "kk_spadd_numeric", "kk_spgemm_multiply_host",
+                   "kk_spgemm_rap_symbolic", "kk_spgemm_rap_numeric",
                    "kk_spgemm_kernel_times",
                    "kk_spgemm_timing_reset"):
             getattr(lib, fn).restype = ctypes.c_int
@@ -203,6 +206,20 @@ def kk_spgemm_multiply_host(h, A: kk_csr_t, B: kk_csr_t, c_row_map_ptr: int, blo
                                              ctypes.byref(nnz), ctypes.byref(ent), ctypes.byref(val), int(blocks),
                                              stream or None))
     return int(nnz.value), ctypes.cast(ent, _vp).value or 0, val.value or 0
+
+
+def kk_spgemm_rap_symbolic(h, R: kk_csr_t, A: kk_csr_t, P: kk_csr_t, c_row_map_ptr: int, stream: int) -> int:
+    nnz = _i64(0)
+    _check(h, load().kk_spgemm_rap_symbolic(h, ctypes.byref(R), ctypes.byref(A), ctypes.byref(P),
+                                            c_row_map_ptr or None, ctypes.byref(nnz), stream or None))
+    return int(nnz.value)
+
+
+def kk_spgemm_rap_numeric(h, R: kk_csr_t, A: kk_csr_t, P: kk_csr_t, c_row_map_ptr: int, c_entries_ptr: int,
+                          c_values_ptr: int, stream: int) -> None:
+    _check(h, load().kk_spgemm_rap_numeric(h, ctypes.byref(R), ctypes.byref(A), ctypes.byref(P),
+                                           c_row_map_ptr or None, c_entries_ptr or None, c_values_ptr or None,
+                                           stream or None))
 
 
 def kk_spgemm_kernel_times(h) -> list:

@@ -123,6 +123,13 @@ struct kk_spgemm_handle_s {
         const void *arm = nullptr, *aent = nullptr, *brm = nullptr, *bent = nullptr, *crm = nullptr;
         int offt = 0;
     } rec;
+    // record of the last fused triple-product symbolic
+    struct RapRec {
+        bool valid = false;
+        int64_t mc = 0, nnzR = 0, nnzA = 0, nnzP = 0, nnzC = 0;
+        const void *rrm = nullptr, *arm = nullptr, *prm = nullptr, *crm = nullptr;
+        int offt = 0;
+    } raprec;
     // record of the last SpAdd symbolic
     struct AddRec {
         bool valid = false;
@@ -938,6 +945,87 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
     *c_entries = (int32_t*)P.h_cent;
     *c_values = P.h_cval;
     return KK_OK;
+}
+
+// ---- fused triple product Ac = R*A*P (NEXT-4) ----------------------
+static kk_status_t check_triple(kk_spgemm_handle_t h, const kk_csr_t* R, const kk_csr_t* A, const kk_csr_t* P,
+                                bool need_values) {
+    kk_status_t s;
+    if ((s = check_pair(h, R, A, need_values)) != KK_OK) return s;
+    if ((s = check_pair(h, A, P, need_values)) != KK_OK) return s;
+    return KK_OK;
+}
+
+extern "C" kk_status_t kk_spgemm_rap_symbolic(kk_spgemm_handle_t h, const kk_csr_t* R, const kk_csr_t* A,
+                                             const kk_csr_t* P, void* c_row_map, int64_t* c_nnz, void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    NvtxRange nvtx_("kk_spgemm_rap_symbolic");
+    h->raprec.valid = false;
+    kk_status_t st;
+    if ((st = check_triple(h, R, A, P, false)) != KK_OK) return st;
+    if (!c_row_map || !c_nnz) return fail(h, KK_ERR_INVALID_ARG, "c_row_map / c_nnz is NULL");
+    cudaSetDevice(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t mc = R->nrows;
+    const bool off64 = R->offset_type == KK_I64;
+    if ((st = ensure(h, h->status_aux, sizeof(DevStatus), s)) != KK_OK) return st;
+    if ((st = ensure(h, h->counts, (size_t)mc * 4, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->partial, (size_t)kk::scan_partial_len(mc) * 8, s)) != KK_OK) return st;
+    if ((st = ensure(h, h->spflag, sizeof(int), s)) != KK_OK) return st;
+    DevStatus* dst = (DevStatus*)h->status_aux.p;
+    kk::Launch L = make_launch(h, s);
+    kk::init_status(L, dst);
+    cudaMemsetAsync(h->spflag.p, 0, sizeof(int), s);
+    kk::rap_symbolic(L, off64, view(R), view(A), view(P), (int32_t*)h->counts.p, (int*)h->spflag.p);
+    kk::exclusive_scan(L, false, h->counts.p, off64, c_row_map, mc, (int64_t*)h->partial.p, &dst->nnz_c,
+                       &dst->overflow);
+    DevStatus hs;
+    int too_many = 0;
+    cudaMemcpyAsync(&hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&too_many, h->spflag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_rap_symbolic launch")) != KK_OK) return st;
+    if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_rap_symbolic sync")) != KK_OK) return st;
+    if (too_many)
+        return fail(h, KK_ERR_UNSUPPORTED_TYPE,
+                    "fused R*A*P: a coarse row has more than 256 distinct columns (use two products)");
+    if (hs.overflow)
+        return fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(Ac) = %llu exceeds int32 row offsets; use KK_I64",
+                    (unsigned long long)hs.nnz_c);
+    *c_nnz = (int64_t)hs.nnz_c;
+    auto& Q = h->raprec;
+    Q.valid = true;
+    Q.mc = mc;
+    Q.nnzR = R->nnz;
+    Q.nnzA = A->nnz;
+    Q.nnzP = P->nnz;
+    Q.nnzC = (int64_t)hs.nnz_c;
+    Q.rrm = R->row_map;
+    Q.arm = A->row_map;
+    Q.prm = P->row_map;
+    Q.crm = c_row_map;
+    Q.offt = (int)R->offset_type;
+    return KK_OK;
+}
+
+extern "C" kk_status_t kk_spgemm_rap_numeric(kk_spgemm_handle_t h, const kk_csr_t* R, const kk_csr_t* A,
+                                            const kk_csr_t* P, const void* c_row_map, int32_t* c_entries,
+                                            void* c_values, void* stream) {
+    if (!h) return KK_ERR_INVALID_ARG;
+    NvtxRange nvtx_("kk_spgemm_rap_numeric");
+    kk_status_t st;
+    if ((st = check_triple(h, R, A, P, true)) != KK_OK) return st;
+    const auto& Q = h->raprec;
+    if (!Q.valid || Q.mc != R->nrows || Q.nnzR != R->nnz || Q.nnzA != A->nnz || Q.nnzP != P->nnz ||
+        Q.rrm != R->row_map || Q.arm != A->row_map || Q.prm != P->row_map || Q.crm != c_row_map ||
+        Q.offt != (int)R->offset_type)
+        return fail(h, KK_ERR_STALE_HANDLE, "rap numeric: no matching rap symbolic for these matrices / row map");
+    if (Q.nnzC > 0 && (!c_entries || !c_values)) return fail(h, KK_ERR_INVALID_ARG, "c_entries/c_values is NULL");
+    cudaSetDevice(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    kk::Launch L = make_launch(h, s);
+    kk::rap_numeric(L, R->offset_type == KK_I64, R->value_type == KK_F64, view(R), view(A), view(P), c_row_map,
+                    c_entries, c_values);
+    return cuda_check(h, cudaGetLastError(), "kk_spgemm_rap_numeric launch");
 }
 
 // ---- SpAdd (Sec. 2.3) -------------------------------------------------

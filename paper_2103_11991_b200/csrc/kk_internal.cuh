@@ -175,6 +175,12 @@ void spadd_symbolic(Launch& L, bool off64, int64_t m, const MatView& A, const Ma
 void spadd_numeric(Launch& L, bool off64, bool f64, int64_t m, double alpha, const MatView& A, double beta,
                    const MatView& B, const void* crm, int32_t* cent, void* cval, const int32_t* apos,
                    const int32_t* bpos, const uint8_t* dup);
+// Fused triple product Ac = R*A*P (kk_rap.cu): symbolic fills counts[R.nrows] and sets
+// *too_many (device) when a coarse row has more distinct columns than the warp table holds
+void rap_symbolic(Launch& L, bool off64, const MatView& R, const MatView& A, const MatView& P, int32_t* counts,
+                  int* too_many);
+void rap_numeric(Launch& L, bool off64, bool f64, const MatView& R, const MatView& A, const MatView& P,
+                 const void* crm, int32_t* cent, void* cval);
 // validate for the Jacobi-fused numeric: *missing (host) = rows of the square A without a
 // stored diagonal entry; scratch: one device int.  Synchronises L.stream.  false on a CUDA error.
 bool check_diagonal(Launch& L, bool off64, int64_t m, const void* row_map, const int32_t* entries, int* scratch,

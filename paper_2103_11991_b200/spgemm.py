@@ -193,6 +193,36 @@ class SpGEMM:
         ent, val = self.numeric(A, B, rm, nnz=nnz, stream=stream)
         return CsrMatrix(A.nrows, B.ncols, rm, ent, val)
 
+    # -- fused Galerkin triple product (NEXT-4) --------------------------------------------
+    def rap_symbolic(self, R, A, P, c_row_map: Optional[torch.Tensor] = None, stream=None):
+        """Row map and nnz of Ac = R*A*P (one pass, A*P never formed)."""
+        R, A, P = (CsrMatrix.from_any(M) for M in (R, A, P))
+        if c_row_map is None:
+            c_row_map = torch.empty(R.nrows + 1, dtype=R.row_map.dtype, device=R.row_map.device)
+        nnz = _ffi.kk_spgemm_rap_symbolic(self._h, _kk_csr(R, False), _kk_csr(A, False), _kk_csr(P, False),
+                                          c_row_map.data_ptr(), _stream_ptr(self.device, stream))
+        return c_row_map, nnz
+
+    def rap_numeric(self, R, A, P, c_row_map: torch.Tensor, nnz: int, c_entries: Optional[torch.Tensor] = None,
+                    c_values: Optional[torch.Tensor] = None, stream=None):
+        R, A, P = (CsrMatrix.from_any(M) for M in (R, A, P))
+        dev = R.row_map.device
+        if c_entries is None:
+            c_entries = torch.empty(nnz, dtype=torch.int32, device=dev)
+        if c_values is None:
+            c_values = torch.empty(nnz, dtype=R.values.dtype, device=dev)
+        _ffi.kk_spgemm_rap_numeric(self._h, _kk_csr(R, True), _kk_csr(A, True), _kk_csr(P, True),
+                                   c_row_map.data_ptr(), c_entries.data_ptr() if nnz else 0,
+                                   c_values.data_ptr() if nnz else 0, _stream_ptr(self.device, stream))
+        return c_entries, c_values
+
+    def rap(self, R, A, P, stream=None) -> CsrMatrix:
+        """Ac = R*A*P, fused (kk_spgemm_rap_symbolic + kk_spgemm_rap_numeric)."""
+        rm, nnz = self.rap_symbolic(R, A, P, stream=stream)
+        ent, val = self.rap_numeric(R, A, P, rm, nnz, stream=stream)
+        R = CsrMatrix.from_any(R)
+        return CsrMatrix(R.nrows, CsrMatrix.from_any(P).ncols, rm, ent, val)
+
     # -- end to end from host memory ------------------------------------------------------
     def multiply_host(self, A, B, stream=None, blocks: Optional[int] = None) -> "CsrMatrix":
         """C = A*B for CSR operands in (pinned) HOST memory, C returned in HOST memory, through
