@@ -12,6 +12,8 @@
 // reported and the call fails (the two-product path handles them).
 #include "kk_device.cuh"
 
+#include <type_traits>
+
 namespace kk {
 
 constexpr int RAP_S = 512;    // table slots per warp
@@ -40,7 +42,7 @@ __device__ __forceinline__ uint32_t rap_claim(uint32_t* keys, uint32_t key, bool
 }
 
 template <typename OffT, typename ValT, bool NUMERIC>
-__global__ void __launch_bounds__(RAP_WARPS * 32) k_rap(int64_t mc, const OffT* __restrict__ rrm,
+__global__ void __launch_bounds__(RAP_WARPS * 32, 8) k_rap(int64_t mc, const OffT* __restrict__ rrm,
                                                       const int32_t* __restrict__ rent, const ValT* __restrict__ rval,
                                                       const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                       const ValT* __restrict__ aval, const OffT* __restrict__ prm,
@@ -66,6 +68,24 @@ __global__ void __launch_bounds__(RAP_WARPS * 32) k_rap(int64_t mc, const OffT* 
         const int64_t rs = ld(rrm, I), re = ld(rrm, I + 1);
         int n = 0;  // distinct columns claimed (counted by the claiming lanes)
         bool full = false;
+        // a lane's products come in runs of one column (the fine rows and neighbours of an
+        // aggregate map to few coarse columns): a run is summed in registers and added to the
+        // table once, which keeps most lanes off the same slot's compare-and-swap loop
+        uint32_t run_c = EMPTY;
+        ValT run_v = (ValT)0;
+        auto flush = [&]() {
+            if (run_c == EMPTY || full) return;
+            bool fresh;
+            const uint32_t h = rap_claim<RAP_S>(keys, run_c, &fresh);
+            if (h == (uint32_t)RAP_S) {
+                full = true;
+                return;
+            }
+            n += fresh ? 1 : 0;
+            if (NUMERIC) atomicAdd(&vals[h], run_v);
+            run_c = EMPTY;
+        };
+
         for (int64_t r0 = rs; r0 < re; r0 += 32) {
             const int nr = (int)min((int64_t)32, re - r0);
             int ii = 0;
@@ -89,18 +109,19 @@ __global__ void __launch_bounds__(RAP_WARPS * 32) k_rap(int64_t mc, const OffT* 
                     const int64_t ps = ld(prm, j), pe = ld(prm, j + 1);
                     for (int64_t u = ps; u < pe; ++u) {
                         const uint32_t c = (uint32_t)__ldg(pent + u);
-                        bool fresh;
-                        const uint32_t h = rap_claim<RAP_S>(keys, c, &fresh);
-                        if (h == (uint32_t)RAP_S) {
-                            full = true;
-                            break;
+                        const ValT v = NUMERIC ? ra * __ldg(pval + u) : (ValT)0;
+                        if (c == run_c) {
+                            run_v += v;  // same column as the lane's previous product
+                        } else {
+                            flush();
+                            run_c = c;
+                            run_v = v;
                         }
-                        n += fresh ? 1 : 0;
-                        if (NUMERIC) atomicAdd(&vals[h], ra * __ldg(pval + u));
                     }
                 }
             }
         }
+        flush();
         __syncwarp();
         n = warp_sum(n);
         full = __any_sync(FULL, full);
@@ -131,51 +152,51 @@ __global__ void __launch_bounds__(RAP_WARPS * 32) k_rap(int64_t mc, const OffT* 
         cmin = __reduce_min_sync(FULL, cmin);
         __syncwarp();
         const int nn = min(min(cnt, clen), RAP_CAP);
-        // keys (col - cmin) << 9 | slot; columns of a <= 256-entry row differ by < 2^23 here
-        constexpr int E = RAP_CAP / 32;
-        uint32_t v[E];
-        bool wide = false;
-#pragma unroll
-        for (int q = 0; q < E; ++q) {
-            const int idx = lane * E + q;
-            if (idx < nn) {
-                const uint32_t sl = stage[idx];
-                const uint32_t d = keys[sl] - cmin;
-                wide |= d >= (1u << 23);
-                v[q] = (d << 9) | sl;
-            } else {
-                v[q] = 0xffffffffu;
-            }
-        }
-        if (__any_sync(FULL, wide)) {
-            // columns spread over >= 2^23: sort the columns themselves, find slots again
-#pragma unroll
-            for (int q = 0; q < E; ++q) {
-                const int idx = lane * E + q;
-                v[q] = idx < nn ? keys[stage[idx]] : 0xffffffffu;
-            }
-            warp_bitonic_sort<E>(v);
+        // keys (col - cmin) << 9 | slot, sorted by a warp bitonic sort sized to the row (E keys
+        // per lane, 32E >= nn); columns spread over >= 2^23 sort the columns themselves
+        auto sort_write = [&](auto EC) {
+            constexpr int E = decltype(EC)::value;
+            uint32_t v[E];
+            bool wide = false;
 #pragma unroll
             for (int q = 0; q < E; ++q) {
                 const int idx = lane * E + q;
                 if (idx < nn) {
-                    const uint32_t h = probe_find<RAP_S>(keys, v[q]);
-                    cent[cb + idx] = (int32_t)v[q];
-                    cval[cb + idx] = vals[h];
+                    const uint32_t sl = stage[idx];
+                    const uint32_t d = keys[sl] - cmin;
+                    wide |= d >= (1u << 23);
+                    v[q] = (d << 9) | sl;
+                } else {
+                    v[q] = 0xffffffffu;
                 }
             }
-        } else {
+            const bool anywide = __any_sync(FULL, wide);
+            if (anywide) {
+#pragma unroll
+                for (int q = 0; q < E; ++q) {
+                    const int idx = lane * E + q;
+                    v[q] = idx < nn ? keys[stage[idx]] : 0xffffffffu;
+                }
+            }
             warp_bitonic_sort<E>(v);
 #pragma unroll
             for (int q = 0; q < E; ++q) {
                 const int idx = lane * E + q;
                 if (idx < nn) {
-                    const uint32_t sl = v[q] & (RAP_S - 1);
+                    const uint32_t sl = anywide ? probe_find<RAP_S>(keys, v[q]) : (v[q] & (RAP_S - 1));
                     cent[cb + idx] = (int32_t)keys[sl];
                     cval[cb + idx] = vals[sl];
                 }
             }
-        }
+        };
+        if (nn <= 32)
+            sort_write(std::integral_constant<int, 1>{});
+        else if (nn <= 64)
+            sort_write(std::integral_constant<int, 2>{});
+        else if (nn <= 128)
+            sort_write(std::integral_constant<int, 4>{});
+        else
+            sort_write(std::integral_constant<int, 8>{});
         __syncwarp();
         for (int t = lane; t < RAP_S; t += 32) {
             keys[t] = EMPTY;
