@@ -29,17 +29,42 @@ namespace cg = cooperative_groups;
 // (big = 1), else added into C's values in global memory (fp64/fp32 reduction at L2).
 // ------------------------------------------------------------------------------------
 constexpr int HUB_THREADS = 1024;
+
+// L2 residency hints for a long row's values accumulated at L2 (the zeroing stores and the
+// reductions): evict_last keeps the row's value range in L2 while B's rows stream through,
+// so the reductions do not re-read and re-write evicted lines in HBM
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void red_add_keep(double* a, double v, unsigned long long pol) {
+    asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void red_add_keep(float* a, float v, unsigned long long pol) {
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(double* a, double v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(float* a, float v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
 constexpr int HUB_WARPS = HUB_THREADS / 32;
 
 __host__ __device__ constexpr int64_t hub_words(int64_t k) { return ((k + 127) / 128) * 4; }  // multiple of 4
 constexpr int HUB_LONG = 256;  // B rows longer than this are walked by the whole CTA
 constexpr int HUB_LIST = 1024; // capacity of the per-row list of such A entries
+constexpr int HUB_HUGE = 1024; // listed B rows longer than this are walked by the whole CTA
+constexpr int HUB_BATCH = 8;   // A entries per dynamically handed-out batch (short tails at the barrier)
+constexpr int HUB_HLIST = 256; // capacity of the list of such rows (more: walked by one warp)
 
 // shared layout: bm[NW] | gp[NW/4] (padded to 8 bytes) | wtot[HUB_WARPS] (int64) |
-//                list[HUB_LIST] (int32) | nlist (+pad to 16) | vals[vcap]
+//                list[HUB_LIST] (int32) | nlist (+pad to 16) | hlist[HUB_HLIST] | vals[vcap]
 __host__ __device__ constexpr int64_t hub_gp_words(int64_t k) { return (hub_words(k) / 4 + 1) & ~1ll; }
 __host__ __device__ constexpr size_t hub_smem(int64_t k) {
-    return (size_t)(hub_words(k) + hub_gp_words(k)) * 4 + (size_t)HUB_WARPS * 8 + (size_t)HUB_LIST * 4 + 16;
+    return (size_t)(hub_words(k) + hub_gp_words(k)) * 4 + (size_t)HUB_WARPS * 8 + (size_t)HUB_LIST * 4 + 16 +
+           (size_t)HUB_HLIST * 4;
 }
 
 // The products of the A entries [s, e): each warp takes batches of 32 A entries (one
@@ -92,12 +117,12 @@ __device__ __forceinline__ void hub_walk(int64_t s, int64_t e, const int32_t* __
     while (true) {
         int b = 0;
         if (lane == 0) b = atomicAdd(nlist + 1, 1);
-        const int64_t p0 = s + (int64_t)__shfl_sync(FULL, b, 0) * 32;
+        const int64_t p0 = s + (int64_t)__shfl_sync(FULL, b, 0) * HUB_BATCH;
         if (p0 >= e) break;
         const int64_t p = p0 + lane;
         int64_t bs = 0, bl = 0;
         ValT a = (ValT)0;
-        if (p < e) {
+        if (p < e && lane < HUB_BATCH) {
             const int j = __ldg(aent + p);
             if (VALS) a = __ldg(aval + p);
             bs = ld(brm, j);
@@ -118,7 +143,7 @@ __device__ __forceinline__ void hub_walk(int64_t s, int64_t e, const int32_t* __
             }
         }
         const unsigned skip = __ballot_sync(FULL, listed);
-        const int n = (int)min((int64_t)32, e - p0);
+        const int n = (int)min((int64_t)HUB_BATCH, e - p0);
         for (int t = 0; t < n; ++t) {
             if ((skip >> t) & 1u) continue;
             const int64_t tb = __shfl_sync(FULL, bs, t);
@@ -129,8 +154,33 @@ __device__ __forceinline__ void hub_walk(int64_t s, int64_t e, const int32_t* __
     }
     __syncthreads();
     const int nl = min(*nlist, HUB_LIST);
-    for (int l = 0; l < nl; ++l) {
+    // listed rows of up to HUB_HUGE entries: one warp each, handed out by a counter (a CTA-wide
+    // walk of a 300-entry row would leave most of the 1024 threads idle); longer ones are
+    // re-listed at the front of the list and walked by the whole CTA
+    while (true) {
+        int l = 0;
+        if (lane == 0) l = atomicAdd(nlist + 2, 1);
+        l = __shfl_sync(FULL, l, 0);
+        if (l >= nl) break;
         const int64_t p = s + list[l];
+        const int j = __ldg(aent + p);
+        const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
+        if (be - bs > HUB_HUGE) {
+            int h = 0;
+            if (lane == 0) h = atomicAdd(nlist + 3, 1);
+            h = __shfl_sync(FULL, h, 0);
+            if (h < HUB_HLIST) {
+                if (lane == 0) nlist[4 + h] = (int)(p - s);
+                continue;
+            }
+        }
+        const ValT a = VALS ? __ldg(aval + p) : (ValT)0;
+        hub_segment<8, VALS>(bent, bval, bs, be - bs, lane, 32, a, f);
+    }
+    __syncthreads();
+    const int nh = min(nlist[3], HUB_HLIST);
+    for (int l = 0; l < nh; ++l) {
+        const int64_t p = s + nlist[4 + l];
         const int j = __ldg(aent + p);
         const ValT a = VALS ? __ldg(aval + p) : (ValT)0;
         const int64_t bs = ld(brm, j), be = ld(brm, j + 1);
@@ -154,11 +204,12 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
     long long* wtot = (long long*)(gp + hub_gp_words(k));
     int* list = (int*)(wtot + HUB_WARPS);
     int* nlist = list + HUB_LIST;
-    ValT* svals = (ValT*)(nlist + 4);
+    ValT* svals = (ValT*)(nlist + 4 + HUB_HLIST);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r0 = bin_start[bin], r1 = bin_start[bin + 1];
     if (r0 + (int)blockIdx.x >= r1) return;
     const int64_t per = (NW / 4 + HUB_WARPS - 1) / HUB_WARPS * 4;  // words per warp (multiple of 4)
+    const unsigned long long keep = l2_keep_policy();
     for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
         const int i = perm[r];
         const int64_t s = ld(arm, i), e = ld(arm, i + 1);
@@ -167,7 +218,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
         const bool inshared = clen <= (int64_t)vcap;
         if (!inshared && big) continue;  // the cluster tier's row
         for (int64_t t = threadIdx.x; t < NW / 4; t += HUB_THREADS) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
-        if (threadIdx.x == 0) nlist[0] = nlist[1] = 0;
+        if (threadIdx.x == 0) nlist[0] = nlist[1] = nlist[2] = nlist[3] = 0;
         __syncthreads();
         // (1) pattern (accum = OR)
         hub_walk<false>(s, e, aent, aval, brm, bent, bval, list, nlist,
@@ -217,8 +268,8 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
         if (inshared)
             for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) svals[t] = (ValT)0;
         else
-            for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) cval[cb + t] = (ValT)0;
-        if (threadIdx.x == 0) nlist[0] = nlist[1] = 0;
+            for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) st_keep(cval + cb + t, (ValT)0, keep);
+        if (threadIdx.x == 0) nlist[0] = nlist[1] = nlist[2] = nlist[3] = 0;
         __syncthreads();
         // (3) values: rank lookup, accumulation at the rank
         hub_walk<true>(s, e, aent, aval, brm, bent, bval, list, nlist, [&](int c, ValT prod) {
@@ -238,7 +289,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
                 } else if (inshared) {
                     atomicAdd(&svals[rk], prod);
                 } else {
-                    atomicAdd(&cval[cb + rk], prod);
+                    red_add_keep(cval + cb + rk, prod, keep);
                 }
             }
         }, det != 0);
