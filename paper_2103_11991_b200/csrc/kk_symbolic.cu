@@ -998,7 +998,7 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
                     act = actn;
                 }
             };
-            if (COMP && !HT && atom && maxbl <= 32) {
+            if (COMP && atom && maxbl <= 32) {
                 // the chunk's B_C rows back to back, 32 pairs per step: one round of atomic ORs
                 // per step (lanes of different rows sharing a word are ordered by the atomics),
                 // no lanes idle past the end of short rows.  Row of flat pair f: the rows that
@@ -1269,7 +1269,7 @@ static void launch_sym_rows_ht(Launch& L, const SymArgs& a, int bin) {
     L.begin(kname("sym_rows_ht", S), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
-                                               a.counts, a.pat, (DevStatus*)a.st, pblk, 0);
+                                               a.counts, a.pat, (DevStatus*)a.st, pblk, sym_atom());
     L.end(L.stream);
 }
 
