@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=None, help="rows of A in the oracle sample")
     ap.add_argument("--kernel-table", action="store_true", help="print the per-kernel timing table to stderr")
     ap.add_argument("--streams", type=int, default=2, help="library internal streams (1 = serialise the bins)")
+    ap.add_argument("--no-patterns", action="store_true",
+                    help="opts.patterns = 0 (numeric re-derives every row: the A/B of the kept patterns)")
     ap.add_argument("--halo", action="store_true",
                     help="N>1: B row-distributed, each rank fetches only the B rows its A block references "
                          "(NEXT-2) instead of a broadcast of B")
@@ -452,7 +454,7 @@ def run_ours(args):
 
         def __init__(self, X, Y, jacobi=None):
             self.X, self.Y, self.jacobi = X, Y, jacobi
-            self.h = SpGEMM(device=dev, timing=True, num_streams=args.streams)
+            self.h = SpGEMM(device=dev, timing=True, num_streams=args.streams, patterns=not args.no_patterns)
             self.crm = torch.empty(X.nrows + 1, dtype=odt, device=dev)
             _, n = self.h.symbolic(X, Y, c_row_map=self.crm)
             self.cent = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
