@@ -893,8 +893,17 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
         if ((st = ensure(h, P.cval[sl], nnz * vsz, s)) != KK_OK) break;
         if ((st = kk_spgemm_numeric(h, &Ab[q], &Bd, P.crm[sl].p, (int32_t*)P.cent[sl].p, P.cval[sl].p, s)) != KK_OK)
             break;
-        cudaEventRecord(ev_c[q], s);
         nnz_off[q + 1] = nnz_off[q] + nnz;
+        if (osz == 4 && nnz_off[q + 1] > INT32_MAX) {
+            st = fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) exceeds int32 row offsets; use KK_I64");
+            break;
+        }
+        {
+            // the block's row map shifted to global offsets on the device (no host pass)
+            kk::Launch L = make_launch(h, s);
+            kk::add_offset(L, osz == 8, (char*)P.crm[sl].p + osz, r1 - r0, nnz_off[q]);
+        }
+        cudaEventRecord(ev_c[q], s);
         // host output capacity (grows on a larger product: earlier blocks are kept)
         if (P.h_cent_bytes < (size_t)nnz_off[q + 1] * 4 || P.h_cval_bytes < (size_t)nnz_off[q + 1] * vsz) {
             cudaStreamSynchronize(P.s_out);
@@ -905,7 +914,7 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
                 break;
         }
         cudaStreamWaitEvent(P.s_out, ev_c[q], 0);
-        // rows r0+1..r1 of the row map (entry r0 is the previous block's end, fixed below)
+        // rows r0+1..r1 of the global row map (entry r0 is the previous block's end)
         cudaMemcpyAsync((char*)c_row_map + (r0 + 1) * osz, (const char*)P.crm[sl].p + osz, (r1 - r0) * osz,
                         cudaMemcpyDeviceToHost, P.s_out);
         cudaMemcpyAsync((char*)P.h_cent + nnz_off[q] * 4, P.cent[sl].p, nnz * 4, cudaMemcpyDeviceToHost, P.s_out);
@@ -925,18 +934,7 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
     cudaEventDestroy(ev_b);
     if (st != KK_OK) return st;
     if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_multiply_host")) != KK_OK) return st;
-    // global row map: block q's local offsets + the nnz of the blocks before it
-    if (osz == 4 && nnz_off[blocks] > INT32_MAX)
-        return fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) = %lld exceeds int32 row offsets; use KK_I64",
-                    (long long)nnz_off[blocks]);
-    for (int q = 0; q < blocks; ++q) {
-        for (int64_t r = cuts[q] + 1; r <= cuts[q + 1]; ++r) {
-            if (osz == 8)
-                ((int64_t*)c_row_map)[r] += nnz_off[q];
-            else
-                ((int32_t*)c_row_map)[r] += (int32_t)nnz_off[q];
-        }
-    }
+    // the blocks' row maps arrived already shifted to global offsets; entry 0 is 0
     if (osz == 8)
         ((int64_t*)c_row_map)[0] = 0;
     else

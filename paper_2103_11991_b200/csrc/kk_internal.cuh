@@ -108,6 +108,7 @@ void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, in
 // *total_dst (device, may be null) receives the sum; *overflow set when out is
 // int32 and the sum exceeds INT32_MAX.  partial: >= scan_partial_len(m) int64.
 int64_t scan_partial_len(int64_t m);
+void add_offset(Launch& L, bool off64, void* p, int64_t n, int64_t delta);
 void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out, int64_t m, int64_t* partial,
                     unsigned long long* total_dst, int* overflow);
 // pat_off (may be null): rows with a stored pattern (and strictly sorted B) go to the

@@ -6,6 +6,8 @@
 //   a3 k_bin_*            stable row binning by work
 #include "kk_device.cuh"
 
+#include <algorithm>
+
 namespace kk {
 // ------------------------------------------------------------------------------------
 // status init
@@ -27,6 +29,25 @@ __global__ void k_init_status(DevStatus* st) {
         st->sym_bin_start[threadIdx.x] = 0;
         st->num_bin_start[threadIdx.x] = 0;
     }
+}
+
+// p[0..n) += delta (the host-buffer product rebases a row block's row map to global offsets on
+// the device before copying it out)
+template <typename T>
+__global__ void __launch_bounds__(256) k_add_offset(T* __restrict__ p, int64_t n, T delta) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] += delta;
+}
+
+void add_offset(Launch& L, bool off64, void* p, int64_t n, int64_t delta) {
+    if (n <= 0 || delta == 0) return;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)L.num_sms * 8);
+    L.begin("add_offset", L.stream);
+    if (off64)
+        k_add_offset<int64_t><<<grid, 256, 0, L.stream>>>((int64_t*)p, n, (int64_t)delta);
+    else
+        k_add_offset<int32_t><<<grid, 256, 0, L.stream>>>((int32_t*)p, n, (int32_t)delta);
+    L.end(L.stream);
 }
 
 void init_status(Launch& L, DevStatus* st) {
