@@ -218,11 +218,16 @@ kk_status_t kk_spgemm_rap_numeric(kk_spgemm_handle_t handle, const kk_csr_t* R, 
 /* C = A*B with A, B and C in HOST memory: the paper's protocol run end to
  * end over host buffers.  A, B: CSR whose row_map / entries / values are HOST pointers
  * (pinned memory, e.g. cudaHostAlloc, lets the copies run asynchronously; pageable memory
- * works but serialises them).  B is copied to the device once; A is processed in `blocks`
- * contiguous row blocks (<= 0: 8 when A has >= 65,536 rows, else 1), each block's host->device
- * copy, symbolic + numeric phases and device->host copy of its rows of C overlapped with the
- * neighbouring blocks' on three streams (row blocks are independent products, Eq. 1 at
- * PAPER.md:160-163).  Outputs:
+ * works but serialises them).  A is processed in contiguous row blocks (row blocks are
+ * independent products, Eq. 1 at PAPER.md:160-163): each block's host->device copies, symbolic
+ * + numeric phases and device->host copy of its rows of C overlap the neighbouring blocks' on
+ * four streams.  `blocks` > 0 fixes the block count (with 4 or more the first two are a quarter
+ * and a half of the others); `blocks` <= 0 with A of >= 65,536 rows runs a small first block
+ * (1/64 of the rows) and plans the rest from its output size, about 48 MB of host<->device
+ * traffic per block (env KK_HOST_BLOCK_BYTES overrides); fewer rows: one block.  B is copied
+ * once, in 16 row chunks; a block whose columns all lie in a prefix of B's rows starts as soon
+ * as that prefix has arrived.  When A and B are the same host matrix (same three pointers), A's
+ * rows are taken from B's device copy instead of crossing PCIe twice.  Outputs:
  *   c_row_map: HOST, A.nrows+1 of A.offset_type, caller-allocated, filled with C's row map;
  *   *c_nnz: nnz(C);
  *   *c_entries, *c_values: HOST (pinned) arrays of nnz(C) column indices / values owned by the

@@ -11,6 +11,12 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
+#include <array>
+#include <atomic>
+#include <memory>
+#include <chrono>
+#include <thread>
 #include <cstring>
 #include <string>
 #include <algorithm>
@@ -113,7 +119,24 @@ struct kk_spgemm_handle_s {
                          &bc_len,  &pairs,   &cursors, &partial,  &status,   &bmeta,  &wlo,        &pat,
                          &pat_off, &pat_len, &diagchk, &apos,     &bpos,     &spdup,  &spflag,     &status_aux,
                          &workctr};
-    DevStatus* h_status = nullptr;  // pinned
+    // B_C of a B prefix kept between the blocks of kk_spgemm_multiply_host (armed only there)
+    struct BcCarry {
+        bool armed = false, valid = false;
+        const void *brm = nullptr, *bent = nullptr, *bmeta = nullptr, *bc_len = nullptr, *pairs = nullptr;
+        int64_t rows = 0, k = 0;
+        int comp_mode = 0, validate = 0;
+        kk::StatusCarry c;
+    } bcc;
+    DevStatus* h_status = nullptr;  // pinned, mapped (d_status: its device address)
+    DevStatus* d_status = nullptr;
+    // small status reads of the other entry points (pinned, mapped; d_aux: device address)
+    struct Aux {
+        DevStatus st;
+        int flag;
+        int missing;
+    };
+    Aux* h_aux = nullptr;
+    Aux* d_aux = nullptr;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // record of the last symbolic (stale-handle check)
@@ -143,10 +166,8 @@ struct kk_spgemm_handle_s {
     // kk_spgemm_multiply_host: streams, events, device staging (B; two slots of A blocks and
     // C blocks), pinned host staging (rebased row maps; C's entries and values, grow-only)
     struct HostPath {
-        cudaStream_t s_in = nullptr, s_out = nullptr;
+        cudaStream_t s_in = nullptr, s_out = nullptr, s_a = nullptr;
         Buf brm, bent, bval, arm[2], aent[2], aval[2], crm[2], cent[2], cval[2];
-        void* h_reb = nullptr;
-        size_t h_reb_bytes = 0;
         void* h_cent = nullptr;
         size_t h_cent_bytes = 0;
         void* h_cval = nullptr;
@@ -171,7 +192,9 @@ static void tex_release(kk_spgemm_handle_t h) {
 static void tex_for(kk_spgemm_handle_t h, const kk_csr_t* B, unsigned long long* te, unsigned long long* tv) {
     *te = *tv = 0;
     auto& T = h->texb;
-    if (T.ent == B->entries && T.val == B->values && T.nnz == B->nnz && T.vt == (int)B->value_type) {
+    // a texture spanning more of the same arrays serves a B that is a prefix of them (the host
+    // path's row-chunked B)
+    if (T.ent == B->entries && T.val == B->values && T.nnz >= B->nnz && T.vt == (int)B->value_type) {
         *te = T.te;
         *tv = T.tv;
         return;
@@ -369,12 +392,18 @@ kk_status_t kk_spgemm_create(kk_spgemm_handle_t* out, int device, const kk_spgem
     h->device = device;
     h->opts = o;
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (cudaMallocHost((void**)&h->h_status, sizeof(DevStatus)) != cudaSuccess) {
+    if (cudaHostAlloc((void**)&h->h_status, sizeof(DevStatus), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&h->d_status, h->h_status, 0) != cudaSuccess ||
+        cudaHostAlloc((void**)&h->h_aux, sizeof(*h->h_aux), cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void**)&h->d_aux, h->h_aux, 0) != cudaSuccess) {
         cudaGetLastError();
+        if (h->h_status) cudaFreeHost(h->h_status);
+        if (h->h_aux) cudaFreeHost(h->h_aux);
         delete h;
         return KK_ERR_OUT_OF_MEMORY;
     }
     memset(h->h_status, 0, sizeof(DevStatus));
+    memset(h->h_aux, 0, sizeof(*h->h_aux));
     if (o.num_streams > 1) {
         cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
         cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
@@ -397,14 +426,15 @@ kk_status_t kk_spgemm_destroy(kk_spgemm_handle_t h) {
         Buf* hb[] = {&P.brm, &P.bent, &P.bval, &P.arm[0], &P.arm[1], &P.aent[0], &P.aent[1], &P.aval[0],
                      &P.aval[1], &P.crm[0], &P.crm[1], &P.cent[0], &P.cent[1], &P.cval[0], &P.cval[1]};
         for (Buf* b : hb) release(h, *b);
-        if (P.h_reb) cudaFreeHost(P.h_reb);
         if (P.h_cent) cudaFreeHost(P.h_cent);
         if (P.h_cval) cudaFreeHost(P.h_cval);
         if (P.s_in) cudaStreamDestroy(P.s_in);
         if (P.s_out) cudaStreamDestroy(P.s_out);
+        if (P.s_a) cudaStreamDestroy(P.s_a);
     }
     delete h->timer;
     if (h->h_status) cudaFreeHost(h->h_status);
+    if (h->h_aux) cudaFreeHost(h->h_aux);
     if (h->side) cudaStreamDestroy(h->side);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
@@ -420,6 +450,19 @@ static kk::Launch make_launch(kk_spgemm_handle_t h, cudaStream_t s) {
     L.launches = &h->launches;
     L.timer = h->timer;
     return L;
+}
+
+// the status block (and an optional flag word) to the handle's mapped host copy, then one sync
+static kk_status_t read_status(kk_spgemm_handle_t h, cudaStream_t s, const DevStatus* dst, const int* dflag,
+                               const char* what) {
+    kk::Launch L = make_launch(h, s);
+    void* d[2] = {&h->d_aux->st, &h->d_aux->flag};
+    const void* src[2] = {dst, dflag};
+    const size_t nb[2] = {sizeof(DevStatus), sizeof(int)};
+    kk::post_words(L, dflag ? 2 : 1, d, src, nb);
+    kk_status_t st;
+    if ((st = cuda_check(h, cudaGetLastError(), what)) != KK_OK) return st;
+    return cuda_check(h, cudaStreamSynchronize(s), what);
 }
 
 kk_status_t kk_spgemm_compress(kk_spgemm_handle_t h, const kk_csr_t* B, int32_t* len, uint64_t* pairs,
@@ -469,9 +512,8 @@ kk_status_t kk_spgemm_row_flops(kk_spgemm_handle_t h, const kk_csr_t* A, const k
     if (flops_scan) kk::exclusive_scan(L, true, f, true, flops_scan, m, (int64_t*)h->partial.p, nullptr, nullptr);
     if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_row_flops launch")) != KK_OK) return st;
     if (total) {
-        DevStatus hs;
-        cudaMemcpyAsync(&hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
-        if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_row_flops sync")) != KK_OK) return st;
+        if ((st = read_status(h, s, dst, nullptr, "kk_spgemm_row_flops sync")) != KK_OK) return st;
+        const DevStatus hs = h->h_aux->st;
         if (h->opts.validate && hs.bad_index) return fail(h, KK_ERR_INDEX_OVERFLOW, "column index of A out of range");
         *total = (int64_t)hs.total_flops;
     }
@@ -524,11 +566,23 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     kk::Launch L = make_launch(h, s);
     const MatView Av = view(A), Bv = view(B);
 
-    kk::init_status(L, dst);
+    // inside kk_spgemm_multiply_host, B is the same staging copy growing by row chunks: its rows
+    // compressed by the previous block (outputs and flags) are kept
+    auto& Cc = h->bcc;
+    kk::StatusCarry carry;
+    int64_t row0 = 0;
+    if (Cc.armed && Cc.valid && Cc.brm == B->row_map && Cc.bent == B->entries && Cc.rows <= n && Cc.k == k &&
+        Cc.comp_mode == comp_mode && Cc.validate == h->opts.validate && Cc.bmeta == h->bmeta.p &&
+        Cc.bc_len == h->bc_len.p && Cc.pairs == h->pairs.p) {
+        row0 = Cc.rows;
+        carry = Cc.c;
+    }
+    Cc.valid = false;
+    kk::init_status(L, dst, &carry);
     nvtxRangePushA("a4 compress + a1 flops + a2 scan + a3 bins");
     // a4: sortedness flags (+ B_C unless compression is off)
     kk::check_compress(L, off64, Bv, k, comp_mode != 0, h->opts.validate != 0, (int32_t*)h->bc_len.p,
-                       (uint2*)h->pairs.p, (int4*)h->bmeta.p, dst);
+                       (uint2*)h->pairs.p, (int4*)h->bmeta.p, dst, row0);
     // a1: flops per row, symbolic bins
     kk::row_flops_bin(L, off64, Av, Bv, k, comp_mode, h->opts.validate != 0, (const int32_t*)h->bc_len.p,
                       (const int4*)h->bmeta.p, (int64_t*)h->flops.p,
@@ -539,7 +593,12 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     kk::bin_rows(L, m, (const uint8_t*)h->binid.p, (int32_t*)h->binscratch.p, (int32_t*)h->perm_sym.p, sym_start);
     // the symbolic bin sizes on the host (one sync): empty bins are not launched and grids
     // are sized to their bins
-    cudaMemcpyAsync(h->h_status->sym_bin_start, sym_start, sizeof(int) * (kk::NB + 1), cudaMemcpyDeviceToHost, s);
+    {
+        void* d = h->d_status->sym_bin_start;
+        const void* src = sym_start;
+        const size_t nb = sizeof(int) * (kk::NB + 1);
+        kk::post_words(L, 1, &d, &src, &nb);
+    }
     nvtxRangePop();
     if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_symbolic bins")) != KK_OK) return st;
     NvtxRange nvtx_a5("a5 symbolic bins + a6 row map");
@@ -585,14 +644,35 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
                       (const int*)h->pat_len.p, (const uint2*)h->pat.p, (const int64_t*)h->flops.p,
                       (uint8_t*)h->binid.p, dst);
     kk::bin_rows(L, m, (const uint8_t*)h->binid.p, (int32_t*)h->binscratch.p, (int32_t*)h->perm_num.p, num_start);
-    // copy bin starts next to the status block, then the single device->host read
-    cudaMemcpyAsync(dst->sym_bin_start, sym_start, sizeof(int) * (kk::NB + 1), cudaMemcpyDeviceToDevice, s);
-    cudaMemcpyAsync(dst->num_bin_start, num_start, sizeof(int) * (kk::NB + 1), cudaMemcpyDeviceToDevice, s);
-    cudaMemcpyAsync(h->h_status, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
+    // the status words and both bins' starts to the mapped host copy (one CTA's stores), then
+    // the phase's second sync
+    {
+        void* d[3] = {h->d_status, h->d_status->sym_bin_start, h->d_status->num_bin_start};
+        const void* src[3] = {dst, sym_start, num_start};
+        const size_t nb[3] = {offsetof(DevStatus, sym_bin_start), sizeof(int) * (kk::NB + 1),
+                              sizeof(int) * (kk::NB + 1)};
+        kk::post_words(L, 3, d, src, nb);
+    }
     if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_symbolic launch")) != KK_OK) return st;
     if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_symbolic sync")) != KK_OK) return st;
     const DevStatus& hs = *h->h_status;
     if (h->opts.validate && hs.bad_index) return fail(h, KK_ERR_INDEX_OVERFLOW, "column index out of range");
+    if (Cc.armed) {
+        Cc.valid = true;
+        Cc.brm = B->row_map;
+        Cc.bent = B->entries;
+        Cc.rows = n;
+        Cc.k = k;
+        Cc.comp_mode = comp_mode;
+        Cc.validate = h->opts.validate;
+        Cc.bmeta = h->bmeta.p;
+        Cc.bc_len = h->bc_len.p;
+        Cc.pairs = h->pairs.p;
+        Cc.c.b_sorted = hs.b_sorted;
+        Cc.c.b_strict = hs.b_strict;
+        Cc.c.bad_index = hs.bad_index;
+        Cc.c.total_words = hs.total_words;
+    }
     if (hs.overflow)
         return fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) = %llu exceeds int32 row offsets; use KK_I64",
                     (unsigned long long)hs.nnz_c);
@@ -685,8 +765,9 @@ static kk_status_t numeric_impl(kk_spgemm_handle_t h, const kk_csr_t* A, const k
             int missing = 0;
             if ((st = ensure(h, h->diagchk, sizeof(int), s)) != KK_OK) return st;
             if (!kk::check_diagonal(L, A->offset_type == KK_I64, A->nrows, A->row_map, A->entries, (int*)h->diagchk.p,
-                                    &missing))
+                                    &h->h_aux->missing, &h->d_aux->missing))
                 return fail(h, KK_ERR_CUDA, "jacobi numeric: diagonal check failed");
+            missing = h->h_aux->missing;
             if (missing)
                 return fail(h, KK_ERR_INVALID_ARG, "jacobi numeric: A(i,i) is not stored in %d rows (PAPER.md:194)",
                             missing);
@@ -767,12 +848,16 @@ kk_status_t kk_spgemm_stats(kk_spgemm_handle_t h, kk_spgemm_stats_t* out) {
 }
 
 // ---- C = A*B from host memory (PAPER.md:169-174 on host buffers) -------------------------
-// B is copied to the device once; A runs in `blocks` contiguous row blocks, each an
-// independent product (Eq. 1): block q's host->device copy (stream s_in),
-// its symbolic + numeric phases (the caller's stream) and the device->host copy of its rows
-// of C (stream s_out) overlap the neighbouring blocks' (two staging slots, events between
-// the streams).  The global row map is the blocks' row maps shifted by the nnz of the
-// blocks before them, assembled on the host.
+// A runs in contiguous row blocks, each an independent product (Eq. 1):
+// block q's host->device copies, its symbolic + numeric phases (the caller's stream) and the
+// device->host copy of its rows of C (stream s_out) overlap the neighbouring blocks' (two
+// staging slots, events between the streams).  B is copied once, in row chunks (stream s_in),
+// and a block waits only for the prefix of B's rows its columns reach; A's blocks go on s_a
+// (or, for A == B, are taken from B's device copy).  Without a block count the first block is
+// small and the rest are planned from its output size: about KK_HOST_BLOCK_BYTES (48 MB) of traffic
+// per block (each block's fixed cost is ~25 launches, slow while PCIe is saturated).  The
+// global row map is the blocks' row maps shifted on the device by the nnz before them; status
+// reads go through mapped memory (no copy engine), so the copy-out of C runs back to back.
 static kk_status_t ensure_host(kk_spgemm_handle_t h, void** p, size_t* have, size_t need, bool keep, size_t used) {
     if (*have >= need) return KK_OK;
     const size_t bytes = need + need / 4 + 256;
@@ -785,6 +870,32 @@ static kk_status_t ensure_host(kk_spgemm_handle_t h, void** p, size_t* have, siz
     if (*p) cudaFreeHost(*p);
     *p = q;
     *have = bytes;
+    return KK_OK;
+}
+
+// grow a staging buffer outside stream order (its old contents may be in use on any of the
+// host path's streams: they are drained first; a warm handle never gets here)
+static kk_status_t ensure_now(kk_spgemm_handle_t h, Buf& b, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return KK_OK;
+    auto& P = h->hp;
+    cudaStreamSynchronize(s);
+    cudaStreamSynchronize(P.s_in);
+    cudaStreamSynchronize(P.s_a);
+    cudaStreamSynchronize(P.s_out);
+    release(h, b);
+    bytes = bytes + bytes / 8 + 256;
+    void* p = nullptr;
+    if (h->opts.alloc) {
+        p = h->opts.alloc(bytes, s, h->opts.alloc_ctx);
+        if (!p) return fail(h, KK_ERR_OUT_OF_MEMORY, "staging allocation of %zu bytes failed", bytes);
+        cudaStreamSynchronize(s);
+    } else {
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) return cuda_check(h, e, "cudaMalloc(staging)");
+    }
+    b.p = p;
+    b.bytes = bytes;
     return KK_OK;
 }
 
@@ -802,98 +913,247 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
     if (!P.s_in) {
         cudaStreamCreateWithFlags(&P.s_in, cudaStreamNonBlocking);
         cudaStreamCreateWithFlags(&P.s_out, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&P.s_a, cudaStreamNonBlocking);
     }
-    const int64_t m = A->nrows;
+    const int64_t m = A->nrows, n = B->nrows;
     const size_t osz = A->offset_type == KK_I64 ? 8 : 4, vsz = A->value_type == KK_F64 ? 8 : 4;
     auto rmv = [&](const void* rm, int64_t i) -> int64_t {
         return osz == 8 ? ((const int64_t*)rm)[i] : (int64_t)((const int32_t*)rm)[i];
     };
-    if (blocks <= 0) blocks = m >= 65536 ? 8 : 1;
-    blocks = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, std::max<int64_t>(m, 1)));
-    std::vector<int64_t> cuts(blocks + 1);
-    for (int q = 0; q <= blocks; ++q) cuts[q] = m * q / blocks;
-    // B once (every block reads all of it)
-    if ((st = ensure(h, P.brm, (B->nrows + 1) * osz, s)) != KK_OK) return st;
+    // C = A*A with one host matrix (the squaring the paper benchmarks): A's blocks are copied from
+    // the device copy of B instead of crossing PCIe again
+    const bool alias = A->row_map == B->row_map && A->entries == B->entries && A->values == B->values &&
+                       A->offset_type == B->offset_type && A->nnz == B->nnz && A->nrows == B->nrows;
+    // row cuts: fixed for a given block count (the first two a quarter and a half of the others
+    // when there are 4+); planned after block 0 otherwise
+    const bool adaptive = blocks <= 0 && m >= 65536;
+    std::vector<int64_t> cuts{0};
+    if (adaptive) {
+        cuts.push_back(std::max<int64_t>(1, m / 64));
+    } else {
+        blocks = (int)std::max<int64_t>(1, std::min<int64_t>(blocks <= 0 ? 1 : blocks, std::max<int64_t>(m, 1)));
+        std::vector<double> w(blocks, 1.0);
+        if (blocks >= 4) w[0] = 0.25, w[1] = 0.5;
+        double wt = 0.0, acc = 0.0;
+        for (double x : w) wt += x;
+        for (int q = 1; q < blocks; ++q) {
+            acc += w[q - 1];
+            cuts.push_back(std::max(cuts.back(), std::min<int64_t>(m, (int64_t)((double)m * acc / wt))));
+        }
+        cuts.push_back(m);
+    }
+    auto nblocks = [&]() { return (int)cuts.size() - 1; };
+    if ((st = ensure(h, P.brm, (n + 1) * osz, s)) != KK_OK) return st;
     if ((st = ensure(h, P.bent, B->nnz * 4, s)) != KK_OK) return st;
     if ((st = ensure(h, P.bval, B->nnz * vsz, s)) != KK_OK) return st;
+    // the B_C workspace sized for all of B, so the blocks' symbolic phases compress only the
+    // rows their prefix adds (kk_spgemm_symbolic keeps the rest while armed)
+    h->bcc = kk_spgemm_handle_s::BcCarry();
+    const bool carry_ok = ensure(h, h->bmeta, (size_t)n * 16, s) == KK_OK &&
+                          ensure(h, h->bc_len, (size_t)n * 4, s) == KK_OK &&
+                          ensure(h, h->pairs, (size_t)B->nnz * 8, s) == KK_OK;
     cudaStreamSynchronize(s);  // the workspace may have been (re)allocated on s
-    cudaEvent_t ev_b;
-    cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
-    cudaMemcpyAsync(P.brm.p, B->row_map, (B->nrows + 1) * osz, cudaMemcpyHostToDevice, P.s_in);
-    cudaMemcpyAsync(P.bent.p, B->entries, B->nnz * 4, cudaMemcpyHostToDevice, P.s_in);
-    cudaMemcpyAsync(P.bval.p, B->values, B->nnz * vsz, cudaMemcpyHostToDevice, P.s_in);
-    cudaEventRecord(ev_b, P.s_in);
-    kk_csr_t Bd = *B;
-    Bd.row_map = P.brm.p;
-    Bd.entries = (const int32_t*)P.bent.p;
-    Bd.values = P.bval.p;
-    // the blocks' row maps rebased to 0, in pinned staging (block q at offset q + cuts[q])
-    if ((st = ensure_host(h, &P.h_reb, &P.h_reb_bytes, (m + blocks) * osz, false, 0)) != KK_OK) return st;
-    for (int q = 0; q < blocks; ++q) {
-        const int64_t r0 = cuts[q], r1 = cuts[q + 1], base = rmv(A->row_map, r0);
-        for (int64_t r = r0; r <= r1; ++r) {
-            const int64_t v = rmv(A->row_map, r) - base;
-            if (osz == 8)
-                ((int64_t*)P.h_reb)[q + r] = v;
-            else
-                ((int32_t*)P.h_reb)[q + r] = (int32_t)v;
+    h->bcc.armed = carry_ok;
+    // KK_HOST_TRACE=1: per-block copy/compute completion times on stderr (diagnostic)
+    static const bool trace = getenv("KK_HOST_TRACE") && atoi(getenv("KK_HOST_TRACE")) > 0;
+    const unsigned evflags = trace ? cudaEventDefault : cudaEventDisableTiming;
+    const auto t_host0 = std::chrono::steady_clock::now();
+    auto host_ms = [&]() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count();
+    };
+    std::vector<std::array<double, 3>> hts;
+    cudaEvent_t ev_t0 = nullptr;
+    if (trace) {
+        cudaEventCreate(&ev_t0);
+        cudaEventRecord(ev_t0, P.s_in);
+    }
+    // B's row chunks, issued on s_in in the order the blocks need them
+    const int nch = (int)std::max<int64_t>(1, std::min<int64_t>(16, n));
+    std::vector<int64_t> bcut(nch + 1);
+    for (int c = 0; c <= nch; ++c) bcut[c] = n * c / nch;
+    std::vector<cudaEvent_t> ev_bc(nch);
+    for (int c = 0; c < nch; ++c) cudaEventCreateWithFlags(&ev_bc[c], evflags);
+    int b_issued = 0;
+    auto issue_b = [&](int upto) {
+        for (; b_issued <= upto; ++b_issued) {
+            const int64_t lo = bcut[b_issued], hi = bcut[b_issued + 1];
+            const int64_t e_lo = rmv(B->row_map, lo), e_hi = rmv(B->row_map, hi);
+            cudaMemcpyAsync((char*)P.brm.p + lo * osz, (const char*)B->row_map + lo * osz, (hi - lo + 1) * osz,
+                            cudaMemcpyHostToDevice, P.s_in);
+            cudaMemcpyAsync((char*)P.bent.p + e_lo * 4, B->entries + e_lo, (e_hi - e_lo) * 4, cudaMemcpyHostToDevice,
+                            P.s_in);
+            cudaMemcpyAsync((char*)P.bval.p + e_lo * vsz, (const char*)B->values + e_lo * vsz, (e_hi - e_lo) * vsz,
+                            cudaMemcpyHostToDevice, P.s_in);
+            cudaEventRecord(ev_bc[b_issued], P.s_in);
         }
-    }
-    // staging slots: sized for the largest block's A arrays
-    int64_t max_rows = 0, max_nnz = 0;
-    for (int q = 0; q < blocks; ++q) {
-        max_rows = std::max<int64_t>(max_rows, cuts[q + 1] - cuts[q]);
-        max_nnz = std::max<int64_t>(max_nnz, rmv(A->row_map, cuts[q + 1]) - rmv(A->row_map, cuts[q]));
-    }
-    for (int sl = 0; sl < 2; ++sl) {
-        if ((st = ensure(h, P.arm[sl], (max_rows + 1) * osz, s)) != KK_OK) return st;
-        if ((st = ensure(h, P.aent[sl], max_nnz * 4, s)) != KK_OK) return st;
-        if ((st = ensure(h, P.aval[sl], max_nnz * vsz, s)) != KK_OK) return st;
-        if ((st = ensure(h, P.crm[sl], (max_rows + 1) * osz, s)) != KK_OK) return st;
-    }
-    cudaStreamSynchronize(s);
-    std::vector<cudaEvent_t> ev_in(blocks), ev_c(blocks), ev_out(blocks);
-    for (int q = 0; q < blocks; ++q) {
-        cudaEventCreateWithFlags(&ev_in[q], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_c[q], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&ev_out[q], cudaEventDisableTiming);
-    }
-    std::vector<kk_csr_t> Ab(blocks);
-    auto load_block = [&](int q) {
+    };
+    // the largest column of every group of G rows of A, from helper threads running ahead of
+    // the blocks (group g on thread g % T; a group's pass stops once it reaches B's last chunk)
+    constexpr int64_t G = 4096;
+    const int64_t ngr = (m + G - 1) / G;
+    std::vector<int32_t> gmax(std::max<int64_t>(ngr, 1), -1);
+    std::unique_ptr<std::atomic<int>[]> gready(new std::atomic<int>[std::max<int64_t>(ngr, 1)]);
+    for (int64_t g = 0; g < ngr; ++g) gready[g].store(0, std::memory_order_relaxed);
+    std::atomic<bool> stop{false};
+    const char* ts = getenv("KK_HOST_SCAN_THREADS");
+    const int nthr = (int)std::max<int64_t>(
+        1, std::min<int64_t>({ts && atoi(ts) > 0 ? atoi(ts) : 4, (int64_t)std::thread::hardware_concurrency() / 2,
+                              (ngr + 7) / 8}));
+    std::vector<std::thread> scanners;
+    for (int t = 0; t < nthr; ++t)
+        scanners.emplace_back([&, t]() {
+            const int32_t last = (int32_t)std::min<int64_t>(bcut[nch - 1], INT32_MAX);
+            const int32_t* ent = A->entries;
+            for (int64_t g = t; g < ngr && !stop.load(std::memory_order_relaxed); g += nthr) {
+                const int64_t e0 = rmv(A->row_map, g * G), e1 = rmv(A->row_map, std::min<int64_t>(m, (g + 1) * G));
+                int32_t mx = -1;
+                for (int64_t i0 = e0; i0 < e1 && mx < last; i0 += 8192) {
+                    const int64_t i1 = std::min<int64_t>(e1, i0 + 8192);
+                    int32_t m8 = -1;
+                    for (int64_t i = i0; i < i1; ++i) m8 = ent[i] > m8 ? ent[i] : m8;
+                    mx = std::max(mx, m8);
+                }
+                gmax[g] = mx;
+                gready[g].store(1, std::memory_order_release);
+            }
+        });
+    // the chunk holding every B row rows [r0, r1) of A read (and, for A == B, the rows themselves)
+    auto need_chunk = [&](int64_t r0, int64_t r1) {
+        int64_t rows = alias ? r1 : 0;
+        if (r1 > r0) {
+            for (int64_t g = r0 / G; g <= (r1 - 1) / G; ++g) {
+                while (!gready[g].load(std::memory_order_acquire)) std::this_thread::yield();
+                rows = std::max<int64_t>(rows, (int64_t)gmax[g] + 1);
+            }
+        }
+        int c = 0;
+        while (c < nch - 1 && bcut[c + 1] < rows) ++c;
+        return c;
+    };
+    std::vector<cudaEvent_t> ev_in, ev_c, ev_out;
+    std::vector<int> bneed;
+    std::vector<kk_csr_t> Ab, Bq;
+    auto add_events = [&]() {  // per-block records for the blocks cut so far
+        while ((int)ev_in.size() < nblocks()) {
+            cudaEvent_t e[3];
+            for (auto& x : e) cudaEventCreateWithFlags(&x, evflags);
+            ev_in.push_back(e[0]);
+            ev_c.push_back(e[1]);
+            ev_out.push_back(e[2]);
+            bneed.push_back(nch - 1);
+            Ab.emplace_back();
+            Bq.emplace_back();
+            if (trace) hts.push_back({0.0, 0.0, 0.0});
+        }
+    };
+    add_events();
+    // host side of block q: its B prefix, then (A != B) its rows' copies into slot q % 2
+    auto load_block = [&](int q) -> kk_status_t {
         const int sl = q % 2;
         const int64_t r0 = cuts[q], r1 = cuts[q + 1];
         const int64_t e0 = rmv(A->row_map, r0), e1 = rmv(A->row_map, r1);
-        if (q >= 2) cudaStreamWaitEvent(P.s_in, ev_c[q - 2], 0);  // slot free once block q-2 is computed
-        cudaMemcpyAsync(P.arm[sl].p, (const char*)P.h_reb + (q + r0) * osz, (r1 - r0 + 1) * osz,
-                        cudaMemcpyHostToDevice, P.s_in);
-        cudaMemcpyAsync(P.aent[sl].p, A->entries + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, P.s_in);
-        cudaMemcpyAsync(P.aval[sl].p, (const char*)A->values + e0 * vsz, (e1 - e0) * vsz, cudaMemcpyHostToDevice,
-                        P.s_in);
-        cudaEventRecord(ev_in[q], P.s_in);
+        kk_status_t e;
+        if ((e = ensure_now(h, P.arm[sl], (r1 - r0 + 1) * osz, s)) != KK_OK) return e;
+        if ((e = ensure_now(h, P.crm[sl], (r1 - r0 + 1) * osz, s)) != KK_OK) return e;
+        if ((e = ensure_now(h, P.aent[sl], (e1 - e0) * 4, s)) != KK_OK) return e;
+        if ((e = ensure_now(h, P.aval[sl], (e1 - e0) * vsz, s)) != KK_OK) return e;
+        bneed[q] = need_chunk(r0, r1);
+        issue_b(bneed[q]);
+        kk_csr_t b = *B;  // the prefix of B's rows the block reads
+        b.nrows = bcut[bneed[q] + 1];
+        b.nnz = rmv(B->row_map, b.nrows);
+        b.row_map = P.brm.p;
+        b.entries = (const int32_t*)P.bent.p;
+        b.values = P.bval.p;
+        Bq[q] = b;
+        if (!alias) {
+            // the block's row map as is (rebased to 0 on the device), entries, values
+            if (q >= 2) cudaStreamWaitEvent(P.s_a, ev_c[q - 2], 0);  // slot free once block q-2 is computed
+            cudaMemcpyAsync(P.arm[sl].p, (const char*)A->row_map + r0 * osz, (r1 - r0 + 1) * osz,
+                            cudaMemcpyHostToDevice, P.s_a);
+            cudaMemcpyAsync(P.aent[sl].p, A->entries + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, P.s_a);
+            cudaMemcpyAsync(P.aval[sl].p, (const char*)A->values + e0 * vsz, (e1 - e0) * vsz,
+                            cudaMemcpyHostToDevice, P.s_a);
+        }
+        cudaEventRecord(ev_in[q], alias ? P.s_in : P.s_a);
         kk_csr_t a = *A;
         a.nrows = r1 - r0;
+        a.ncols = b.nrows;
         a.nnz = e1 - e0;
         a.row_map = P.arm[sl].p;
         a.entries = (const int32_t*)P.aent[sl].p;
         a.values = P.aval[sl].p;
         Ab[q] = a;
+        return KK_OK;
     };
-    for (int q = 0; q < std::min(2, blocks); ++q) load_block(q);
-    std::vector<int64_t> nnz_off(blocks + 1, 0);
-    st = KK_OK;
-    for (int q = 0; q < blocks && st == KK_OK; ++q) {
+    // the rest of the rows after block 0, from block 0's output size: blocks of about
+    // KK_HOST_BLOCK_BYTES (default 48 MB) of host<->device traffic, the first half size
+    auto plan = [&](int64_t nnz0) {
+        const char* tb = getenv("KK_HOST_BLOCK_BYTES");
+        const double target = tb && atof(tb) > 0 ? atof(tb) : 48e6;
+        const int64_t r0 = cuts[1], rows0 = std::max<int64_t>(cuts[1], 1);
+        if (r0 >= m) return;
+        const double out = (double)nnz0 * (double)(4 + vsz) / (double)rows0 * (double)(m - r0) +
+                           (double)(m - r0) * osz;
+        const double ina = alias ? 0.0 : (double)(rmv(A->row_map, m) - rmv(A->row_map, r0)) * (4.0 + vsz) +
+                                             (double)(m - r0) * osz;
+        const double inb = (double)(B->nnz - rmv(B->row_map, bcut[bneed[0] + 1])) * (4.0 + vsz);
+        const int nb = (int)std::max<double>(1.0, std::min<double>(64.0, std::ceil((out + ina + inb) / target)));
+        const double wt = nb - 0.5;
+        double acc = 0.0;
+        for (int q = 0; q < nb - 1; ++q) {
+            acc += q == 0 ? 0.5 : 1.0;
+            cuts.push_back(std::max(cuts.back(), std::min<int64_t>(m, r0 + (int64_t)((double)(m - r0) * acc / wt))));
+        }
+        cuts.push_back(m);
+        add_events();
+    };
+    {
+        // B's texture objects sized for all of it, so the blocks' prefixes share them
+        kk_csr_t bf = *B;
+        bf.row_map = P.brm.p;
+        bf.entries = (const int32_t*)P.bent.p;
+        bf.values = P.bval.p;
+        unsigned long long te, tv;
+        tex_for(h, &bf, &te, &tv);
+    }
+    std::vector<int64_t> nnz_off{0};
+    st = load_block(0);
+    for (int q = 0; q < nblocks() && st == KK_OK; ++q) {
         const int sl = q % 2;
         const int64_t r0 = cuts[q], r1 = cuts[q + 1];
         cudaStreamWaitEvent(s, ev_in[q], 0);
-        cudaStreamWaitEvent(s, ev_b, 0);
+        cudaStreamWaitEvent(s, ev_bc[bneed[q]], 0);
         if (q >= 2) cudaStreamWaitEvent(s, ev_out[q - 2], 0);  // C slot drained to the host
+        {
+            // the block's row map rebased to 0 on the device; for A == B (same host matrix) its rows
+            // come from the device copy of B.  Slot sl is free: block q-2 was computed earlier on
+            // this stream.
+            kk::Launch L = make_launch(h, s);
+            const int64_t e0 = rmv(A->row_map, r0), e1 = rmv(A->row_map, r1);
+            if (alias) {
+                kk::rebase_row_map(L, osz == 8, P.arm[sl].p, (const char*)P.brm.p + r0 * osz, r1 - r0 + 1, e0);
+                kk::copy_bytes(L, P.aent[sl].p, (const char*)P.bent.p + e0 * 4, (e1 - e0) * 4);
+                kk::copy_bytes(L, P.aval[sl].p, (const char*)P.bval.p + e0 * vsz, (e1 - e0) * vsz);
+            } else {
+                kk::rebase_row_map(L, osz == 8, P.arm[sl].p, P.arm[sl].p, r1 - r0 + 1, e0);
+            }
+        }
         int64_t nnz = 0;
-        if ((st = kk_spgemm_symbolic(h, &Ab[q], &Bd, P.crm[sl].p, &nnz, s)) != KK_OK) break;
+        if (trace) hts[q][0] = host_ms();
+        if ((st = kk_spgemm_symbolic(h, &Ab[q], &Bq[q], P.crm[sl].p, &nnz, s)) != KK_OK) break;
+        if (trace) hts[q][1] = host_ms();
+        if (q == 0) {
+            if (adaptive) plan(nnz);
+            // block 1 as soon as block 0's symbolic phase has run
+            if (nblocks() > 1 && (st = load_block(1)) != KK_OK) break;
+        }
         if ((st = ensure(h, P.cent[sl], nnz * 4, s)) != KK_OK) break;
         if ((st = ensure(h, P.cval[sl], nnz * vsz, s)) != KK_OK) break;
-        if ((st = kk_spgemm_numeric(h, &Ab[q], &Bd, P.crm[sl].p, (int32_t*)P.cent[sl].p, P.cval[sl].p, s)) != KK_OK)
+        if ((st = kk_spgemm_numeric(h, &Ab[q], &Bq[q], P.crm[sl].p, (int32_t*)P.cent[sl].p, P.cval[sl].p, s)) !=
+            KK_OK)
             break;
-        nnz_off[q + 1] = nnz_off[q] + nnz;
+        nnz_off.push_back(nnz_off[q] + nnz);
         if (osz == 4 && nnz_off[q + 1] > INT32_MAX) {
             st = fail(h, KK_ERR_INDEX_OVERFLOW, "nnz(C) exceeds int32 row offsets; use KK_I64");
             break;
@@ -921,17 +1181,41 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
         cudaMemcpyAsync((char*)P.h_cval + nnz_off[q] * vsz, P.cval[sl].p, nnz * vsz, cudaMemcpyDeviceToHost,
                         P.s_out);
         cudaEventRecord(ev_out[q], P.s_out);
-        if (q + 2 < blocks) load_block(q + 2);
+        // block q+2's copies once this block's are queued (two ahead); it reuses slot q % 2, whose
+        // wait is on ev_c[q], recorded above
+        if (q + 2 < nblocks() && (st = load_block(q + 2)) != KK_OK) break;
+        if (trace) hts[q][2] = host_ms();
     }
+    stop.store(true);
+    for (auto& t : scanners) t.join();
+    h->bcc = kk_spgemm_handle_s::BcCarry();
     cudaStreamSynchronize(P.s_in);
+    cudaStreamSynchronize(P.s_a);
     cudaStreamSynchronize(P.s_out);
     cudaStreamSynchronize(s);
-    for (int q = 0; q < blocks; ++q) {
+    const int nbk = nblocks();
+    if (trace && st == KK_OK) {
+        auto at = [&](cudaEvent_t e) {
+            float ms = -1.f;
+            cudaEventElapsedTime(&ms, ev_t0, e);
+            return ms;
+        };
+        fprintf(stderr, "[kk host] %d blocks%s; B in %.3f ms (%d chunks)\n", nbk, adaptive ? " (planned)" : "",
+                at(ev_bc[std::min(b_issued, nch) - 1]), nch);
+        for (int q = 0; q < nbk; ++q)
+            fprintf(stderr,
+                    "[kk host] block %d: in %.3f  computed %.3f  out %.3f ms (nnz %lld, B rows %lld)  host: "
+                    "symbolic %.3f-%.3f, issued %.3f\n",
+                    q, at(ev_in[q]), at(ev_c[q]), at(ev_out[q]), (long long)(nnz_off[q + 1] - nnz_off[q]),
+                    (long long)Bq[q].nrows, hts[q][0], hts[q][1], hts[q][2]);
+    }
+    if (ev_t0) cudaEventDestroy(ev_t0);
+    for (size_t q = 0; q < ev_in.size(); ++q) {
         cudaEventDestroy(ev_in[q]);
         cudaEventDestroy(ev_c[q]);
         cudaEventDestroy(ev_out[q]);
     }
-    cudaEventDestroy(ev_b);
+    for (int c = 0; c < nch; ++c) cudaEventDestroy(ev_bc[c]);
     if (st != KK_OK) return st;
     if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_multiply_host")) != KK_OK) return st;
     // the blocks' row maps arrived already shifted to global offsets; entry 0 is 0
@@ -939,7 +1223,7 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
         ((int64_t*)c_row_map)[0] = 0;
     else
         ((int32_t*)c_row_map)[0] = 0;
-    *c_nnz = nnz_off[blocks];
+    *c_nnz = nnz_off[nbk];
     *c_entries = (int32_t*)P.h_cent;
     *c_values = P.h_cval;
     return KK_OK;
@@ -977,12 +1261,9 @@ extern "C" kk_status_t kk_spgemm_rap_symbolic(kk_spgemm_handle_t h, const kk_csr
     kk::rap_symbolic(L, off64, view(R), view(A), view(P), (int32_t*)h->counts.p, (int*)h->spflag.p);
     kk::exclusive_scan(L, false, h->counts.p, off64, c_row_map, mc, (int64_t*)h->partial.p, &dst->nnz_c,
                        &dst->overflow);
-    DevStatus hs;
-    int too_many = 0;
-    cudaMemcpyAsync(&hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&too_many, h->spflag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
-    if ((st = cuda_check(h, cudaGetLastError(), "kk_spgemm_rap_symbolic launch")) != KK_OK) return st;
-    if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spgemm_rap_symbolic sync")) != KK_OK) return st;
+    if ((st = read_status(h, s, dst, (const int*)h->spflag.p, "kk_spgemm_rap_symbolic sync")) != KK_OK) return st;
+    const DevStatus hs = h->h_aux->st;
+    const int too_many = h->h_aux->flag;
     if (too_many)
         return fail(h, KK_ERR_UNSUPPORTED_TYPE,
                     "fused R*A*P: a coarse row has more than 256 distinct columns (use two products)");
@@ -1069,12 +1350,9 @@ kk_status_t kk_spadd_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk_
                        (int32_t*)h->bpos.p, (uint8_t*)h->spdup.p, (int*)h->spflag.p);
     kk::exclusive_scan(L, false, h->counts.p, off64, c_row_map, m, (int64_t*)h->partial.p, &dst->nnz_c,
                        &dst->overflow);
-    DevStatus hs;
-    cudaMemcpyAsync(&hs, dst, sizeof(DevStatus), cudaMemcpyDeviceToHost, s);
-    int too_long = 0;
-    cudaMemcpyAsync(&too_long, h->spflag.p, sizeof(int), cudaMemcpyDeviceToHost, s);
-    if ((st = cuda_check(h, cudaGetLastError(), "kk_spadd_symbolic launch")) != KK_OK) return st;
-    if ((st = cuda_check(h, cudaStreamSynchronize(s), "kk_spadd_symbolic sync")) != KK_OK) return st;
+    if ((st = read_status(h, s, dst, (const int*)h->spflag.p, "kk_spadd_symbolic sync")) != KK_OK) return st;
+    const DevStatus hs = h->h_aux->st;
+    const int too_long = h->h_aux->flag;
     if (too_long)
         return fail(h, KK_ERR_UNSUPPORTED_TYPE, "SpAdd: a row has nnz(A_i) + nnz(B_i) > 16384 (the CTA tier's shared-memory sort)");
     if (hs.overflow)

@@ -94,11 +94,18 @@ struct Launch {
 };
 
 // ---- host launchers (kk_kernels.cu) -------------------------------------------------
-void init_status(Launch& L, DevStatus* st);
+// B-row flags already established for a prefix of B's rows (the host-buffer product compresses
+// only the rows each block adds); default: none
+struct StatusCarry {
+    int b_sorted = 1, b_strict = 1, bad_index = 0;
+    unsigned long long total_words = 0;
+};
+void init_status(Launch& L, DevStatus* st, const StatusCarry* carry = nullptr);
 // bmeta (may be null): per B row {nnz, |B_C row|, first column, last column}
-// (first/last = INT_MAX / -1 for empty rows)
+// (first/last = INT_MAX / -1 for empty rows).  Rows [row0, B.nrows) only (the outputs of the
+// rows before are kept).
 void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_comp, bool validate,
-                    int32_t* bc_len, uint2* pairs, int4* bmeta, DevStatus* st);
+                    int32_t* bc_len, uint2* pairs, int4* bmeta, DevStatus* st, int64_t row0 = 0);
 // bmeta (may be null: then the B row map is read); wlo (may be null): word-aligned first
 // column of the window of rows in window bins
 void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, int64_t k, int comp_mode,
@@ -109,6 +116,10 @@ void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, in
 // int32 and the sum exceeds INT32_MAX.  partial: >= scan_partial_len(m) int64.
 int64_t scan_partial_len(int64_t m);
 void add_offset(Launch& L, bool off64, void* p, int64_t n, int64_t delta);
+// device -> device copy on the SMs (keeps the copy engines free for the host transfers)
+void copy_bytes(Launch& L, void* dst, const void* src, int64_t bytes);
+// dst[i] = src[i] - base for i < n (offsets of the row map's type; dst may be src)
+void rebase_row_map(Launch& L, bool off64, void* dst, const void* src, int64_t n, int64_t base);
 void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out, int64_t m, int64_t* partial,
                     unsigned long long* total_dst, int* overflow);
 // pat_off (may be null): rows with a stored pattern (and strictly sorted B) go to the
@@ -182,9 +193,13 @@ void rap_symbolic(Launch& L, bool off64, const MatView& R, const MatView& A, con
                   int* too_many);
 void rap_numeric(Launch& L, bool off64, bool f64, const MatView& R, const MatView& A, const MatView& P,
                  const void* crm, int32_t* cent, void* cval);
-// validate for the Jacobi-fused numeric: *missing (host) = rows of the square A without a
-// stored diagonal entry; scratch: one device int.  Synchronises L.stream.  false on a CUDA error.
+// validate for the Jacobi-fused numeric: *missing (mapped pinned host int, missing_map its
+// device address) = rows of the square A without a stored diagonal entry; scratch: one device
+// int.  Synchronises L.stream.  false on a CUDA error.
 bool check_diagonal(Launch& L, bool off64, int64_t m, const void* row_map, const int32_t* entries, int* scratch,
-                    int* missing);
+                    int* missing, int* missing_map);
+// dst[g][0 .. bytes[g]/4) = src[g][...] for g < nseg <= 4, by one CTA's stores (dst may be the
+// device address of mapped pinned host memory: a status read without a copy engine)
+void post_words(Launch& L, int nseg, void* const* dst, const void* const* src, const size_t* bytes);
 
 }  // namespace kk

@@ -12,15 +12,15 @@ namespace kk {
 // ------------------------------------------------------------------------------------
 // status init
 // ------------------------------------------------------------------------------------
-__global__ void k_init_status(DevStatus* st) {
+__global__ void k_init_status(DevStatus* st, StatusCarry c) {
     if (threadIdx.x == 0) {
         st->total_flops = 0;
-        st->total_words = 0;
+        st->total_words = c.total_words;
         st->nnz_c = 0;
         st->pat_used = 0;
-        st->b_sorted = 1;
-        st->b_strict = 1;
-        st->bad_index = 0;
+        st->b_sorted = c.b_sorted;
+        st->b_strict = c.b_strict;
+        st->bad_index = c.bad_index;
         st->overflow = 0;
         st->use_comp = 0;
         st->pad = 0;
@@ -50,9 +50,74 @@ void add_offset(Launch& L, bool off64, void* p, int64_t n, int64_t delta) {
     L.end(L.stream);
 }
 
-void init_status(Launch& L, DevStatus* st) {
+// Status words to the host by SM stores into mapped pinned memory: the read does not queue on
+// a copy engine, so a bulk device->host copy in flight on another stream (the host-buffer
+// product's pipeline) cannot delay the phase's sync behind it.
+struct WordSegs {
+    uint32_t* dst[4];
+    const uint32_t* src[4];
+    int n[4];
+};
+
+__global__ void __launch_bounds__(256) k_post_words(WordSegs w, int nseg) {
+    for (int g = 0; g < nseg; ++g)
+        for (int i = threadIdx.x; i < w.n[g]; i += blockDim.x) w.dst[g][i] = w.src[g][i];
+}
+
+void post_words(Launch& L, int nseg, void* const* dst, const void* const* src, const size_t* bytes) {
+    WordSegs w{};
+    for (int g = 0; g < nseg; ++g) {
+        w.dst[g] = (uint32_t*)dst[g];
+        w.src[g] = (const uint32_t*)src[g];
+        w.n[g] = (int)(bytes[g] / 4);
+    }
+    L.begin("post_status", L.stream);
+    k_post_words<<<1, 256, 0, L.stream>>>(w, nseg);
+    L.end(L.stream);
+}
+
+// dst[i] = src[i] - base, i < n (a row block's row map rebased to 0; dst may be src)
+template <typename T>
+__global__ void __launch_bounds__(256) k_rebase(T* dst, const T* src, int64_t n, T base) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i] - base;
+}
+
+void rebase_row_map(Launch& L, bool off64, void* dst, const void* src, int64_t n, int64_t base) {
+    if (n <= 0) return;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)L.num_sms * 8);
+    L.begin("rebase_row_map", L.stream);
+    if (off64)
+        k_rebase<int64_t><<<grid, 256, 0, L.stream>>>((int64_t*)dst, (const int64_t*)src, n, (int64_t)base);
+    else
+        k_rebase<int32_t><<<grid, 256, 0, L.stream>>>((int32_t*)dst, (const int32_t*)src, n, (int32_t)base);
+    L.end(L.stream);
+}
+
+// dst[0..bytes) = src[0..bytes) on the SMs (16-byte words when both are aligned)
+__global__ void __launch_bounds__(256) k_copy_bytes(char* __restrict__ dst, const char* __restrict__ src,
+                                                    int64_t bytes) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+        const int64_t n16 = bytes >> 4;
+        for (int64_t i = tid; i < n16; i += nt) ((int4*)dst)[i] = __ldg((const int4*)src + i);
+        for (int64_t i = (n16 << 4) + tid; i < bytes; i += nt) dst[i] = src[i];
+    } else {
+        for (int64_t i = tid; i < bytes; i += nt) dst[i] = src[i];
+    }
+}
+
+void copy_bytes(Launch& L, void* dst, const void* src, int64_t bytes) {
+    if (bytes <= 0) return;
+    const int grid = (int)std::min<int64_t>((bytes / 16 + 255) / 256 + 1, (int64_t)L.num_sms * 8);
+    L.begin("copy_bytes", L.stream);
+    k_copy_bytes<<<grid, 256, 0, L.stream>>>((char*)dst, (const char*)src, bytes);
+    L.end(L.stream);
+}
+
+void init_status(Launch& L, DevStatus* st, const StatusCarry* carry) {
     L.begin("init_status", L.stream);
-    k_init_status<<<1, 32, 0, L.stream>>>(st);
+    k_init_status<<<1, 32, 0, L.stream>>>(st, carry ? *carry : StatusCarry());
     L.end(L.stream);
 }
 
@@ -143,12 +208,12 @@ __global__ void __launch_bounds__(256) k_check_compress(int64_t n, int64_t k, co
                                                         const int32_t* __restrict__ bent, int do_comp,
                                                         int validate, int32_t* __restrict__ bc_len,
                                                         uint2* __restrict__ pairs, int4* __restrict__ bmeta,
-                                                        DevStatus* st, int lane_max) {
+                                                        DevStatus* st, int lane_max, int64_t row0) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     CompressFlags fl;
-    for (int64_t j0 = gw * 32; j0 < n; j0 += nw * 32) {
+    for (int64_t j0 = row0 + gw * 32; j0 < n; j0 += nw * 32) {
         const int64_t j = j0 + lane;
         bool long_row = false;
         if (j < n) {
@@ -216,10 +281,10 @@ static int grid_for(int64_t warps_needed, int threads, int num_sms, int per_sm =
 }
 
 void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_comp, bool validate,
-                    int32_t* bc_len, uint2* pairs, int4* bmeta, DevStatus* st) {
-    if (B.nrows == 0) return;
+                    int32_t* bc_len, uint2* pairs, int4* bmeta, DevStatus* st, int64_t row0) {
+    if (B.nrows <= row0) return;
     const int threads = 256;
-    const int grid = grid_for((B.nrows + 31) / 32, threads, L.num_sms, 16);
+    const int grid = grid_for((B.nrows - row0 + 31) / 32, threads, L.num_sms, 16);
     // rows longer than lane_max are walked by the whole warp (coalesced, segmented OR scan);
     // shorter ones by one lane each (64 measured fastest on C2: 0.174 vs 0.250 ms at 32)
     const int lane_max = LANE_ROW_MAX;
@@ -227,11 +292,11 @@ void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_
     if (off64)
         k_check_compress<int64_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int64_t*)B.row_map, B.entries,
                                                                   do_comp, validate, bc_len, pairs, bmeta, st,
-                                                                  lane_max);
+                                                                  lane_max, row0);
     else
         k_check_compress<int32_t><<<grid, threads, 0, L.stream>>>(B.nrows, k, (const int32_t*)B.row_map, B.entries,
                                                                   do_comp, validate, bc_len, pairs, bmeta, st,
-                                                                  lane_max);
+                                                                  lane_max, row0);
     L.end(L.stream);
 }
 
@@ -721,7 +786,7 @@ __global__ void __launch_bounds__(256) k_check_diag(int64_t m, const OffT* __res
 }
 
 bool check_diagonal(Launch& L, bool off64, int64_t m, const void* row_map, const int32_t* entries, int* scratch,
-                    int* missing) {
+                    int* missing, int* missing_map) {
     *missing = 0;
     if (m == 0) return true;
     cudaMemsetAsync(scratch, 0, sizeof(int), L.stream);
@@ -732,8 +797,13 @@ bool check_diagonal(Launch& L, bool off64, int64_t m, const void* row_map, const
     else
         k_check_diag<int32_t><<<grid, 256, 0, L.stream>>>(m, (const int32_t*)row_map, entries, scratch);
     L.end(L.stream);
-    cudaMemcpyAsync(missing, scratch, sizeof(int), cudaMemcpyDeviceToHost, L.stream);
-    return cudaStreamSynchronize(L.stream) == cudaSuccess;
+    const void* src = scratch;
+    void* dst = missing_map;
+    const size_t nb = sizeof(int);
+    post_words(L, 1, &dst, &src, &nb);
+    if (cudaStreamSynchronize(L.stream) != cudaSuccess) return false;
+    *missing = *(volatile int*)missing;
+    return true;
 }
 
 }  // namespace kk

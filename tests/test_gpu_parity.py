@@ -400,10 +400,45 @@ def test_multiply_host_blocks(oracle_mod, blocks, ot):
         C = h.multiply_host(host(A), host(B), blocks=blocks)
         got = (C.row_map.numpy().astype(np.int64), C.entries.numpy().copy(), C.values.numpy().copy())
         assert_parity(oracle_mod, A, B, got)
+    # A*A from ONE host matrix (A's row blocks copied from B's device copy), first block a
+    # quarter of the others (blocks >= 4), values changed between calls
+    Ah = host(A)
+    for trial in range(2):
+        if trial:
+            Ah.values.mul_(-0.5)
+        C = h.multiply_host(Ah, Ah, blocks=blocks)
+        Ad = g.CSR(A.nrows, A.ncols, Ah.row_map.to(torch.int64), Ah.entries, Ah.values.clone())
+        got = (C.row_map.numpy().astype(np.int64), C.entries.numpy().copy(), C.values.numpy().copy())
+        assert_parity(oracle_mod, Ad, Ad, got)
     # a row block count above the row count, and an empty A
     E = g.random_csr(0, B.nrows, 3, seed=1)
     C = h.multiply_host(host(E), host(B), blocks=4)
     assert C.row_map.numel() == 1 and int(C.row_map[0]) == 0 and C.entries.numel() == 0
+    h.close()
+
+
+@pytest.mark.parametrize("square", [True, False])
+def test_multiply_host_planned(oracle_mod, square, monkeypatch):
+    """Host-buffer path with the block plan (A of >= 65,536 rows, no block count): a small first
+    block, the rest planned from its output size (a small KK_HOST_BLOCK_BYTES forces many
+    blocks, several B chunks per block and slot reuse); A*A from one host matrix and A*B from
+    two; C equals the oracle."""
+    from paper_2103_11991_b200 import CsrMatrix, SpGEMM
+
+    monkeypatch.setenv("KK_HOST_BLOCK_BYTES", "1500000")
+    A = g.laplacian_3d_27pt(41, values="random", seed=3)  # 68,921 rows
+
+    def host(M):
+        return CsrMatrix(M.nrows, M.ncols, M.row_map.to(torch.int32).pin_memory(), M.entries.pin_memory(),
+                         M.values.pin_memory())
+
+    Ah = host(A)
+    Bh = Ah if square else host(A)
+    h = SpGEMM()
+    for _ in range(2):
+        C = h.multiply_host(Ah, Bh)
+        got = (C.row_map.numpy().astype(np.int64), C.entries.numpy().copy(), C.values.numpy().copy())
+        assert_parity(oracle_mod, A, A, got)
     h.close()
 
 
