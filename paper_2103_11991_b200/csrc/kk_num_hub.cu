@@ -52,6 +52,19 @@ __device__ __forceinline__ void st_keep(float* a, float v, unsigned long long po
 }
 constexpr int HUB_WARPS = HUB_THREADS / 32;
 
+// rank of column c in the row's bit vector: the prefix of its 4-word group plus the bits
+// before it in the group (word loads as needed; one 16-byte load of the group measured
+// slower on C4: num_hub 262 vs 253 ms)
+__device__ __forceinline__ uint32_t hub_rank(const uint32_t* bm, const uint32_t* gp, int c) {
+    const int w = c >> 5;
+    uint32_t rk = gp[w >> 2];
+    const int gw = w & ~3;
+    if (gw + 0 < w) rk += __popc(bm[gw + 0]);
+    if (gw + 1 < w) rk += __popc(bm[gw + 1]);
+    if (gw + 2 < w) rk += __popc(bm[gw + 2]);
+    return rk + __popc(bm[w] & ((1u << (c & 31)) - 1u));
+}
+
 __host__ __device__ constexpr int64_t hub_words(int64_t k) { return ((k + 127) / 128) * 4; }  // multiple of 4
 constexpr int HUB_LONG = 256;  // B rows longer than this are walked by the whole CTA
 constexpr int HUB_LIST = 1024; // capacity of the per-row list of such A entries
@@ -196,7 +209,8 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
                                                              ValT* __restrict__ cval, const int32_t* __restrict__ perm,
                                                              const int* __restrict__ bin_start, int bin, int64_t k,
                                                              int vcap, int big, int det,
-                                                             const ValT* __restrict__ dinv, double omega) {
+                                                             const ValT* __restrict__ dinv, double omega,
+                                                             int* __restrict__ row_ctr) {
     extern __shared__ __align__(16) uint32_t sm_hub[];
     const int64_t NW = hub_words(k);
     uint32_t* bm = sm_hub;
@@ -210,13 +224,26 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
     if (r0 + (int)blockIdx.x >= r1) return;
     const int64_t per = (NW / 4 + HUB_WARPS - 1) / HUB_WARPS * 4;  // words per warp (multiple of 4)
     const unsigned long long keep = l2_keep_policy();
-    for (int r = r0 + blockIdx.x; r < r1; r += gridDim.x) {
+    // rows handed out by a device counter (row_ctr) or round robin: they differ by two orders
+    // of magnitude in work
+    __shared__ int s_row;
+    auto next_row = [&](int r) {
+        if (!row_ctr) return r + (int)gridDim.x;
+        __syncthreads();
+        if (threadIdx.x == 0) s_row = r0 + (int)gridDim.x + atomicAdd(row_ctr, 1);
+        __syncthreads();
+        return s_row;
+    };
+    for (int r = r0 + blockIdx.x; r < r1;) {
         const int i = perm[r];
         const int64_t s = ld(arm, i), e = ld(arm, i + 1);
         const int64_t cb = ld(crm, i);
         const int64_t clen = ld(crm, i + 1) - cb;
         const bool inshared = clen <= (int64_t)vcap;
-        if (!inshared && big) continue;  // the cluster tier's row
+        if (!inshared && big) {  // the cluster tier's row
+            r = next_row(r);
+            continue;
+        }
         for (int64_t t = threadIdx.x; t < NW / 4; t += HUB_THREADS) ((uint4*)bm)[t] = make_uint4(0, 0, 0, 0);
         if (threadIdx.x == 0) nlist[0] = nlist[1] = nlist[2] = nlist[3] = 0;
         __syncthreads();
@@ -273,13 +300,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
         __syncthreads();
         // (3) values: rank lookup, accumulation at the rank
         hub_walk<true>(s, e, aent, aval, brm, bent, bval, list, nlist, [&](int c, ValT prod) {
-            const int w = c >> 5;
-            uint32_t rk = gp[w >> 2];
-            const int gw = w & ~3;
-            if (gw + 0 < w) rk += __popc(bm[gw + 0]);
-            if (gw + 1 < w) rk += __popc(bm[gw + 1]);
-            if (gw + 2 < w) rk += __popc(bm[gw + 2]);
-            rk += __popc(bm[w] & ((1u << (c & 31)) - 1u));
+            const uint32_t rk = hub_rank(bm, gp, c);
             if ((int64_t)rk < clen) {
                 if (det) {
                     if (inshared)
@@ -308,13 +329,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
             for (int64_t q = bs + threadIdx.x; q < be; q += HUB_THREADS) {
                 const int c = __ldg(bent + q);
                 if (c < 0 || (int64_t)c >= k || !((bm[c >> 5] >> (c & 31)) & 1u)) continue;
-                const int w = c >> 5;
-                uint32_t rk = gp[w >> 2];
-                const int gw = w & ~3;
-                if (gw + 0 < w) rk += __popc(bm[gw + 0]);
-                if (gw + 1 < w) rk += __popc(bm[gw + 1]);
-                if (gw + 2 < w) rk += __popc(bm[gw + 2]);
-                rk += __popc(bm[w] & ((1u << (c & 31)) - 1u));
+                const uint32_t rk = hub_rank(bm, gp, c);
                 if ((int64_t)rk >= clen) continue;
                 const ValT b = __ldg(bval + q);
                 if (det) {  // strictly increasing B(i,:): distinct ranks
@@ -334,6 +349,7 @@ __global__ void __launch_bounds__(HUB_THREADS, 1) k_num_hub(const OffT* __restri
             for (int64_t t = threadIdx.x; t < clen; t += HUB_THREADS) __stcs(cval + cb + t, svals[t]);
             __syncthreads();
         }
+        r = next_row(r);
     }
 }
 
@@ -628,12 +644,16 @@ static bool hub_bins_t(Launch& L, const NumArgs& a, cudaStream_t s) {
         auto kern = k_num_hub<OffT, ValT>;
         KCfg c = kernel_cfg(kern, HUB_THREADS, hsm_v, L.num_sms);
         const int grid = (int)std::min<int64_t>(drows, c.grid_cap);
+        // rows from a device counter (C4: num_hub 270 -> 245 ms against round robin); the
+        // cluster tier uses the counter itself
+        int* rc = !cluster && a.work_ctr ? a.work_ctr : nullptr;
+        if (rc) cudaMemsetAsync(rc, 0, sizeof(int), s);
         L.begin("num_hub", s);
         kern<<<grid, HUB_THREADS, hsm_v, s>>>((const OffT*)a.A.row_map, a.A.entries, (const ValT*)a.A.values,
                                               (const OffT*)a.B.row_map, a.B.entries, (const ValT*)a.B.values,
                                               (const OffT*)a.c_row_map, a.c_entries, (ValT*)a.c_values, a.perm,
                                               a.bin_start, NUM_DENSE_BIN, a.k, vcap, cluster ? 1 : 0,
-                                              a.det ? 1 : 0, (const ValT*)a.dinv, a.omega);
+                                              a.det ? 1 : 0, (const ValT*)a.dinv, a.omega, rc);
         L.end(s);
     }
     if (cluster) {
