@@ -30,10 +30,10 @@ timeout 900 ncu --set full --clock-control none --kernel-name-base demangled -k 
     -o /tmp/prof_hub_$TAG -f python bench.py --config C4 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/ncu_hub_$TAG.log 2>&1; echo "ncu hub rc=$?"
 ncu -i /tmp/prof_hub_$TAG.ncu-rep --page raw --csv > $OUT/raw_hub_$TAG.csv 2>/dev/null
 # the C4 side-stream strict tier and the C5 wide-pattern rank tier (one launch each)
-timeout 900 ncu --set full --clock-control none --kernel-name-base demangled -k regex:"k_num_strict<int, double, \(int\)1024" -s 0 -c 1 \
+timeout 900 ncu --set full --clock-control none --kernel-name-base demangled -k regex:"k_num_strict<long, double, \(int\)1024" -s 0 -c 1 \
     -o /tmp/prof_strict_$TAG -f python bench.py --config C4 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/ncu_strict_$TAG.log 2>&1; echo "ncu strict rc=$?"
 ncu -i /tmp/prof_strict_$TAG.ncu-rep --page raw --csv > $OUT/raw_strict_$TAG.csv 2>/dev/null
-timeout 1200 ncu --set full --clock-control none --kernel-name-base demangled -k regex:"k_num_rank<int, double, \(int\)512" -s 0 -c 1 \
+timeout 1200 ncu --set full --clock-control none --kernel-name-base demangled -k regex:"k_num_rank<long, double, \(int\)512" -s 0 -c 1 \
     -o /tmp/prof_rankh_$TAG -f python bench.py --config C5 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $OUT/ncu_rankh_$TAG.log 2>&1; echo "ncu rank_hash rc=$?"
 ncu -i /tmp/prof_rankh_$TAG.ncu-rep --page raw --csv > $OUT/raw_rankh_$TAG.csv 2>/dev/null
 ls -la $OUT | tail -30
