@@ -113,12 +113,12 @@ struct kk_spgemm_handle_s {
     long long launches = 0;
     // workspace
     Buf flops, fscan, binid, perm_sym, perm_num, counts, binscratch, binstart, bc_len, pairs, cursors, partial,
-        status, bmeta, wlo, pat, pat_off, pat_len, diagchk, apos, bpos, spdup, spflag, status_aux, workctr;
+        status, bmeta, wlo, pat, pat_off, pat_len, diagchk, apos, bpos, spdup, spflag, status_aux, workctr, retry;
     // every workspace buffer, for destroy and stats (one list, so neither can miss one)
-    Buf* all_bufs[25] = {&flops,   &fscan,   &binid,   &perm_sym, &perm_num, &counts, &binscratch, &binstart,
+    Buf* all_bufs[26] = {&flops,   &fscan,   &binid,   &perm_sym, &perm_num, &counts, &binscratch, &binstart,
                          &bc_len,  &pairs,   &cursors, &partial,  &status,   &bmeta,  &wlo,        &pat,
                          &pat_off, &pat_len, &diagchk, &apos,     &bpos,     &spdup,  &spflag,     &status_aux,
-                         &workctr};
+                         &workctr, &retry};
     // B_C of a B prefix kept between the blocks of kk_spgemm_multiply_host (armed only there)
     struct BcCarry {
         bool armed = false, valid = false;
@@ -622,6 +622,8 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     sa.pat.len = keep_pat ? (int*)h->pat_len.p : nullptr;
     sa.st = dst;
     sa.comp_mode = comp_mode;
+    if ((st = ensure(h, h->retry, (size_t)(m + 8) * 4, s)) != KK_OK) return st;
+    sa.retry = (int*)h->retry.p;
     sa.logG = pick_logG(n > 0 ? (double)B->nnz / (double)n / (comp_mode != 0 ? 2.0 : 1.0) : 1.0);
     cudaStream_t side = nullptr;
     if (h->side) {

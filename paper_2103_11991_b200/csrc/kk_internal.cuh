@@ -15,13 +15,14 @@ constexpr uint32_t EMPTY = 0xffffffffu;      // empty hash slot (column indices 
 //   slots (ub <= S); 8: CTA-owned dense bit-vector window.
 constexpr int SYM_WARP_BINS = 7;
 constexpr int SYM_DENSE_BIN = 8;
-// 9..13: warp-owned dense bit vector over the row's column window [wlo, wlo + W) with
-// W = 8K, 16K, 32K, 48K, 64K bits (sorted B only; the window comes from the first/last
-// column of each B row, "bit vector for symbolic")
+// 9..15: warp-owned dense bit vector over the row's column window [wlo, wlo + W) with
+// W = 8K, 16K, 32K, 48K, 64K, 128K, 192K bits (sorted B only; the window comes from the
+// first/last column of each B row, "bit vector for symbolic")
 constexpr int SYM_WIN_BIN0 = 9;
-// 14: tiny rows (flops_i <= TINY_MAX): a lane owns a row, its columns in registers
-constexpr int SYM_TINY_BIN = 14;
-constexpr int SYM_NBINS = 15;
+constexpr int SYM_WIN_NBINS = 7;
+// 16: tiny rows (flops_i <= TINY_MAX): a lane owns a row, its columns in registers
+constexpr int SYM_TINY_BIN = 16;
+constexpr int SYM_NBINS = 17;
 constexpr int TINY_MAX = 16;
 // Numeric bins (by exact nnz(C_i)):
 //   0: empty; b = 1..5: warp-owned shared hash with S = 32 << b slots (nnz <= S/2);
@@ -148,6 +149,7 @@ struct SymArgs {
     const DevStatus* st;
     int logG;
     int comp_mode;          // opts.compression: 1 on, 0 off, -1 decided on the device (a1)
+    int* retry = nullptr;   // device int[m + 8]: per-bin lists of rows the speculative small tables gave up on
 };
 void symbolic_bins(Launch& L, const SymArgs& a, cudaStream_t dense_stream);
 

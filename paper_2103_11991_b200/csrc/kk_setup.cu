@@ -318,18 +318,15 @@ __device__ __forceinline__ int sym_bin_of(int64_t ub) {
 }
 
 // window bin for a row whose columns lie in [lo, hi] (sorted B), or 0: the smallest
-// W in {8K, 16K, 32K, 48K, 64K} bits covering [lo & ~31, hi], used when clearing the window
-// (W/32 words) costs at most ~16 words per bound insert and the row is not tiny.
+// W in {8K, 16K, 32K, 48K, 64K, 128K, 192K} bits covering [lo & ~31, hi], used when clearing
+// the window (W/32 words) costs at most ~16 words per bound insert and the row is not tiny.
 __device__ __forceinline__ int sym_win_bin_of(int lo, int hi, int64_t ub) {
     if (hi < lo || ub <= 32) return 0;
     const int64_t span = (int64_t)hi - (int64_t)(lo & ~31) + 1;
+    constexpr int64_t Ws[SYM_WIN_NBINS] = {8192, 16384, 32768, 49152, 65536, 131072, 196608};
     int c = 0;
-    int64_t W = 8192;
-    while (W < span && c < 4) {
-        W = (c == 2) ? 49152 : (c == 3 ? 65536 : W * 2);
-        ++c;
-    }
-    if (span > W || W / 32 > 16 * ub) return 0;
+    while (c < SYM_WIN_NBINS - 1 && Ws[c] < span) ++c;
+    if (span > Ws[c] || Ws[c] / 32 > 16 * ub) return 0;
     return SYM_WIN_BIN0 + c;
 }
 

@@ -854,8 +854,13 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
                                               const int32_t* __restrict__ bc_len, const uint2* __restrict__ pairs,
                                               const int32_t* __restrict__ perm, const int* __restrict__ bin_start,
                                               int bin, const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
-                                              PatOut po, DevStatus* st, int pblk, int atom) {
+                                              PatOut po, DevStatus* st, int pblk, int atom, int* retry) {
     constexpr bool HT = S > 0;
+    // speculative HT (retry != null): a small table for rows whose bound ub overstates their
+    // distinct words; a row that finds more than S/2 words is abandoned (its remaining steps
+    // skipped) and appended to retry[2..] (count in retry[1]) for a full-size table
+    const bool spec = HT && retry != nullptr;
+    bool over = false;
     constexpr int NW = HT ? 2 * S : W / 32;   // bitmap words, or keys[S] | masks[S]
     constexpr int WB = NW + 64 + PAT_WORDS;  // words per warp: bitmap | rec[32] (int2) | list
     extern __shared__ __align__(16) uint32_t sm_rows[];
@@ -915,6 +920,7 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
                 if (pos < PAT_WORDS) wl[pos] = tag;
             }
             nt += __popc(fb);
+            if (spec) over = nt > S / 2;  // warp-uniform; at most S/2 + 32 slots taken
         };
         // OR m into word w for the lanes with act (warp-collective: HT claims slots); returns
         // the old mask, tag = bit-vector index or slot.  PLAIN: the active lanes' words are
@@ -936,7 +942,7 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
             }
             return atomicOr(cell, m);
         };
-        for (int64_t a0 = s; a0 < e; a0 += 32) {
+        for (int64_t a0 = s; a0 < e && !over; a0 += 32) {
             const int na = (int)min((int64_t)32, e - a0);
             int bb = 0, bl = 0;
             if (lane < na) {
@@ -966,7 +972,7 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
                 uint2 p;
                 bool act;
                 fetch(0, p, act);
-                for (int t = 0; t < ntr; t += R) {
+                for (int t = 0; t < ntr && !over; t += R) {
                     uint2 pn;
                     bool actn;
                     fetch(t + R, pn, actn);
@@ -1028,7 +1034,7 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
                 uint2 p;
                 bool act;
                 fetch(0, p, act);
-                for (int f0 = 0; f0 < T; f0 += 32) {
+                for (int f0 = 0; f0 < T && !over; f0 += 32) {
                     uint2 pn = p;
                     bool actn = false;
                     if (f0 + 32 < T) fetch(f0 + 32, pn, actn);
@@ -1048,9 +1054,9 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
             else if (maxbl <= 32)
                 run(std::integral_constant<int, 1>{});
             else {
-                for (int t = 0; t < ntr; ++t) {
+                for (int t = 0; t < ntr && !over; ++t) {
                     const int2 rr = rec[t];
-                    for (int q0 = 0; q0 < rr.y; q0 += 32) {
+                    for (int q0 = 0; q0 < rr.y && !over; q0 += 32) {
                         const bool act = q0 + lane < rr.y;
                         const uint2 pq = pair_at(rr.x + min(q0 + lane, rr.y - 1));
                         uint32_t tag;
@@ -1064,9 +1070,17 @@ __device__ __forceinline__ void sym_rows_body(const OffT* __restrict__ arm, cons
         }
         jfirst = inext >= 0 && lane < en - sn ? __ldg(aent + sn + lane) : 0;
         cnt = warp_sum(cnt);
-        if (lane == 0) counts[i] = cnt;
+        if (over) {
+            // abandoned: to the retry list, table cleared
+            if (lane == 0) retry[2 + atomicAdd(&retry[1], 1)] = i;
+            clear_all();
+        } else if (lane == 0) {
+            counts[i] = cnt;
+        }
         __syncwarp();
-        if (nt <= PAT_WORDS) {
+        if (over) {
+            over = false;
+        } else if (nt <= PAT_WORDS) {
             // sorted pattern into the pool, clear the listed words
             long long off = -1;
             if (po.pat) {
@@ -1155,13 +1169,13 @@ __global__ void __launch_bounds__(256, S == 0 ? 4 : 1) k_sym_rows(const OffT* __
                                                   const uint2* __restrict__ pairs, const int32_t* __restrict__ perm,
                                                   const int* __restrict__ bin_start, int bin,
                                                   const int32_t* __restrict__ wlo, int32_t* __restrict__ counts,
-                                                  PatOut po, DevStatus* st, int pblk, int atom) {
+                                                  PatOut po, DevStatus* st, int pblk, int atom, int* retry) {
     if (st->use_comp)
         sym_rows_body<OffT, W, true, S>(arm, aent, brm, bent, bc_len, pairs, perm, bin_start, bin, wlo, counts, po, st,
-                                        pblk, atom);
+                                        pblk, atom, retry);
     else
         sym_rows_body<OffT, W, false, S>(arm, aent, brm, bent, bc_len, pairs, perm, bin_start, bin, wlo, counts, po,
-                                         st, pblk, atom);
+                                         st, pblk, atom, retry);
 }
 
 // KK_SYM_ROWS=0 selects k_sym_window for the window bins (experiments)
@@ -1173,13 +1187,19 @@ static bool use_sym_rows() {
     return v;
 }
 
+// KK_SYM_SPEC=0 disables the speculative small tables (experiments)
+static bool sym_spec() {
+    const char* s = getenv("KK_SYM_SPEC");
+    return !(s && s[0] == '0');
+}
+
 // Window rows take a step's B_C rows in one round of shared atomic ORs (C2 sym_rows 1.13
 // -> 1.04 ms against one plain read-OR-write round per row)
 static int sym_atom() { return 1; }
 
 template <typename OffT, int W>
 static void launch_sym_rows(Launch& L, const SymArgs& a, int bin) {
-    const int warps = 8;
+    const int warps = W <= 65536 ? 8 : 4;  // 128K/192K-bit windows: 16/24 KB per warp
     const size_t smem = (size_t)warps * ((size_t)W / 32 + 64 + PAT_WORDS) * 4;
     auto kern = k_sym_rows<OffT, W>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
@@ -1192,7 +1212,7 @@ static void launch_sym_rows(Launch& L, const SymArgs& a, int bin) {
     L.begin(kname("sym_rows", W), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
                                                a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
-                                               a.counts, a.pat, (DevStatus*)a.st, pblk, sym_atom());
+                                               a.counts, a.pat, (DevStatus*)a.st, pblk, sym_atom(), nullptr);
     L.end(L.stream);
 }
 
@@ -1254,22 +1274,25 @@ __global__ void __launch_bounds__(256, 1) k_sym_hash(const OffT* __restrict__ ar
     }
 }
 
+// retry: speculative launch (rows abandoned past S/2 words go to the list); list: the
+// retry list as the bin (perm = list + 2, bin_start = list, bin 0; row count unknown on the host)
 template <typename OffT, int S>
-static void launch_sym_rows_ht(Launch& L, const SymArgs& a, int bin) {
+static void launch_sym_rows_ht(Launch& L, const SymArgs& a, int bin, int* retry = nullptr, int* list = nullptr) {
     const int warps = S <= 1024 ? 8 : (S <= 2048 ? 4 : 2);
     const size_t smem = (size_t)warps * ((size_t)2 * S + 64 + PAT_WORDS) * 4;
     auto kern = k_sym_rows<OffT, 32, S>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
-    const int64_t hr = host_rows(a, bin);
+    const int64_t hr = host_rows(a, bin);  // list: at most the bin's rows come back
     if (hr == 0) return;
     int64_t need = ((hr > 0 ? hr : a.A.nrows) + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
     const int64_t share = a.pat.cap / ((int64_t)grid * warps);
     const int pblk = (int)std::max<int64_t>(PAT_WORDS, std::min<int64_t>(2048, share));
-    L.begin(kname("sym_rows_ht", S), L.stream);
+    L.begin(list ? kname("sym_rows_retry", S) : retry ? kname("sym_rows_spec", S) : kname("sym_rows_ht", S), L.stream);
     kern<<<grid, warps * 32, smem, L.stream>>>((const OffT*)a.A.row_map, a.A.entries, (const OffT*)a.B.row_map,
-                                               a.B.entries, a.bc_len, a.pairs, a.perm, a.bin_start, bin, a.wlo,
-                                               a.counts, a.pat, (DevStatus*)a.st, pblk, sym_atom());
+                                               a.B.entries, a.bc_len, a.pairs, list ? list + 2 : a.perm,
+                                               list ? list : a.bin_start, list ? 0 : bin, a.wlo, a.counts, a.pat,
+                                               (DevStatus*)a.st, pblk, sym_atom(), retry);
     L.end(L.stream);
 }
 
@@ -1348,12 +1371,37 @@ static void symbolic_bins_t(Launch& L, const SymArgs& a, cudaStream_t dense_stre
         L.end(s);
     }
     launch_sym_tiny<OffT>(L, a);
+    launch_sym_window<OffT, 196608>(L, a, SYM_WIN_BIN0 + 6);
+    launch_sym_window<OffT, 131072>(L, a, SYM_WIN_BIN0 + 5);
     launch_sym_window<OffT, 65536>(L, a, SYM_WIN_BIN0 + 4);
     launch_sym_window<OffT, 49152>(L, a, SYM_WIN_BIN0 + 3);
     launch_sym_window<OffT, 32768>(L, a, SYM_WIN_BIN0 + 2);
     launch_sym_window<OffT, 16384>(L, a, SYM_WIN_BIN0 + 1);
     launch_sym_window<OffT, 8192>(L, a, SYM_WIN_BIN0);
-    if (a.logG >= 3) {
+    if (a.logG >= 3 && a.retry && a.host_bin_start && a.B.nnz < INT32_MAX && use_sym_rows() && sym_spec()) {
+        // rows bound for the large tables (ub > 512 words) first try a 256-slot table: the
+        // bound (sum of their B_C rows' lengths) overstates the distinct words of rows whose
+        // B rows overlap (C5: ~40 words against ub ~1,000); rows past 128 words are redone
+        // with the largest table from the retry list
+        // per-bin retry lists (list b at retry + off_b: {0, count, rows...}), so a row that
+        // gives up is redone with its own bin's table
+        int64_t off[8] = {0};
+        int64_t o = 0;
+        for (int b = 4; b <= 7; ++b) {
+            off[b] = o;
+            o += (host_rows(a, b) > 0 ? host_rows(a, b) : 0) + 2;
+        }
+        cudaMemsetAsync(a.retry, 0, (size_t)o * sizeof(int), L.stream);
+        for (int b = 7; b >= 4; --b)
+            if (host_rows(a, b) != 0) launch_sym_rows_ht<OffT, 256>(L, a, b, a.retry + off[b]);
+        if (host_rows(a, 7) != 0) launch_sym_rows_ht<OffT, 8192>(L, a, 7, nullptr, a.retry + off[7]);
+        if (host_rows(a, 6) != 0) launch_sym_rows_ht<OffT, 4096>(L, a, 6, nullptr, a.retry + off[6]);
+        if (host_rows(a, 5) != 0) launch_sym_rows_ht<OffT, 2048>(L, a, 5, nullptr, a.retry + off[5]);
+        if (host_rows(a, 4) != 0) launch_sym_rows_ht<OffT, 1024>(L, a, 4, nullptr, a.retry + off[4]);
+        launch_sym_hash<OffT, 512>(L, a, 3);
+        launch_sym_hash<OffT, 256>(L, a, 2);
+        launch_sym_hash<OffT, 128>(L, a, 1);
+    } else if (a.logG >= 3) {
         // B rows of >= ~5 words on average: flattened-pair hash kernels (keep patterns)
         launch_sym_hash<OffT, 8192>(L, a, 7);
         launch_sym_hash<OffT, 4096>(L, a, 6);

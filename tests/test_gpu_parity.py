@@ -372,6 +372,50 @@ def test_window_and_pattern_paths(oracle_mod, band, per_a, per_b, vt):
         assert_parity(oracle_mod, A, B, got, value_dtype=vt)
 
 
+@pytest.mark.parametrize("band,binid", [(45000, 14), (75000, 15)])
+def test_wide_symbolic_windows(oracle_mod, band, binid):
+    """Rows whose columns span 64K-192K (C5's 3-dof stencil rows span ~155K): the symbolic
+    bit-vector windows of 128K and 192K bits (bins 14, 15) instead of the hash table."""
+    n, k = 3000, 600000
+    A = _banded(1200, n, 16, 40, seed=band)
+    B = _banded(n, k, 40, band, seed=band + 1)
+    for ot in (torch.int32, torch.int64):
+        got = gpu_spgemm(A, B, offset_dtype=ot)
+        assert_parity(oracle_mod, A, B, got)
+        assert got[3]["symbolic_bin_rows"][binid] > 0, got[3]["symbolic_bin_rows"]
+
+
+@pytest.mark.parametrize("ot", [torch.int32, torch.int64])
+def test_speculative_symbolic_tables(oracle_mod, ot):
+    """Rows bound for the large symbolic hash tables (ub > 512 words, columns spread past
+    the widest window) first run with a 256-slot table: rows whose B rows overlap (few
+    distinct words) finish there, rows with more than 128 distinct words are abandoned and
+    redone from the retry list with the 8192-slot table; C equals the oracle."""
+    rng = np.random.default_rng(31)
+    k, nb = 1_000_000, 400
+    base = np.sort(rng.choice(k, 30, replace=False))
+    b_rows = []
+    for j in range(nb):
+        if j < 200:  # near-identical rows: the shared 30 columns, two of them moved
+            r = base.copy()
+            r[rng.choice(30, 2, replace=False)] = rng.choice(k, 2, replace=False)
+            b_rows.append(np.unique(r))
+        else:
+            b_rows.append(np.sort(rng.choice(k, 30, replace=False)))
+    brm = np.cumsum([0] + [len(r) for r in b_rows])
+    B = g.CSR(nb, k, torch.tensor(brm), torch.tensor(np.concatenate(b_rows), dtype=torch.int32),
+              torch.tensor(rng.uniform(-1, 1, brm[-1])))
+    a_rows = [np.sort(rng.choice(200, 40, replace=False)) if i < 150 else
+              np.sort(200 + rng.choice(200, 40, replace=False)) for i in range(300)]
+    arm = np.cumsum([0] + [len(r) for r in a_rows])
+    A = g.CSR(300, nb, torch.tensor(arm), torch.tensor(np.concatenate(a_rows), dtype=torch.int32),
+              torch.tensor(rng.uniform(-1, 1, arm[-1])))
+    got = gpu_spgemm(A, B, offset_dtype=ot, timing=True)
+    assert_parity(oracle_mod, A, B, got)
+    names = " ".join(got[3]["kernels"])
+    assert "sym_rows_spec" in names and "sym_rows_retry" in names, names
+
+
 def test_pattern_pool_overflow(oracle_mod):
     """Rows of ~60 words each overflow the 48-pairs-per-row pattern pool: the rows that do
     not get a slot are computed by the hash kernels; the result is unchanged."""
