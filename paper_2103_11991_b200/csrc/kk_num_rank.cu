@@ -313,18 +313,7 @@ struct RankLayout {
     }
 };
 
-// ASYNC (experiment, KK_NUM_ASYNC=1): B's entries and values of the steps two ahead staged
-// into shared memory with cp.async (LDGSTS), four stages per warp, instead of register
-// prefetch through LDG/TEX
-constexpr uint32_t ASYNC_STAGE_BYTES = 4 * 32 * 12;
-__device__ __forceinline__ void cp_async(uint32_t dst, const void* src, int bytes) {
-    if (bytes == 8)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
-    else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
-
-template <typename OffT, typename ValT, int CAP, int MINB, bool HASHW, bool TEX = false, bool ASYNC = false>
+template <typename OffT, typename ValT, int CAP, int MINB, bool HASHW, bool TEX = false>
 __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__ arm, const int32_t* __restrict__ aent,
                                                         const ValT* __restrict__ aval, const OffT* __restrict__ brm,
                                                         const int32_t* __restrict__ bent, const ValT* __restrict__ bval,
@@ -465,43 +454,6 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                 int colA, colB;
                 ValT bA, bB, aA, aB;
                 bool vA, vB;
-                if constexpr (ASYNC) {
-                    const uint32_t o_stg = (uint32_t)warps * (uint32_t)LY::bytes + (uint32_t)warp * ASYNC_STAGE_BYTES;
-                    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sm_rank) + o_stg;
-                    auto issue = [&](int t) {
-                        const int4 rr = *(const int4*)(sm_rank + o_rec + (uint32_t)min(t, nt - 1) * 16u);
-                        const int q = rr.x + min(lane, rr.y - 1);
-                        const uint32_t st = (uint32_t)(t & 3);
-                        cp_async(sbase + st * 128u + (uint32_t)lane * 4u, bent + q, 4);
-                        cp_async(sbase + 512u + st * 256u + (uint32_t)lane * 8u, bval + q, (int)sizeof(ValT));
-                        asm volatile("cp.async.commit_group;" ::: "memory");
-                    };
-                    auto take = [&](int t, int& col, ValT& bv, ValT& a, bool& valid) {
-                        const int4 rr = *(const int4*)(sm_rank + o_rec + (uint32_t)min(t, nt - 1) * 16u);
-                        valid = t < nt && lane < rr.y;
-                        a = (ValT)__hiloint2double(rr.w, rr.z);
-                        const uint32_t st = (uint32_t)(t & 3);
-                        col = *(const int*)(sm_rank + o_stg + st * 128u + (uint32_t)lane * 4u);
-                        bv = *(const ValT*)(sm_rank + o_stg + 512u + st * 256u + (uint32_t)lane * 8u);
-                    };
-                    issue(0);
-                    issue(1);
-                    for (int t = 0; t < nt; t += 2) {
-                        issue(t + 2);
-                        issue(t + 3);
-                        asm volatile("cp.async.wait_group 2;" ::: "memory");
-                        take(t, colA, bA, aA, vA);
-                        take(t + 1, colB, bB, aB, vB);
-                        const uint32_t rA = slot_of(colA, vA), rB = slot_of(colB, vB);
-                        acc(rA, aA * bA);
-                        __syncwarp();
-                        acc(rB, aB * bB);
-                        __syncwarp();
-                    }
-                    asm volatile("cp.async.wait_all;" ::: "memory");
-                    __syncwarp();
-                    return;
-                }
                 load(0, colA, bA, aA, vA);
                 load(1, colB, bB, aB, vB);
                 for (int t = 0; t < nt; t += 2) {
@@ -624,15 +576,13 @@ static void launch_num_rank(Launch& L, const NumArgs& a, int bin) {
     const int rows = a.host_bin_start[bin + 1] - a.host_bin_start[bin];
     if (rows <= 0) return;
     const int warps = 8;
-    static const bool async = getenv("KK_NUM_ASYNC") && atoi(getenv("KK_NUM_ASYNC")) > 0;
-    const size_t smem = (size_t)warps * (RankLayout<ValT, CAP, HASHW>::bytes + (async ? ASYNC_STAGE_BYTES : 0));
+    const size_t smem = (size_t)warps * RankLayout<ValT, CAP, HASHW>::bytes;
     // B's entries and values through the texture pipe when the handle made texture objects
     // for them (C2: num_rank 1.97 -> 1.88 ms; the kernel is bound by the LSU's L1 data
     // wavefronts, and texture fetches are the TEX pipe's)
     const cudaTextureObject_t tb = a.tex_ent, tv = a.tex_val;
     const bool tex = tb != 0 && tv != 0;
-    auto kern = async ? k_num_rank<OffT, ValT, CAP, 4, HASHW, false, true>
-                : tex ? k_num_rank<OffT, ValT, CAP, 4, HASHW, true> : k_num_rank<OffT, ValT, CAP, 4, HASHW, false>;
+    auto kern = tex ? k_num_rank<OffT, ValT, CAP, 4, HASHW, true> : k_num_rank<OffT, ValT, CAP, 4, HASHW, false>;
     KCfg c = kernel_cfg(kern, warps * 32, smem, L.num_sms);
     int64_t need = (rows + warps - 1) / warps;
     int grid = (int)std::min<int64_t>(need, c.grid_cap);
