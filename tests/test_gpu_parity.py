@@ -486,6 +486,50 @@ def test_multiply_host_planned(oracle_mod, square, monkeypatch):
     h.close()
 
 
+def test_multiply_host_edges(oracle_mod, monkeypatch):
+    """Host-buffer path: int64 offsets and fp32 values with planned blocks; B with unsorted
+    rows (B_C off, the sortedness flags carried across the blocks' B prefixes); a column out of
+    range under validate fails with KK_ERR_INDEX_OVERFLOW mid-pipeline and the handle stays
+    usable."""
+    from paper_2103_11991_b200 import CsrMatrix, SpGEMM
+    from paper_2103_11991_b200._ffi import KKError
+
+    monkeypatch.setenv("KK_HOST_BLOCK_BYTES", "1000000")
+    A = g.laplacian_3d_27pt(41, values="random", seed=4)  # 68,921 rows
+
+    def host(M, ot=torch.int32, vt=torch.float64):
+        return CsrMatrix(M.nrows, M.ncols, M.row_map.to(ot).pin_memory(), M.entries.pin_memory(),
+                         M.values.to(vt).pin_memory())
+
+    h = SpGEMM(validate=True)
+    # int64 offsets, fp32 values
+    C = h.multiply_host(host(A, torch.int64, torch.float32), host(A, torch.int64, torch.float32))
+    got = (C.row_map.numpy().astype(np.int64), C.entries.numpy().copy(), C.values.numpy().copy())
+    assert_parity(oracle_mod, A, A, got, value_dtype=torch.float32)
+    # B with reversed rows (unsorted)
+    rm = A.row_map.numpy()
+    ent = A.entries.numpy().copy()
+    for r in range(0, A.nrows, 7):
+        ent[rm[r]:rm[r + 1]] = ent[rm[r]:rm[r + 1]][::-1].copy()
+    val = A.values.numpy().copy()
+    for r in range(0, A.nrows, 7):
+        val[rm[r]:rm[r + 1]] = val[rm[r]:rm[r + 1]][::-1].copy()
+    Bu = g.CSR(A.nrows, A.ncols, A.row_map, torch.tensor(ent), torch.tensor(val))
+    C = h.multiply_host(host(A), host(Bu))
+    got = (C.row_map.numpy().astype(np.int64), C.entries.numpy().copy(), C.values.numpy().copy())
+    assert_parity(oracle_mod, A, Bu, got)
+    # a bad column in the last rows of A
+    ent2 = A.entries.clone()
+    ent2[-3] = A.ncols + 5
+    Ab = g.CSR(A.nrows, A.ncols, A.row_map, ent2, A.values)
+    with pytest.raises(KKError, match="INDEX_OVERFLOW|out of range"):
+        h.multiply_host(host(Ab), host(A))
+    C = h.multiply_host(host(A), host(A))
+    got = (C.row_map.numpy().astype(np.int64), C.entries.numpy().copy(), C.values.numpy().copy())
+    assert_parity(oracle_mod, A, A, got)
+    h.close()
+
+
 @pytest.mark.parametrize("vt", [torch.float64, torch.float32])
 def test_wide_pattern_hashed_word_table(oracle_mod, vt):
     """Rows whose kept pattern (<= 64 words) spans more than the dense word index (2,048
