@@ -451,22 +451,58 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                     }
                     a = (ValT)__hiloint2double(rr.w, rr.z);
                 };
-                int colA, colB;
-                ValT bA, bB, aA, aB;
-                bool vA, vB;
-                load(0, colA, bA, aA, vA);
-                load(1, colB, bB, aB, vB);
-                for (int t = 0; t < nt; t += 2) {
-                    const uint32_t rA = slot_of(colA, vA), rB = slot_of(colB, vB);
-                    const ValT pA = aA * bA, pB = aB * bB;
-                    if (t + 2 < nt) {
-                        load(t + 2, colA, bA, aA, vA);
-                        load(t + 3, colB, bB, aB, vB);
+                if constexpr (!HASHW) {
+                    // one register set (the two-set form below spills here: 64 registers +
+                    // 8 bytes of stack, num_rank 1.88 -> 2.10 ms on C2; at 3 CTAs per SM without
+                    // the spill 2.15 ms)
+                    int colA, colB;
+                    ValT bA, bB, aA, aB;
+                    bool vA, vB;
+                    load(0, colA, bA, aA, vA);
+                    load(1, colB, bB, aB, vB);
+                    for (int t = 0; t < nt; t += 2) {
+                        const uint32_t rA = slot_of(colA, vA), rB = slot_of(colB, vB);
+                        const ValT pA = aA * bA, pB = aB * bB;
+                        if (t + 2 < nt) {
+                            load(t + 2, colA, bA, aA, vA);
+                            load(t + 3, colB, bB, aB, vB);
+                        }
+                        acc(rA, pA);
+                        __syncwarp();
+                        acc(rB, pB);
+                        __syncwarp();
+                    }
+                    return;
+                }
+                // two register sets: the steps two ahead load into the set not being consumed,
+                // so no loop-carried copy waits on the fetch it was just issued (with one set the
+                // compiler moves the fetched value at the end of every iteration, which stalls
+                // the iteration on the fetch: ncu, C2, 31 % of stall samples on that move;
+                // C5 num_rank_hash 224.5 -> 210.5 ms)
+                struct Step {
+                    int col;
+                    ValT b, a;
+                    bool v;
+                };
+                Step x0, y0, x1, y1;
+                load(0, x0.col, x0.b, x0.a, x0.v);
+                load(1, y0.col, y0.b, y0.a, y0.v);
+                auto half = [&](const Step& cA, const Step& cB, Step& nA, Step& nB, int tn) {
+                    const uint32_t rA = slot_of(cA.col, cA.v), rB = slot_of(cB.col, cB.v);
+                    const ValT pA = cA.a * cA.b, pB = cB.a * cB.b;
+                    if (tn < nt) {
+                        load(tn, nA.col, nA.b, nA.a, nA.v);
+                        load(tn + 1, nB.col, nB.b, nB.a, nB.v);
                     }
                     acc(rA, pA);
                     __syncwarp();
                     acc(rB, pB);
                     __syncwarp();
+                };
+                for (int t = 0; t < nt; t += 4) {
+                    half(x0, y0, x1, y1, t + 2);
+                    if (t + 2 >= nt) break;
+                    half(x1, y1, x0, y0, t + 4);
                 }
             };
             // (HASHW rows -- wide patterns, e.g. C5's 81-entry B rows -- always take the
