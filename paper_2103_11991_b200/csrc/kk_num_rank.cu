@@ -287,6 +287,9 @@ struct RankPrime<512> {
     static constexpr int M = 521;
 };
 constexpr uint32_t SLOT_MUL = 53;
+#ifndef KK_RANK_DEP
+#define KK_RANK_DEP 1
+#endif
 
 template <typename ValT, int CAP, bool HASHW = false>
 struct RankLayout {
@@ -464,8 +467,13 @@ __global__ void __launch_bounds__(256, MINB) k_num_rank(const OffT* __restrict__
                         const uint32_t rA = slot_of(colA, vA), rB = slot_of(colB, vB);
                         const ValT pA = aA * bA, pB = aB * bB;
                         if (t + 2 < nt) {
-                            load(t + 2, colA, bA, aA, vA);
-                            load(t + 3, colB, bB, aB, vB);
+                            // the next loads take the step index through an empty asm that
+                            // consumes the products: the multiplies are issued first, so the
+                            // fetches can target the registers they free
+                            int t2 = t + 2;
+                            if (KK_RANK_DEP) asm volatile("" : "+r"(t2) : "d"((double)pA), "d"((double)pB));
+                            load(t2, colA, bA, aA, vA);
+                            load(t2 + 1, colB, bB, aB, vB);
                         }
                         acc(rA, pA);
                         __syncwarp();
