@@ -945,6 +945,15 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
         cuts.push_back(m);
     }
     auto nblocks = [&]() { return (int)cuts.size() - 1; };
+    // the caller's row map as device-writable mapped memory, when it is pinned
+    void* rm_dev = nullptr;
+    {
+        cudaPointerAttributes pa;
+        if (cudaPointerGetAttributes(&pa, c_row_map) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer != nullptr)
+            rm_dev = pa.devicePointer;
+        cudaGetLastError();
+    }
     if ((st = ensure(h, P.brm, (n + 1) * osz, s)) != KK_OK) return st;
     if ((st = ensure(h, P.bent, B->nnz * 4, s)) != KK_OK) return st;
     if ((st = ensure(h, P.bval, B->nnz * vsz, s)) != KK_OK) return st;
@@ -1161,9 +1170,12 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
             break;
         }
         {
-            // the block's row map shifted to global offsets on the device (no host pass)
+            // the block's row map shifted to global offsets on the device (no host pass); when
+            // the caller's row map is pinned (mapped) the kernel writes it there directly, one
+            // copy-engine transfer less per block (each costs ~45 us of DMA restart)
             kk::Launch L = make_launch(h, s);
-            kk::add_offset(L, osz == 8, (char*)P.crm[sl].p + osz, r1 - r0, nnz_off[q]);
+            kk::add_offset(L, osz == 8, (char*)P.crm[sl].p + osz, r1 - r0, nnz_off[q],
+                           rm_dev ? (char*)rm_dev + (r0 + 1) * osz : nullptr);
         }
         cudaEventRecord(ev_c[q], s);
         // host output capacity (grows on a larger product: earlier blocks are kept)
@@ -1177,8 +1189,9 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
         }
         cudaStreamWaitEvent(P.s_out, ev_c[q], 0);
         // rows r0+1..r1 of the global row map (entry r0 is the previous block's end)
-        cudaMemcpyAsync((char*)c_row_map + (r0 + 1) * osz, (const char*)P.crm[sl].p + osz, (r1 - r0) * osz,
-                        cudaMemcpyDeviceToHost, P.s_out);
+        if (!rm_dev)
+            cudaMemcpyAsync((char*)c_row_map + (r0 + 1) * osz, (const char*)P.crm[sl].p + osz, (r1 - r0) * osz,
+                            cudaMemcpyDeviceToHost, P.s_out);
         cudaMemcpyAsync((char*)P.h_cent + nnz_off[q] * 4, P.cent[sl].p, nnz * 4, cudaMemcpyDeviceToHost, P.s_out);
         cudaMemcpyAsync((char*)P.h_cval + nnz_off[q] * vsz, P.cval[sl].p, nnz * vsz, cudaMemcpyDeviceToHost,
                         P.s_out);

@@ -116,7 +116,8 @@ void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, in
 // *total_dst (device, may be null) receives the sum; *overflow set when out is
 // int32 and the sum exceeds INT32_MAX.  partial: >= scan_partial_len(m) int64.
 int64_t scan_partial_len(int64_t m);
-void add_offset(Launch& L, bool off64, void* p, int64_t n, int64_t delta);
+// out != null: out[0..n) = p[...] + delta instead (out may be mapped pinned host memory)
+void add_offset(Launch& L, bool off64, void* p, int64_t n, int64_t delta, void* out = nullptr);
 // device -> device copy on the SMs (keeps the copy engines free for the host transfers)
 void copy_bytes(Launch& L, void* dst, const void* src, int64_t bytes);
 // dst[i] = src[i] - base for i < n (offsets of the row map's type; dst may be src)

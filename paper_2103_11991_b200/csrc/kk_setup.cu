@@ -34,19 +34,24 @@ __global__ void k_init_status(DevStatus* st, StatusCarry c) {
 // p[0..n) += delta (the host-buffer product rebases a row block's row map to global offsets on
 // the device before copying it out)
 template <typename T>
-__global__ void __launch_bounds__(256) k_add_offset(T* __restrict__ p, int64_t n, T delta) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        p[i] += delta;
+__global__ void __launch_bounds__(256) k_add_offset(T* __restrict__ p, int64_t n, T delta, T* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = p[i] + delta;
+        if (out)
+            out[i] = v;
+        else
+            p[i] = v;
+    }
 }
 
-void add_offset(Launch& L, bool off64, void* p, int64_t n, int64_t delta) {
-    if (n <= 0 || delta == 0) return;
+void add_offset(Launch& L, bool off64, void* p, int64_t n, int64_t delta, void* out) {
+    if (n <= 0 || (delta == 0 && !out)) return;
     const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)L.num_sms * 8);
     L.begin("add_offset", L.stream);
     if (off64)
-        k_add_offset<int64_t><<<grid, 256, 0, L.stream>>>((int64_t*)p, n, (int64_t)delta);
+        k_add_offset<int64_t><<<grid, 256, 0, L.stream>>>((int64_t*)p, n, (int64_t)delta, (int64_t*)out);
     else
-        k_add_offset<int32_t><<<grid, 256, 0, L.stream>>>((int32_t*)p, n, (int32_t)delta);
+        k_add_offset<int32_t><<<grid, 256, 0, L.stream>>>((int32_t*)p, n, (int32_t)delta, (int32_t*)out);
     L.end(L.stream);
 }
 
