@@ -226,10 +226,12 @@ class SpGEMM:
     # -- end to end from host memory ------------------------------------------------------
     def multiply_host(self, A, B, stream=None, blocks: Optional[int] = None) -> "CsrMatrix":
         """C = A*B for CSR operands in (pinned) HOST memory, C returned in HOST memory, through
-        the C ABI's kk_spgemm_multiply_host (B copied once; A in `blocks` row blocks whose
-        copies in both PCIe directions overlap the kernels; the global row map assembled in
-        the library).  C's entries and values are the handle's pinned buffers: valid until
-        the next call on this handle (copy them to keep them)."""
+        the C ABI's kk_spgemm_multiply_host (B copied once in row chunks; A in row blocks whose
+        copies in both PCIe directions overlap the kernels -- `blocks` fixes their number, None
+        plans them from the first block's output; pass the same matrix twice for A*A and it
+        crosses PCIe once; the global row map assembled in the library).  C's entries and
+        values are the handle's pinned buffers: valid until the next call on this handle (copy
+        them to keep them)."""
         import numpy as np
 
         A, B = CsrMatrix.from_any(A), CsrMatrix.from_any(B)
