@@ -554,7 +554,6 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
         if ((st = ensure(h, h->pat, (size_t)pat_cap * 8, s)) != KK_OK) return st;
         if ((st = ensure(h, h->pat_off, (size_t)m * 8, s)) != KK_OK) return st;
         if ((st = ensure(h, h->pat_len, (size_t)m * 4, s)) != KK_OK) return st;
-        if (m > 0) cudaMemsetAsync(h->pat_off.p, 0xff, (size_t)m * 8, s);
     }
     if (comp_mode != 0) {
         if ((st = ensure(h, h->bc_len, (size_t)n * 4, s)) != KK_OK) return st;
@@ -586,7 +585,8 @@ kk_status_t kk_spgemm_symbolic(kk_spgemm_handle_t h, const kk_csr_t* A, const kk
     // a1: flops per row, symbolic bins
     kk::row_flops_bin(L, off64, Av, Bv, k, comp_mode, h->opts.validate != 0, (const int32_t*)h->bc_len.p,
                       (const int4*)h->bmeta.p, (int64_t*)h->flops.p,
-                      (uint8_t*)h->binid.p, (int32_t*)h->counts.p, (int32_t*)h->wlo.p, dst);
+                      (uint8_t*)h->binid.p, (int32_t*)h->counts.p, (int32_t*)h->wlo.p, dst,
+                      keep_pat ? (long long*)h->pat_off.p : nullptr);
     // a2: F = exclusive scan of flops (kept in the handle for flop-balanced partitioning)
     kk::exclusive_scan(L, true, h->flops.p, true, h->fscan.p, m, (int64_t*)h->partial.p, nullptr, nullptr);
     // a3: bin rows by symbolic work
@@ -1143,9 +1143,9 @@ extern "C" kk_status_t kk_spgemm_multiply_host(kk_spgemm_handle_t h, const kk_cs
             kk::Launch L = make_launch(h, s);
             const int64_t e0 = rmv(A->row_map, r0), e1 = rmv(A->row_map, r1);
             if (alias) {
-                kk::rebase_row_map(L, osz == 8, P.arm[sl].p, (const char*)P.brm.p + r0 * osz, r1 - r0 + 1, e0);
-                kk::copy_bytes(L, P.aent[sl].p, (const char*)P.bent.p + e0 * 4, (e1 - e0) * 4);
-                kk::copy_bytes(L, P.aval[sl].p, (const char*)P.bval.p + e0 * vsz, (e1 - e0) * vsz);
+                kk::copy_rows(L, osz == 8, P.arm[sl].p, (const char*)P.brm.p + r0 * osz, r1 - r0 + 1, e0,
+                              P.aent[sl].p, (const char*)P.bent.p + e0 * 4, (e1 - e0) * 4, P.aval[sl].p,
+                              (const char*)P.bval.p + e0 * vsz, (e1 - e0) * vsz);
             } else {
                 kk::rebase_row_map(L, osz == 8, P.arm[sl].p, P.arm[sl].p, r1 - r0 + 1, e0);
             }

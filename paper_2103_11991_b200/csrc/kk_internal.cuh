@@ -111,15 +111,16 @@ void check_compress(Launch& L, bool off64, const MatView& B, int64_t k, bool do_
 // column of the window of rows in window bins
 void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, int64_t k, int comp_mode,
                    bool validate, const int32_t* bc_len, const int4* bmeta, int64_t* flops, uint8_t* binid,
-                   int32_t* counts, int32_t* wlo, DevStatus* st);
+                   int32_t* counts, int32_t* wlo, DevStatus* st, long long* pat_off = nullptr);
 // exclusive scan of in[0..m) (int32 or int64) into out[0..m] (int32 or int64);
 // *total_dst (device, may be null) receives the sum; *overflow set when out is
 // int32 and the sum exceeds INT32_MAX.  partial: >= scan_partial_len(m) int64.
 int64_t scan_partial_len(int64_t m);
 // out != null: out[0..n) = p[...] + delta instead (out may be mapped pinned host memory)
 void add_offset(Launch& L, bool off64, void* p, int64_t n, int64_t delta, void* out = nullptr);
-// device -> device copy on the SMs (keeps the copy engines free for the host transfers)
-void copy_bytes(Launch& L, void* dst, const void* src, int64_t bytes);
+// one launch: rm_dst[0..nrm) = rm_src[...] - base, e_dst/v_dst = e_src/v_src (bytes)
+void copy_rows(Launch& L, bool off64, void* rm_dst, const void* rm_src, int64_t nrm, int64_t base, void* e_dst,
+               const void* e_src, int64_t e_bytes, void* v_dst, const void* v_src, int64_t v_bytes);
 // dst[i] = src[i] - base for i < n (offsets of the row map's type; dst may be src)
 void rebase_row_map(Launch& L, bool off64, void* dst, const void* src, int64_t n, int64_t base);
 void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out, int64_t m, int64_t* partial,

@@ -7,6 +7,8 @@
 #include "kk_device.cuh"
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 
 namespace kk {
 // ------------------------------------------------------------------------------------
@@ -99,24 +101,41 @@ void rebase_row_map(Launch& L, bool off64, void* dst, const void* src, int64_t n
     L.end(L.stream);
 }
 
-// dst[0..bytes) = src[0..bytes) on the SMs (16-byte words when both are aligned)
-__global__ void __launch_bounds__(256) k_copy_bytes(char* __restrict__ dst, const char* __restrict__ src,
-                                                    int64_t bytes) {
+// a row block of a matrix already on the device, in one launch: row map rebased by `base`,
+// entries and values copied (16-byte words when aligned)
+template <typename T>
+__global__ void __launch_bounds__(256) k_copy_rows(T* __restrict__ rm_dst, const T* __restrict__ rm_src, int64_t nrm,
+                                                   T base, char* __restrict__ e_dst, const char* __restrict__ e_src,
+                                                   int64_t e_bytes, char* __restrict__ v_dst,
+                                                   const char* __restrict__ v_src, int64_t v_bytes) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
-    if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
-        const int64_t n16 = bytes >> 4;
-        for (int64_t i = tid; i < n16; i += nt) ((int4*)dst)[i] = __ldg((const int4*)src + i);
-        for (int64_t i = (n16 << 4) + tid; i < bytes; i += nt) dst[i] = src[i];
-    } else {
-        for (int64_t i = tid; i < bytes; i += nt) dst[i] = src[i];
-    }
+    for (int64_t i = tid; i < nrm; i += nt) rm_dst[i] = rm_src[i] - base;
+    auto copy = [&](char* d, const char* sp, int64_t bytes) {
+        if ((((uintptr_t)d | (uintptr_t)sp) & 15) == 0) {
+            const int64_t n16 = bytes >> 4;
+            for (int64_t i = tid; i < n16; i += nt) ((int4*)d)[i] = __ldg((const int4*)sp + i);
+            for (int64_t i = (n16 << 4) + tid; i < bytes; i += nt) d[i] = sp[i];
+        } else {
+            for (int64_t i = tid; i < bytes; i += nt) d[i] = sp[i];
+        }
+    };
+    copy(e_dst, e_src, e_bytes);
+    copy(v_dst, v_src, v_bytes);
 }
 
-void copy_bytes(Launch& L, void* dst, const void* src, int64_t bytes) {
-    if (bytes <= 0) return;
-    const int grid = (int)std::min<int64_t>((bytes / 16 + 255) / 256 + 1, (int64_t)L.num_sms * 8);
-    L.begin("copy_bytes", L.stream);
-    k_copy_bytes<<<grid, 256, 0, L.stream>>>((char*)dst, (const char*)src, bytes);
+void copy_rows(Launch& L, bool off64, void* rm_dst, const void* rm_src, int64_t nrm, int64_t base, void* e_dst,
+               const void* e_src, int64_t e_bytes, void* v_dst, const void* v_src, int64_t v_bytes) {
+    const int64_t work = std::max<int64_t>(nrm, std::max(e_bytes, v_bytes) / 16);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)L.num_sms * 8));
+    L.begin("copy_rows", L.stream);
+    if (off64)
+        k_copy_rows<int64_t><<<grid, 256, 0, L.stream>>>((int64_t*)rm_dst, (const int64_t*)rm_src, nrm, (int64_t)base,
+                                                         (char*)e_dst, (const char*)e_src, e_bytes, (char*)v_dst,
+                                                         (const char*)v_src, v_bytes);
+    else
+        k_copy_rows<int32_t><<<grid, 256, 0, L.stream>>>((int32_t*)rm_dst, (const int32_t*)rm_src, nrm, (int32_t)base,
+                                                         (char*)e_dst, (const char*)e_src, e_bytes, (char*)v_dst,
+                                                         (const char*)v_src, v_bytes);
     L.end(L.stream);
 }
 
@@ -368,7 +387,7 @@ __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t
                                                    int validate, const int4* __restrict__ bmeta,
                                                    int64_t* __restrict__ flops, uint8_t* __restrict__ binid,
                                                    int32_t* __restrict__ counts, int32_t* __restrict__ wlo,
-                                                   DevStatus* st) {
+                                                   DevStatus* st, long long* __restrict__ pat_off) {
     bool comp = false;
     if (comp_mode == 1)
         comp = true;
@@ -439,6 +458,7 @@ __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t
                 }
             }
             binid[i] = (uint8_t)b;
+            if (pat_off) pat_off[i] = -1;  // no kept pattern yet (symbolic sets the kept ones)
             if (b == 0) counts[i] = 0;
             tot += (unsigned long long)acc.f;
         }
@@ -450,7 +470,7 @@ __global__ void __launch_bounds__(256) k_row_flops(int64_t m, int64_t n, int64_t
 
 void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, int64_t k, int comp_mode,
                    bool validate, const int32_t* bc_len, const int4* bmeta, int64_t* flops, uint8_t* binid,
-                   int32_t* counts, int32_t* wlo, DevStatus* st) {
+                   int32_t* counts, int32_t* wlo, DevStatus* st, long long* pat_off) {
     if (A.nrows == 0) return;
     const int threads = 256;
     const int grid = grid_for((A.nrows + 31) / 32, threads, L.num_sms, 16);
@@ -459,23 +479,30 @@ void row_flops_bin(Launch& L, bool off64, const MatView& A, const MatView& B, in
         k_row_flops<int64_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int64_t*)A.row_map,
                                                              A.entries, (const int64_t*)B.row_map, bc_len,
                                                              comp_mode, B.nnz, validate, bmeta, flops, binid, counts,
-                                                             wlo, st);
+                                                             wlo, st, pat_off);
     else
         k_row_flops<int32_t><<<grid, threads, 0, L.stream>>>(A.nrows, A.ncols, k, (const int32_t*)A.row_map,
                                                              A.entries, (const int32_t*)B.row_map, bc_len,
                                                              comp_mode, B.nnz, validate, bmeta, flops, binid, counts,
-                                                             wlo, st);
+                                                             wlo, st, pat_off);
     L.end(L.stream);
 }
 
 // ------------------------------------------------------------------------------------
-// a2 / a6: exclusive scan (reduce -> scan partials -> downsweep), int64 accumulation.
+// a2 / a6: exclusive scan in one pass (decoupled look-back), int64 accumulation.
+// Tiles of SCAN_TILE items; a persistent grid of resident CTAs takes tiles in increasing
+// order per CTA.  A tile publishes its aggregate, finds its exclusive prefix by walking back
+// over its predecessors' published aggregates / inclusive prefixes, publishes its inclusive
+// prefix and writes its outputs.  Flags carry a per-call epoch (no reset between calls).
+// Deadlock-free because every tile below t is owned by a resident CTA that takes its tiles
+// in increasing order (tile 0 never waits).
 // ------------------------------------------------------------------------------------
 constexpr int SCAN_THREADS = 512;
 constexpr int SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
-int64_t scan_partial_len(int64_t m) { return (m + SCAN_TILE - 1) / SCAN_TILE + 2; }
+// per tile: flag (epoch << 2 | state), aggregate, inclusive prefix
+int64_t scan_partial_len(int64_t m) { return 3 * ((m + SCAN_TILE - 1) / SCAN_TILE) + 4; }
 
 // block-wide exclusive scan of one int64 per thread; returns the block total
 __device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* excl) {
@@ -506,71 +533,97 @@ __device__ __forceinline__ int64_t block_exclusive_scan(int64_t v, int64_t* excl
     return total;
 }
 
-template <typename InT>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(int64_t m, const InT* __restrict__ in,
-                                                              int64_t* __restrict__ partial) {
-    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
-    int64_t s = 0;
-#pragma unroll
-    for (int t = 0; t < SCAN_ITEMS; ++t) {
-        const int64_t i = base + t * SCAN_THREADS + threadIdx.x;
-        if (i < m) s += (int64_t)in[i];
-    }
-    s = warp_sum(s);
-    __shared__ int64_t ws[SCAN_THREADS / 32];
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        int64_t v = threadIdx.x < SCAN_THREADS / 32 ? ws[threadIdx.x] : 0;
-        v = warp_sum(v);
-        if (threadIdx.x == 0) partial[blockIdx.x] = v;
-    }
-}
+constexpr long long SCAN_AGG = 1, SCAN_INCL = 2;
 
-__global__ void __launch_bounds__(1024) k_scan_partials(int64_t nb, int64_t* __restrict__ partial,
-                                                        unsigned long long* total_dst) {
-    int64_t carry = 0;
-    for (int64_t b0 = 0; b0 < nb; b0 += blockDim.x) {
-        const int64_t b = b0 + threadIdx.x;
-        const int64_t v = b < nb ? partial[b] : 0;
+template <typename InT, typename OutT>
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(int64_t m, const InT* __restrict__ in,
+                                                                OutT* __restrict__ out, long long* __restrict__ tiles,
+                                                                long long epoch, unsigned long long* total_dst,
+                                                                int* overflow) {
+    __shared__ long long s_prefix;
+    const int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
+    volatile long long* flag = tiles;  // tiles[3t], [3t+1] aggregate, [3t+2] inclusive prefix
+    for (int64_t t = blockIdx.x; t < nb; t += gridDim.x) {
+        const int64_t base = t * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+        int64_t v[SCAN_ITEMS];
+        int64_t sum = 0;
+#pragma unroll
+        for (int u = 0; u < SCAN_ITEMS; ++u) {
+            const int64_t i = base + u;
+            v[u] = i < m ? (int64_t)in[i] : 0;
+            sum += v[u];
+        }
         int64_t ex;
-        const int64_t tot = block_exclusive_scan(v, &ex);
-        if (b < nb) partial[b] = carry + ex;
-        carry += tot;
-    }
-    if (threadIdx.x == 0) {
-        partial[nb] = carry;
-        if (total_dst) *total_dst = (unsigned long long)carry;
+        const int64_t total = block_exclusive_scan(sum, &ex);
+        if (threadIdx.x < 32) {
+            // warp 0: publish the aggregate, then look back 32 predecessors at a time: wait
+            // until all of the window are published, take the nearest inclusive prefix in it
+            // (plus the aggregates after it), else all 32 aggregates and the next window
+            const int lane = threadIdx.x;
+            long long prefix = 0;
+            if (lane == 0) {
+                if (t == 0) {
+                    tiles[2] = total;
+                    __threadfence();
+                    flag[0] = (epoch << 2) | SCAN_INCL;
+                } else {
+                    tiles[3 * t + 1] = total;
+                    __threadfence();
+                    flag[3 * t] = (epoch << 2) | SCAN_AGG;
+                }
+            }
+            for (int64_t w = t - 1; w >= 0; w -= 32) {
+                const int64_t p = w - lane;  // lane 0: the nearest predecessor
+                long long f = 0;
+                if (p >= 0) {
+                    do {
+                        f = flag[3 * p];
+                    } while ((f >> 2) != epoch);
+                }
+                __threadfence();
+                const unsigned incl = __ballot_sync(FULL, p >= 0 && (f & 3) == SCAN_INCL);
+                const int stop = incl ? __ffs(incl) - 1 : 32;  // nearest lane holding an inclusive prefix
+                long long v = 0;
+                if (p >= 0 && lane < stop) v = ((volatile long long*)tiles)[3 * p + 1];
+                if (p >= 0 && lane == stop) v = ((volatile long long*)tiles)[3 * p + 2];
+                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+                prefix += v;
+                if (incl) break;
+            }
+            if (lane == 0) {
+                if (t > 0) {
+                    tiles[3 * t + 2] = prefix + total;
+                    __threadfence();
+                    flag[3 * t] = (epoch << 2) | SCAN_INCL;
+                }
+                s_prefix = prefix;
+            }
+        }
+        __syncthreads();
+        int64_t run = s_prefix + ex;
+#pragma unroll
+        for (int u = 0; u < SCAN_ITEMS; ++u) {
+            const int64_t i = base + u;
+            if (i < m) out[i] = (OutT)run;
+            run += v[u];
+        }
+        if (t == nb - 1 && threadIdx.x == 0) {
+            const int64_t all = s_prefix + total;
+            out[m] = (OutT)all;
+            if (total_dst) *total_dst = (unsigned long long)all;
+            if (sizeof(OutT) == 4 && all > (int64_t)INT_MAX && overflow) *overflow = 1;
+        }
+        __syncthreads();
     }
 }
 
 template <typename InT, typename OutT>
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_down(int64_t m, const InT* __restrict__ in,
-                                                            const int64_t* __restrict__ partial,
-                                                            OutT* __restrict__ out, int64_t nb, int* overflow) {
-    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
-    int64_t v[SCAN_ITEMS];
-    int64_t s = 0;
-#pragma unroll
-    for (int t = 0; t < SCAN_ITEMS; ++t) {
-        const int64_t i = base + t;
-        v[t] = i < m ? (int64_t)in[i] : 0;
-        s += v[t];
-    }
-    int64_t ex;
-    block_exclusive_scan(s, &ex);
-    int64_t run = partial[blockIdx.x] + ex;
-#pragma unroll
-    for (int t = 0; t < SCAN_ITEMS; ++t) {
-        const int64_t i = base + t;
-        if (i < m) out[i] = (OutT)run;
-        run += v[t];
-    }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-        const int64_t total = partial[nb];
-        out[m] = (OutT)total;
-        if (sizeof(OutT) == 4 && total > (int64_t)INT_MAX && overflow) *overflow = 1;
-    }
+static void scan_t(Launch& L, const void* in, void* out, int64_t m, int64_t nb, long long* tiles, long long epoch,
+                   unsigned long long* total_dst, int* overflow) {
+    auto kern = k_scan_lookback<InT, OutT>;
+    KCfg c = kernel_cfg(kern, SCAN_THREADS, 0, L.num_sms);
+    const int grid = (int)std::min<int64_t>(nb, c.grid_cap);
+    kern<<<grid, SCAN_THREADS, 0, L.stream>>>(m, (const InT*)in, (OutT*)out, tiles, epoch, total_dst, overflow);
 }
 
 void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out, int64_t m, int64_t* partial,
@@ -582,25 +635,27 @@ void exclusive_scan(Launch& L, bool in64, const void* in, bool out64, void* out,
         if (total_dst) cudaMemsetAsync(total_dst, 0, 8, L.stream);
         return;
     }
+    // a fresh epoch per call: flags left in the tile array by earlier calls never match; the
+    // epochs start at a salted 60-bit value so that stale data in a reused buffer cannot
+    // pass for a flag (flag = epoch << 2 | state)
+    static std::atomic<long long> g_epoch{(long long)(0x0A5A5A5A5A000000ull ^
+                                                      ((unsigned long long)(uintptr_t)&g_epoch << 12) ^
+                                                      (unsigned long long)std::chrono::steady_clock::now()
+                                                          .time_since_epoch()
+                                                          .count()) &
+                                          ((1ll << 60) - 1)};
+    const long long epoch = g_epoch.fetch_add(1) & ((1ll << 60) - 1);
+    long long* tiles = (long long*)partial;
     L.begin("exclusive_scan", L.stream);
-    if (in64)
-        k_scan_reduce<int64_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int64_t*)in, partial);
-    else
-        k_scan_reduce<int32_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int32_t*)in, partial);
-    k_scan_partials<<<1, 1024, 0, L.stream>>>(nb, partial, total_dst);
     if (in64 && out64)
-        k_scan_down<int64_t, int64_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int64_t*)in, partial,
-                                                                                  (int64_t*)out, nb, overflow);
+        scan_t<int64_t, int64_t>(L, in, out, m, nb, tiles, epoch, total_dst, overflow);
     else if (in64)
-        k_scan_down<int64_t, int32_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int64_t*)in, partial,
-                                                                                  (int32_t*)out, nb, overflow);
+        scan_t<int64_t, int32_t>(L, in, out, m, nb, tiles, epoch, total_dst, overflow);
     else if (out64)
-        k_scan_down<int32_t, int64_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int32_t*)in, partial,
-                                                                                  (int64_t*)out, nb, overflow);
+        scan_t<int32_t, int64_t>(L, in, out, m, nb, tiles, epoch, total_dst, overflow);
     else
-        k_scan_down<int32_t, int32_t><<<(unsigned)nb, SCAN_THREADS, 0, L.stream>>>(m, (const int32_t*)in, partial,
-                                                                                  (int32_t*)out, nb, overflow);
-    L.end(L.stream, 3);
+        scan_t<int32_t, int32_t>(L, in, out, m, nb, tiles, epoch, total_dst, overflow);
+    L.end(L.stream);
 }
 
 // ------------------------------------------------------------------------------------
