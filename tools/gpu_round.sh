@@ -14,6 +14,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG
 tail -2 $OUT/smoke_$TAG.log
 timeout 900 python bench.py --kernel-table > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"
 cat $OUT/bench_$TAG.json | cut -c1-400; head -12 $OUT/bench_$TAG.err
+# the host-buffer path's per-block timeline (KK_HOST_TRACE=1) of one C2 call
+KK_HOST_TRACE=1 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > /dev/null 2> $OUT/e2e_trace_$TAG.err
+grep "kk host" $OUT/e2e_trace_$TAG.err | tail -40 > $OUT/e2e_trace_$TAG.txt
 for C in C3 C3J C5 C4; do
   timeout 1200 python bench.py --config $C --steps 5 --warmup 3 --kernel-table --no-cpu-baseline > $OUT/bench_${C}_$TAG.json 2> $OUT/bench_${C}_$TAG.err
   echo "bench $C rc=$?"; cut -c1-300 $OUT/bench_${C}_$TAG.json; head -6 $OUT/bench_${C}_$TAG.err
